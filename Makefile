@@ -1,0 +1,30 @@
+# Builds the product library (sm_100a) and the CPU checkers.
+#   make            -> paper_2007_08501_b200/libdr_raster_b200.so + oracle/liboracle.so (+ oracle/_ref when
+#                      /root/reference is present)
+NVCC ?= nvcc
+ARCH = -gencode arch=compute_100a,code=sm_100a
+# -fmad=false: no FMA contraction anywhere in the kernels (bit-exact pix_to_face, SURVEY.md §7 hard part 1)
+NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v
+PKG = paper_2007_08501_b200
+SRCS = $(PKG)/csrc/raster_fwd.cu $(PKG)/csrc/raster_bwd.cu $(PKG)/csrc/capi.cu
+HDRS = $(PKG)/csrc/raster_math.cuh $(PKG)/csrc/raster_kernels.cuh include/dr_raster.h
+LIB = $(PKG)/libdr_raster_b200.so
+OBJS = $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
+
+all: $(LIB) oracle
+
+build/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+oracle:
+	$(MAKE) -C oracle liboracle.so
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; fi
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all oracle clean

@@ -1,0 +1,394 @@
+"""bench.py — rasterize_meshes forward+backward throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl b200|reference]
+
+One step = rasterize_meshes forward + rasterize_backward over the whole (rank-local) mesh batch, with inputs
+resident in HBM (``value``), and once more end to end through the public API with host buffers (``e2e``).
+Default workload: C4 = 64 rotated cubes (1k-200k faces, 6,581,760 total), 512x512, K=8, blur 1e-4,
+perspective_correct + cull_backfaces (BASELINE.json configs[3], the config the metric is quoted on at
+1/2/4/8 GPUs). Multi-GPU: torchrun, one rank per GPU; meshes are sharded by face count (LPT), no collective
+on the data path; the timed region is bracketed by barrier + synchronize and the max over ranks is reported.
+
+``--impl reference`` times the reference's own CPU implementation (oracle/_ref/libdr3d_ref.so, compiled from
+the unmodified reference sources; the oracle port if that library is absent) on a bounded sample of the same
+workload, with all host threads. The reference has no perspective_correct / cull_backfaces: it runs its only
+semantics on the same meshes.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2007_08501_b200 import scenes as S  # noqa: E402
+
+METRIC = "rasterize_meshes fwd+bwd Mfaces·px/s"
+UNIT = "Mfaces·px/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(S.CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-faces", type=float, default=0.06,
+                    help="fraction of the batch's faces the CPU sample covers")
+    return ap.parse_args()
+
+
+def lpt_shards(face_counts, world):
+    from paper_2007_08501_b200.shard import lpt_partition
+
+    return lpt_partition(face_counts, world)
+
+
+def config_settings(cfg):
+    from paper_2007_08501_b200 import RasterSettings
+
+    c = S.CONFIGS[cfg]
+    return RasterSettings(image_size=c["image"], faces_per_pixel=c["K"], blur_radius=c["blur"],
+                          bin_size=c["bin_size"], perspective_correct=c.get("perspective_correct", False),
+                          cull_backfaces=c.get("cull_backfaces", False), znear=0.1, clip_nonpositive_z=True)
+
+
+def face_px(meshes: S.Meshes, H, W):
+    return float(meshes.num_faces_per_mesh().sum()) * H * W
+
+
+def subset(meshes: S.Meshes, idx):
+    return S.Meshes([meshes.verts[i] for i in idx], [meshes.faces[i] for i in idx])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# -------------------------------------------------------------------------------------------------
+# CPU arms
+
+
+def cpu_reference_run(meshes: S.Meshes, cfg, steps=1, warmup=0):
+    """Reference CPU path (oracle/_ref) fwd+bwd on `meshes`; falls back to the oracle port."""
+    c = S.CONFIGS[cfg]
+    H = W = c["image"]
+    K, blur = c["K"], c["blur"]
+    cam = S.bench_camera()
+    ncores = os.cpu_count() or 1
+    try:
+        from oracle.oracle import RefLib
+
+        ref = RefLib()
+        ref.set_num_threads(ncores)
+        rb = ref.batch(meshes)
+        kind = "reference"
+
+        def step():
+            fr = ref.rasterize(rb, cam.packed(), H, W, K, blur, c["bin_size"])
+            if c["backward"]:
+                S_ = fr[0].size
+                g = np.random.default_rng(0)
+                ref.rasterize_backward(rb, cam.packed(), H, W, K, blur, fr, g.standard_normal(S_),
+                                       g.standard_normal(3 * S_), g.standard_normal(S_), c["bin_size"])
+    except (FileNotFoundError, OSError):
+        from oracle.oracle import Oracle, make_settings
+
+        orc = Oracle()
+        ncores = 1
+        kind = "port"
+        fv = S.face_verts(meshes, cam)
+        first, num = meshes.mesh_to_face_first_idx(), meshes.num_faces_per_mesh()
+        st = make_settings(H, W, K, blur, perspective_correct=int(c.get("perspective_correct", False)),
+                           cull_backfaces=int(c.get("cull_backfaces", False)))
+
+        def step():
+            fr = orc.forward(fv, first, num, st)
+            if c["backward"]:
+                S_ = fr[0].size
+                g = np.random.default_rng(0)
+                orc.backward(fv, first, num, st, fr[0], fr[2], g.standard_normal(S_), g.standard_normal(3 * S_),
+                             g.standard_normal(S_))
+    for _ in range(warmup):
+        step()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return face_px(meshes, H, W) / t / 1e6, t, kind, ncores
+
+
+def cpu_sample(meshes: S.Meshes, frac: float):
+    counts = meshes.num_faces_per_mesh()
+    target = frac * counts.sum()
+    idx, acc = [], 0
+    for i, c in enumerate(counts):
+        idx.append(i)
+        acc += c
+        if acc >= target:
+            break
+    return idx
+
+
+# -------------------------------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = args.config
+    c = S.CONFIGS[cfg]
+    H = W = c["image"]
+    meshes_all = S.config_meshes(cfg)
+    total_fpx = face_px(meshes_all, H, W)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        idx = cpu_sample(meshes_all, args.cpu_sample_faces)
+        sample = subset(meshes_all, idx)
+        v, t, kind, cores = cpu_reference_run(sample, cfg, steps=max(1, min(args.steps, 3)), warmup=0)
+        desc = (f"meshes 0..{len(idx) - 1} of {cfg} ({int(sample.num_faces_per_mesh().sum())} faces), fwd"
+                + ("+bwd" if c["backward"] else "") + ", reference semantics (no perspective_correct/cull)")
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
+                          "steps": max(1, min(args.steps, 3)), "warmup": 0, "ms_per_step": t * 1e3,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": cfg, "desc": c["desc"]},
+                          "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc},
+                          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+
+    from paper_2007_08501_b200 import (KernelTimer, launch_count, rasterize_meshes, rasterize_meshes_backward,
+                                       workspace_bytes)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    shards = lpt_shards(meshes_all.num_faces_per_mesh(), world)
+    my = subset(meshes_all, shards[rank])
+    cam = S.bench_camera()
+    rs = config_settings(cfg)
+    fv_np = S.face_verts(my, cam)
+    first_np, num_np = my.mesh_to_face_first_idx(), my.num_faces_per_mesh()
+    N, F = len(num_np), len(fv_np)
+    K = c["K"]
+    S_ = N * H * W * K
+    fv = torch.as_tensor(fv_np, device=dev)
+    first = torch.as_tensor(first_np, device=dev)
+    num = torch.as_tensor(num_np, device=dev)
+    ws = torch.empty(workspace_bytes(N, F, rs), dtype=torch.uint8, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    dz = torch.randn((N, H, W, K), generator=gen, device=dev)
+    db = torch.randn((N, H, W, K, 3), generator=gen, device=dev)
+    dd = torch.randn((N, H, W, K), generator=gen, device=dev)
+
+    def step():
+        p2f, zbuf, bary, dists = rasterize_meshes(fv, first, num, rs, workspace=ws)
+        grad = None
+        if c["backward"]:
+            grad = rasterize_meshes_backward(fv, first, num, rs, p2f, bary, dz, db, dd)
+        return p2f, grad
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = launch_count()
+    with ClockSampler(local) as clk, KernelTimer() as kt:
+        barrier()
+        e0.record(st)
+        for _ in range(args.steps):
+            step()
+        e1.record(st)
+        barrier()
+    launches = launch_count() - n_launch0
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = ms_local
+    if dist is not None:
+        t = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = total_fpx / (ms * 1e-3) / 1e6
+
+    # roofline of the dominant kernel (per-launch averages from the library's event timing)
+    shares = {}
+    for name in ("k_face_setup", "k_bin_faces", "k_fine", "k_backward"):
+        tot, n = kt.total(name)
+        if n:
+            shares[name] = (tot, n)
+    dom = max(shares, key=lambda k: shares[k][0])
+    dom_ms = shares[dom][0] / shares[dom][1]
+    if dom == "k_backward":
+        alg_bytes = 40 * S_ + 144 * F
+    elif dom == "k_fine":
+        alg_bytes = 72 * F + 16 * N + 28 * S_
+    else:
+        alg_bytes = 72 * F + 16 * F
+    peaks, peak_kind = measured_peaks()
+    achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
+    step_ms_sum = sum(v[0] for v in shares.values()) / args.steps
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom,
+                "kernel_ms": dom_ms, "kernel_share_of_step": shares[dom][0] / args.steps / max(step_ms_sum, 1e-9),
+                "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
+                "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in shares.items()}}
+
+    # end to end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h_fv = torch.from_numpy(fv_np).pin_memory()
+        h_dz = dz.cpu().pin_memory()
+        h_db = db.cpu().pin_memory()
+        h_dd = dd.cpu().pin_memory()
+        d_fv = torch.empty_like(fv)
+        d_dz, d_db, d_dd = torch.empty_like(dz), torch.empty_like(db), torch.empty_like(dd)
+        o_p2f = torch.empty((N, H, W, K), dtype=torch.int64).pin_memory()
+        o_z = torch.empty((N, H, W, K), dtype=torch.float32).pin_memory()
+        o_b = torch.empty((N, H, W, K, 3), dtype=torch.float32).pin_memory()
+        o_d = torch.empty((N, H, W, K), dtype=torch.float32).pin_memory()
+        o_g = torch.empty((F, 3, 3), dtype=torch.float64).pin_memory()
+        h2d = h_fv.numel() * 8 + (h_dz.numel() + h_db.numel() + h_dd.numel()) * 4 * bool(c["backward"])
+        d2h = S_ * 28 + (F * 72 if c["backward"] else 0)
+
+        def e2e_step():
+            d_fv.copy_(h_fv, non_blocking=True)
+            if c["backward"]:
+                d_dz.copy_(h_dz, non_blocking=True)
+                d_db.copy_(h_db, non_blocking=True)
+                d_dd.copy_(h_dd, non_blocking=True)
+            p2f, zbuf, bary, dists = rasterize_meshes(d_fv, first, num, rs, workspace=ws)
+            o_p2f.copy_(p2f, non_blocking=True)
+            o_z.copy_(zbuf, non_blocking=True)
+            o_b.copy_(bary, non_blocking=True)
+            o_d.copy_(dists, non_blocking=True)
+            if c["backward"]:
+                g = rasterize_meshes_backward(d_fv, first, num, rs, p2f, bary, d_dz, d_db, d_dd)
+                o_g.copy_(g, non_blocking=True)
+
+        e2e_steps = max(1, min(args.steps, 5))
+        e2e_step()
+        barrier()
+        e0.record(st)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(st)
+        barrier()
+        ems = e0.elapsed_time(e1) / e2e_steps
+        if dist is not None:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": total_fpx / (ems * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        idx = cpu_sample(meshes_all, args.cpu_sample_faces)
+        sample = subset(meshes_all, idx)
+        v, t, kind, cores = cpu_reference_run(sample, cfg, steps=1)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"meshes 0..{len(idx) - 1} of {cfg} ({int(sample.num_faces_per_mesh().sum())} faces), "
+                         f"fwd{'+bwd' if c['backward'] else ''}, {t:.2f} s, reference semantics"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": cfg, "desc": c["desc"], "meshes": len(meshes_all),
+                          "faces": int(meshes_all.num_faces_per_mesh().sum()), "image": H, "K": K,
+                          "blur_radius": c["blur"], "bin_size": c["bin_size"], "parallelism": f"mesh-shard{world}",
+                          "l2": "inputs+outputs (GBs) exceed the 126 MB L2; no flush"},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+               "clocks": clk.summary()}
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

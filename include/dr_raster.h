@@ -1,0 +1,137 @@
+/*
+ * dr_raster.h — C-ABI of the B200-native rasterize_meshes hot path (libdr_raster_b200.so).
+ *
+ * Replaces, on the north-star boundary (BASELINE.json):
+ *   dr::rasterize_meshes        /root/reference/proj/include/dr/mesh_raster.hpp:41  (src/mesh_raster.cpp:234-285)
+ *   dr::rasterize_meshes_naive  /root/reference/proj/include/dr/mesh_raster.hpp:44  (src/mesh_raster.cpp:214-232)
+ *   dr::rasterize_backward      /root/reference/proj/include/dr/mesh_raster.hpp:66-69 (src/mesh_raster.cpp:329-403)
+ *   dr::RasterSettings          /root/reference/proj/include/dr/mesh_raster.hpp:18-23
+ *   dr::MeshFragments           /root/reference/proj/include/dr/mesh_raster.hpp:28-39
+ *
+ * The reference consumes MeshBatch + Camera; this ABI consumes what the reference derives from them:
+ *   face_verts [F,3,3] fp64       per face vertex (x_ndc, y_ndc, z_view) = world_to_ndc (camera.cpp:36-70)
+ *                                 gathered through MeshBatch::faces_packed (batching.hpp:100-103)
+ *   mesh_to_face_first_idx [N]    MeshBatch::faces_packed().offsets[0..N)   (batching.hpp:20-27)
+ *   num_faces_per_mesh [N]        MeshBatch::num_faces_per_mesh()           (batching.hpp:98)
+ * Camera knowledge that face_verts cannot carry travels in the settings (znear, clip_nonpositive_z).
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers, caller-owned, stream-ordered on `stream`.
+ *   - Fragment layout is the reference's row-major [N,H,W,K] (mesh_raster.hpp:36-38):
+ *     slot = ((b*H + i)*W + j)*K + s; bary_coords has a trailing dimension of 3.
+ *   - Empty slots: pix_to_face -1, zbuf -1, bary 0, pix_dists 0 (mesh_raster.cpp:191-195, 205-208).
+ *   - No exceptions cross the ABI: every entry point returns a dr_status; dr_last_error() holds a
+ *     thread-local message for the last failure on the calling thread.
+ *   - Reentrant: no global state besides the per-thread error message, the launch counter and the
+ *     optional profiling ring (dr_profile_*), which are diagnostics only.
+ *   - There is no CPU fallback: without a usable CUDA device every compute entry point fails with
+ *     DR_ERR_CUDA.
+ */
+#ifndef DR_RASTER_H
+#define DR_RASTER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ABI-compatible with cudaStream_t without requiring CUDA headers (NULL = legacy default stream). */
+typedef struct CUstream_st* dr_stream_t;
+
+typedef enum {
+  DR_OK = 0,
+  DR_ERR_SHAPE = 1, /* dr::ShapeError  (batching.cpp:10-31, mesh_raster.cpp:333-336) */
+  DR_ERR_INDEX = 2, /* dr::IndexError  (batching.cpp:17-21) */
+  DR_ERR_RANGE = 3, /* dr::RangeError  (core.hpp:38-40): settings out of range */
+  DR_ERR_CUDA = 4,  /* CUDA runtime failure / no device */
+  DR_ERR_OOM = 5,   /* workspace too small or allocation failure */
+  DR_ERR_USAGE = 6  /* dr::UsageError (core.hpp:47-49): null pointers, bad arguments */
+} dr_status;
+
+/* RasterSettings (mesh_raster.hpp:18-23) plus the north-star parameters. Zero-initialise, then set. */
+typedef struct dr_raster_settings {
+  int32_t image_h, image_w;    /* RasterSettings.image_h / image_w, >= 1 */
+  int32_t faces_per_pixel;     /* K >= 1 (RasterSettings.faces_per_pixel) */
+  int32_t bin_size;            /* 0 => naive semantics (mesh_raster.cpp:214); > 0 => coarse-to-fine with
+                                  bins of bin_size x bin_size pixels (RasterSettings.tile_size) */
+  int32_t max_faces_per_bin;   /* fast-path capacity of one bin list; 0 => automatic. A bin that overflows
+                                  is rasterized by the spill path: results never change (reference bins
+                                  are unbounded, mesh_raster.cpp:244) */
+  int32_t _reserved0;          /* must be 0 */
+  double blur_radius;          /* squared NDC distance (RasterSettings.blur_radius) */
+  double znear;                /* Camera.znear (camera.hpp:26): all-behind cull (mesh_raster.cpp:113) and the
+                                  per-pixel z cut (mesh_raster.cpp:174) */
+  uint8_t clip_nonpositive_z;  /* 1 for perspective cameras: drop faces with any vertex z_view <= 0
+                                  (world_to_ndc's `clipped`, camera.cpp:44-47, mesh_raster.cpp:112) */
+  uint8_t perspective_correct; /* 0 = reference behaviour; 1 = builder-defined correction */
+  uint8_t clip_barycentric_coords; /* 1 = reference behaviour (always clamps, mesh_raster.cpp:172) */
+  uint8_t cull_backfaces;      /* 0 = reference; 1 = drop faces whose NDC signed_area2 > 0 */
+  uint8_t _reserved1[4];       /* must be 0 */
+} dr_raster_settings;
+
+/* Fill `s` with the reference defaults (RasterSettings{} + Camera{} + perspective): 64x64, K=1,
+ * blur 1e-4, bin 16, znear 0.1, clip_nonpositive_z=1, clip_barycentric_coords=1, others 0. */
+void dr_raster_settings_default(dr_raster_settings* s);
+
+/* Workspace bytes the forward needs for (N meshes, F packed faces, settings). */
+size_t dr_rasterize_meshes_workspace_bytes(int64_t N, int64_t F, const dr_raster_settings* s);
+
+/* Forward (rasterize_meshes): fp32 fragment payload (zbuf, bary, dists), int64 pix_to_face.
+ * pix_to_face/zbuf/pix_dists: [N,H,W,K]; bary_coords: [N,H,W,K,3]. Every slot is written. */
+int dr_rasterize_meshes_fwd(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                            const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
+                            const dr_raster_settings* s, int64_t* pix_to_face, float* zbuf,
+                            float* bary_coords, float* pix_dists, void* workspace, size_t workspace_bytes,
+                            dr_stream_t stream);
+
+/* Same contract with fp64 payload: bit-identical to the reference MeshFragments (mesh_raster.hpp:28-39). */
+int dr_rasterize_meshes_fwd_f64(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                                const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
+                                const dr_raster_settings* s, int64_t* pix_to_face, double* zbuf,
+                                double* bary_coords, double* pix_dists, void* workspace,
+                                size_t workspace_bytes, dr_stream_t stream);
+
+/* Backward (rasterize_backward, mesh_raster.cpp:345-378): cotangents on zbuf [N,H,W,K], bary [N,H,W,K,3],
+ * dists [N,H,W,K] pulled back to grad_face_verts [F,3,3] = d(x_ndc, y_ndc, z_view) per face vertex
+ * (overwritten). bary_coords is the forward's output (the reference reads frag.bary, mesh_raster.cpp:359).
+ * Accumulation uses fp64 atomics: the summation order is not fixed, results agree to ~1e-15 relative. */
+int dr_rasterize_meshes_bwd(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                            const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
+                            const dr_raster_settings* s, const int64_t* pix_to_face, const float* bary_coords,
+                            const float* grad_zbuf, const float* grad_bary, const float* grad_dists,
+                            double* grad_face_verts, dr_stream_t stream);
+
+/* fp64 variant (bary and cotangents in fp64, as the reference's std::vector<double>). */
+int dr_rasterize_meshes_bwd_f64(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                                const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
+                                const dr_raster_settings* s, const int64_t* pix_to_face,
+                                const double* bary_coords, const double* grad_zbuf, const double* grad_bary,
+                                const double* grad_dists, double* grad_face_verts, dr_stream_t stream);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* dr_last_error(void);
+
+/* ---- diagnostics (not part of the reference surface) ---- */
+
+/* Reads the coarse-stage counters a forward left in `workspace` (synchronises `stream`):
+ * out[0] = bins, out[1] = bins that overflowed max_faces_per_bin (spill path), out[2] = total bin entries,
+ * out[3] = largest bin. Returns DR_ERR_USAGE for bin_size == 0. */
+int dr_rasterize_meshes_bin_stats(int64_t N, int64_t F, const dr_raster_settings* s, const void* workspace,
+                                  dr_stream_t stream, int64_t out[4]);
+
+/* Number of kernels this library has launched in this process. */
+uint64_t dr_launch_count(void);
+
+/* Optional per-kernel CUDA-event timing (on the launching stream). enable=1 starts recording (clears the
+ * ring); dr_profile_read synchronises and returns up to `cap` entries (name index, milliseconds).
+ * Names: dr_profile_kernel_name(idx). */
+void dr_profile_enable(int enable);
+int dr_profile_read(int* kernel_idx, float* ms, int cap);
+const char* dr_profile_kernel_name(int idx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DR_RASTER_H */

@@ -1,0 +1,225 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// extern "C" shim over the *unmodified* reference `dr3d` library
+// (/root/reference/proj/src/{core,batching,camera,mesh_raster,templates}.cpp), compiled
+// by oracle/Makefile into oracle/_ref/libdr3d_ref.so. It lets the Python tests and the
+// bench's reference arm call the reference's own rasterizer and generators:
+//   dr::rasterize_meshes / rasterize_meshes_naive   (mesh_raster.hpp:41,44)
+//   dr::rasterize_backward                          (mesh_raster.hpp:66-69)
+//   dr::world_to_ndc                                (camera.hpp:50)
+//   dr::ico_sphere / cube / synthetic_batch         (templates.hpp:12-24)
+// Errors are caught and reported through ref_last_error() (the reference throws).
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "dr/batching.hpp"
+#include "dr/camera.hpp"
+#include "dr/core.hpp"
+#include "dr/mesh_raster.hpp"
+#include "dr/templates.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+// cam: [kind(0 ortho,1 persp), R(9 row-major), t(3), focal, ppx, ppy, sx, sy, znear, zfar]
+dr::Camera make_camera(const double* cam) {
+  dr::Mat3 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r.m[i][j] = cam[1 + 3 * i + j];
+  dr::Vec3 t{cam[10], cam[11], cam[12]};
+  if (cam[0] != 0.0)
+    return dr::Camera::perspective(r, t, cam[13], {cam[14], cam[15]}, cam[18], cam[19]);
+  return dr::Camera::orthographic(r, t, {cam[16], cam[17]}, cam[18], cam[19]);
+}
+
+dr::RasterSettings make_settings(const int32_t* si, double blur) {
+  dr::RasterSettings s;
+  s.image_h = si[0];
+  s.image_w = si[1];
+  s.faces_per_pixel = si[2];
+  s.tile_size = si[3];
+  s.blur_radius = blur;
+  return s;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+void ref_set_num_threads(int n) { dr::set_num_threads(n); }
+int ref_num_threads(void) { return dr::num_threads(); }
+
+// ---- mesh batches (opaque handles) ----
+void* ref_batch_from_arrays(const double* verts, const int64_t* faces_local, const int64_t* vert_counts,
+                            const int64_t* face_counts, int32_t n) {
+  dr::MeshBatch* out = nullptr;
+  int rc = guarded([&] {
+    std::vector<std::vector<dr::Vec3>> vl(size_t(n > 0 ? n : 0));
+    std::vector<std::vector<dr::Face>> fl(size_t(n > 0 ? n : 0));
+    int64_t vo = 0, fo = 0;
+    for (int32_t b = 0; b < n; ++b) {
+      for (int64_t v = 0; v < vert_counts[b]; ++v, ++vo)
+        vl[size_t(b)].push_back({verts[3 * vo], verts[3 * vo + 1], verts[3 * vo + 2]});
+      for (int64_t f = 0; f < face_counts[b]; ++f, ++fo)
+        fl[size_t(b)].push_back({faces_local[3 * fo], faces_local[3 * fo + 1], faces_local[3 * fo + 2]});
+    }
+    out = new dr::MeshBatch(std::move(vl), std::move(fl));
+  });
+  return rc == 0 ? out : nullptr;
+}
+void* ref_ico_sphere(int level) {
+  dr::MeshBatch* out = nullptr;
+  guarded([&] { out = new dr::MeshBatch(dr::ico_sphere(level)); });
+  return out;
+}
+void* ref_cube(double half, int n) {
+  dr::MeshBatch* out = nullptr;
+  guarded([&] { out = new dr::MeshBatch(dr::cube(half, n)); });
+  return out;
+}
+void* ref_synthetic_batch(double mean_faces, double sigma, int batch, uint64_t seed) {
+  dr::MeshBatch* out = nullptr;
+  guarded([&] { out = new dr::MeshBatch(dr::synthetic_batch(mean_faces, sigma, batch, seed)); });
+  return out;
+}
+void ref_batch_free(void* h) { delete static_cast<dr::MeshBatch*>(h); }
+// sizes: [N, total_verts, total_faces]
+void ref_batch_sizes(void* h, int64_t* out3) {
+  auto* m = static_cast<dr::MeshBatch*>(h);
+  out3[0] = m->size();
+  out3[1] = m->total_verts();
+  out3[2] = m->total_faces();
+}
+// packed verts [V,3], packed faces with GLOBAL indices [F,3], per-mesh counts
+void ref_batch_export(void* h, double* verts, int64_t* faces_packed, int64_t* vert_counts,
+                      int64_t* face_counts) {
+  auto* m = static_cast<dr::MeshBatch*>(h);
+  const auto& v = m->verts_packed().data;
+  for (size_t i = 0; i < v.size(); ++i) {
+    verts[3 * i] = v[i].x;
+    verts[3 * i + 1] = v[i].y;
+    verts[3 * i + 2] = v[i].z;
+  }
+  const auto& f = m->faces_packed().data;
+  for (size_t i = 0; i < f.size(); ++i) {
+    faces_packed[3 * i] = f[i].a;
+    faces_packed[3 * i + 1] = f[i].b;
+    faces_packed[3 * i + 2] = f[i].c;
+  }
+  for (int b = 0; b < m->size(); ++b) {
+    vert_counts[b] = m->num_verts_per_mesh()[size_t(b)];
+    face_counts[b] = m->num_faces_per_mesh()[size_t(b)];
+  }
+}
+
+// ---- camera ----
+int ref_world_to_ndc(const double* cam, const double* pts, int64_t n, double* xy, double* zv,
+                     uint8_t* clipped) {
+  return guarded([&] {
+    dr::Camera c = make_camera(cam);
+    for (int64_t i = 0; i < n; ++i) {
+      dr::NdcPoint p = dr::world_to_ndc(c, dr::Vec3{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});
+      xy[2 * i] = p.xy.x;
+      xy[2 * i + 1] = p.xy.y;
+      zv[i] = p.z_view;
+      clipped[i] = p.clipped ? 1 : 0;
+    }
+  });
+}
+int ref_world_to_ndc_backward(const double* cam, const double* pts, const double* d_xy,
+                              const double* d_z, int64_t n, double* d_world) {
+  return guarded([&] {
+    dr::Camera c = make_camera(cam);
+    for (int64_t i = 0; i < n; ++i) {
+      dr::Vec3 g = dr::world_to_ndc_backward(c, {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]},
+                                             {d_xy[2 * i], d_xy[2 * i + 1]}, d_z[i]);
+      d_world[3 * i] = g.x;
+      d_world[3 * i + 1] = g.y;
+      d_world[3 * i + 2] = g.z;
+    }
+  });
+}
+
+// ---- the hot path ----
+// si: [H, W, K, tile]; outputs sized N*H*W*K (bary x3)
+int ref_rasterize(void* h, const double* cam, const int32_t* si, double blur, int naive,
+                  int64_t* p2f, double* zbuf, double* bary, double* dists) {
+  return guarded([&] {
+    auto* m = static_cast<dr::MeshBatch*>(h);
+    dr::Camera c = make_camera(cam);
+    dr::RasterSettings s = make_settings(si, blur);
+    dr::MeshFragments f = naive ? dr::rasterize_meshes_naive(*m, c, s) : dr::rasterize_meshes(*m, c, s);
+    std::memcpy(p2f, f.pix_to_face.data(), f.pix_to_face.size() * sizeof(int64_t));
+    std::memcpy(zbuf, f.zbuf.data(), f.zbuf.size() * sizeof(double));
+    std::memcpy(bary, f.bary.data(), f.bary.size() * sizeof(double));
+    std::memcpy(dists, f.dists.data(), f.dists.size() * sizeof(double));
+  });
+}
+
+// fragments in, world-space d_verts [V,3] out (dr::rasterize_backward, mesh_raster.hpp:66-69)
+int ref_rasterize_backward(void* h, const double* cam, const int32_t* si, double blur, int32_t nbatch,
+                           const int64_t* p2f, const double* zbuf, const double* bary,
+                           const double* dists, const double* d_zbuf, const double* d_bary,
+                           const double* d_dists, double* d_verts) {
+  return guarded([&] {
+    auto* m = static_cast<dr::MeshBatch*>(h);
+    dr::Camera c = make_camera(cam);
+    dr::RasterSettings s = make_settings(si, blur);
+    dr::MeshFragments f;
+    f.batch = nbatch;
+    f.h = s.image_h;
+    f.w = s.image_w;
+    f.k = s.faces_per_pixel;
+    size_t ns = size_t(f.slots());
+    f.pix_to_face.assign(p2f, p2f + ns);
+    f.zbuf.assign(zbuf, zbuf + ns);
+    f.bary.assign(bary, bary + 3 * ns);
+    f.dists.assign(dists, dists + ns);
+    std::vector<double> dz(d_zbuf, d_zbuf + ns), db(d_bary, d_bary + 3 * ns), dd(d_dists, d_dists + ns);
+    std::vector<dr::Vec3> g = dr::rasterize_backward(*m, c, s, f, dz, db, dd);
+    for (size_t i = 0; i < g.size(); ++i) {
+      d_verts[3 * i] = g[i].x;
+      d_verts[3 * i + 1] = g[i].y;
+      d_verts[3 * i + 2] = g[i].z;
+    }
+  });
+}
+
+// kernel-level helpers for the known-answer tests (mesh_raster.hpp:51-64)
+double ref_point_triangle_dist2(const double* p, const double* a, const double* b, const double* c) {
+  return dr::point_triangle_dist2({p[0], p[1]}, {a[0], a[1]}, {b[0], b[1]}, {c[0], c[1]});
+}
+void ref_barycentric(const double* p, const double* a, const double* b, const double* c, double* w) {
+  dr::Vec3 r = dr::barycentric_coords({p[0], p[1]}, {a[0], a[1]}, {b[0], b[1]}, {c[0], c[1]});
+  w[0] = r.x;
+  w[1] = r.y;
+  w[2] = r.z;
+}
+void ref_clamp_barycentric(const double* w, double* out) {
+  dr::Vec3 r = dr::clamp_barycentric({w[0], w[1], w[2]});
+  out[0] = r.x;
+  out[1] = r.y;
+  out[2] = r.z;
+}
+void ref_point_triangle_dist2_backward(const double* p, const double* a, const double* b, const double* c,
+                                       double d_out, double* g6) {
+  dr::Vec2 da{}, db{}, dc{};
+  dr::point_triangle_dist2_backward({p[0], p[1]}, {a[0], a[1]}, {b[0], b[1]}, {c[0], c[1]}, d_out, da, db,
+                                    dc);
+  g6[0] = da.x; g6[1] = da.y; g6[2] = db.x; g6[3] = db.y; g6[4] = dc.x; g6[5] = dc.y;
+}
+}  // extern "C"

@@ -1,0 +1,24 @@
+"""B200-native rasterize_meshes: the hot path of arXiv 2007.08501 (PyTorch3D) re-built for sm_100a.
+
+Public surface (mirrors /root/reference/proj/include/dr/mesh_raster.hpp on the north-star boundary):
+    RasterSettings, rasterize_meshes, rasterize_meshes_naive, rasterize_meshes_backward, RasterizeMeshes
+Input generators and the host camera transform live in ``scenes``; mesh sharding across GPUs in ``shard``.
+"""
+from .raster import (  # noqa: F401
+    CudaError,
+    KernelTimer,
+    MeshIndexError,
+    RangeError,
+    RasterError,
+    RasterizeMeshes,
+    RasterSettings,
+    ShapeError,
+    UsageError,
+    WorkspaceError,
+    bin_stats,
+    launch_count,
+    rasterize_meshes,
+    rasterize_meshes_backward,
+    rasterize_meshes_naive,
+    workspace_bytes,
+)

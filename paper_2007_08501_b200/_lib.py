@@ -1,0 +1,82 @@
+"""ctypes binding of libdr_raster_b200.so (include/dr_raster.h).
+
+The shared library is built in-tree by ``make`` (or ``__graft_entry__.build()``). There is no fallback: if
+the library is missing, importing the package's compute entry points raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdr_raster_b200.so")
+
+DR_OK, DR_ERR_SHAPE, DR_ERR_INDEX, DR_ERR_RANGE, DR_ERR_CUDA, DR_ERR_OOM, DR_ERR_USAGE = range(7)
+
+# symbols include/dr_raster.h declares (the CPU suite checks the library exports all of them)
+EXPORTED_SYMBOLS = (
+    "dr_raster_settings_default",
+    "dr_rasterize_meshes_workspace_bytes",
+    "dr_rasterize_meshes_fwd",
+    "dr_rasterize_meshes_fwd_f64",
+    "dr_rasterize_meshes_bwd",
+    "dr_rasterize_meshes_bwd_f64",
+    "dr_last_error",
+    "dr_rasterize_meshes_bin_stats",
+    "dr_launch_count",
+    "dr_profile_enable",
+    "dr_profile_read",
+    "dr_profile_kernel_name",
+)
+
+
+class DrRasterSettings(C.Structure):
+    """dr_raster_settings (include/dr_raster.h)."""
+
+    _fields_ = [
+        ("image_h", C.c_int32), ("image_w", C.c_int32), ("faces_per_pixel", C.c_int32),
+        ("bin_size", C.c_int32), ("max_faces_per_bin", C.c_int32), ("_reserved0", C.c_int32),
+        ("blur_radius", C.c_double), ("znear", C.c_double),
+        ("clip_nonpositive_z", C.c_uint8), ("perspective_correct", C.c_uint8),
+        ("clip_barycentric_coords", C.c_uint8), ("cull_backfaces", C.c_uint8), ("_reserved1", C.c_uint8 * 4),
+    ]
+
+
+_vp = C.c_void_p
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load (once) and return the library; raises ImportError when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
+                          "there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    sp = C.POINTER(DrRasterSettings)
+    L.dr_raster_settings_default.argtypes = [sp]
+    L.dr_rasterize_meshes_workspace_bytes.argtypes = [C.c_int64, C.c_int64, sp]
+    L.dr_rasterize_meshes_workspace_bytes.restype = C.c_size_t
+    fwd_args = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, _vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]
+    L.dr_rasterize_meshes_fwd.argtypes = fwd_args
+    L.dr_rasterize_meshes_fwd_f64.argtypes = fwd_args
+    bwd_args = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.dr_rasterize_meshes_bwd.argtypes = bwd_args
+    L.dr_rasterize_meshes_bwd_f64.argtypes = bwd_args
+    L.dr_last_error.restype = C.c_char_p
+    L.dr_rasterize_meshes_bin_stats.argtypes = [C.c_int64, C.c_int64, sp, _vp, _vp, C.POINTER(C.c_int64)]
+    L.dr_launch_count.restype = C.c_uint64
+    L.dr_profile_enable.argtypes = [C.c_int]
+    L.dr_profile_read.argtypes = [C.POINTER(C.c_int), C.POINTER(C.c_float), C.c_int]
+    L.dr_profile_kernel_name.argtypes = [C.c_int]
+    L.dr_profile_kernel_name.restype = C.c_char_p
+    for fn in ("dr_rasterize_meshes_fwd", "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
+               "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_bin_stats"):
+        getattr(L, fn).restype = C.c_int
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return load().dr_last_error().decode()

@@ -1,0 +1,383 @@
+// C-ABI of libdr_raster_b200.so (include/dr_raster.h): validation, workspace planning, launch sequence,
+// error reporting, launch counting and optional per-kernel event timing.
+//
+// Error behaviour mirrors the reference's exceptions as status codes:
+//   empty batch                          -> DR_ERR_SHAPE (MeshBatch ctor "empty mesh batch", batching.cpp:14)
+//   negative face counts                 -> DR_ERR_SHAPE
+//   mesh face range outside [0, F)       -> DR_ERR_INDEX (cf. IndexError, batching.cpp:17-21)
+//   image size / K / bin size out of range -> DR_ERR_RANGE
+//   null pointers / short workspace      -> DR_ERR_USAGE / DR_ERR_OOM
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dr_raster.h"
+#include "raster_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(DR_ERR_CUDA, "CUDA error in %s: %s", where, cudaGetErrorString(e));
+}
+
+// ---- optional per-kernel timing ring ----
+const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine", "k_backward", "memset"};
+enum { KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4 };
+struct ProfEntry {
+  int kernel;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof_on{false};
+std::vector<ProfEntry> g_prof;
+
+struct ProfScope {
+  cudaStream_t st;
+  int kernel;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(cudaStream_t s, int k) : st(s), kernel(k) {
+    if (g_prof_on.load()) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+    if (k != KN_MEMSET) g_launches.fetch_add(1);
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEventRecord(b, st);
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      g_prof.push_back({kernel, a, b});
+    }
+  }
+};
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Plan {
+  int64_t N = 0, F = 0;
+  int H = 0, W = 0, K = 0;
+  int bs = 0;  // bin side used by the fine stage (16 when naive)
+  bool binned = false;
+  int nbx = 0, nby = 0, cap = 0;
+  size_t off_ibbox = 0, off_counts = 0, off_lists = 0, total = 0;
+};
+
+int auto_cap(int64_t F) { return (int)std::max<int64_t>(1, std::min<int64_t>(F, 4096)); }
+
+int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
+  if (!s) return fail(DR_ERR_USAGE, "settings pointer is null");
+  if (N < 1) return fail(DR_ERR_SHAPE, "empty mesh batch (N=%lld)", (long long)N);
+  if (N > 65535) return fail(DR_ERR_RANGE, "N=%lld meshes exceeds 65535", (long long)N);
+  if (F < 0) return fail(DR_ERR_SHAPE, "negative face count F=%lld", (long long)F);
+  if (F > INT32_MAX - 1) return fail(DR_ERR_RANGE, "F=%lld exceeds the int32 face-id range", (long long)F);
+  if (s->image_h < 1 || s->image_w < 1 || s->image_h > 32768 || s->image_w > 32768)
+    return fail(DR_ERR_RANGE, "image size %dx%d outside [1, 32768]", s->image_h, s->image_w);
+  if (s->faces_per_pixel < 1 || s->faces_per_pixel > 1024)
+    return fail(DR_ERR_RANGE, "faces_per_pixel=%d outside [1, 1024]", s->faces_per_pixel);
+  if (s->bin_size < 0) return fail(DR_ERR_RANGE, "bin_size=%d < 0", s->bin_size);
+  if (s->max_faces_per_bin < 0) return fail(DR_ERR_RANGE, "max_faces_per_bin=%d < 0", s->max_faces_per_bin);
+  if (std::isnan(s->blur_radius) || std::isnan(s->znear)) return fail(DR_ERR_RANGE, "blur_radius/znear is NaN");
+  p.N = N;
+  p.F = F;
+  p.H = s->image_h;
+  p.W = s->image_w;
+  p.K = s->faces_per_pixel;
+  p.binned = s->bin_size > 0;
+  p.bs = p.binned ? s->bin_size : 16;
+  p.nbx = (p.W + p.bs - 1) / p.bs;
+  p.nby = (p.H + p.bs - 1) / p.bs;
+  p.cap = p.binned ? (s->max_faces_per_bin > 0 ? s->max_faces_per_bin : auto_cap(F)) : 0;
+  size_t off = 0;
+  p.off_ibbox = off;
+  off = align_up(off + sizeof(int4) * (size_t)std::max<int64_t>(F, 1));
+  p.off_counts = off;
+  if (p.binned) {
+    off = align_up(off + sizeof(int) * (size_t)N * p.nbx * p.nby);
+    p.off_lists = off;
+    off = align_up(off + sizeof(int32_t) * (size_t)N * p.nbx * p.nby * (size_t)p.cap);
+  }
+  p.total = off;
+  return DR_OK;
+}
+
+// host copy of the mesh ranges: validation + grid sizing (N is small; one D2H per call)
+int read_ranges(const int64_t* first, const int64_t* num, int64_t N, int64_t F, cudaStream_t st,
+                int64_t* max_faces) {
+  std::vector<int64_t> h(2 * (size_t)N);
+  cudaError_t e = cudaMemcpyAsync(h.data(), first, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data() + N, num, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "reading mesh_to_face_first_idx / num_faces_per_mesh");
+  int64_t mx = 0;
+  for (int64_t b = 0; b < N; ++b) {
+    int64_t f0 = h[b], n = h[N + b];
+    if (n < 0) return fail(DR_ERR_SHAPE, "num_faces_per_mesh[%lld] = %lld < 0", (long long)b, (long long)n);
+    if (f0 < 0 || f0 > F || f0 + n > F)
+      return fail(DR_ERR_INDEX, "mesh %lld face range [%lld, %lld) outside [0, %lld)", (long long)b, (long long)f0,
+                  (long long)(f0 + n), (long long)F);
+    mx = std::max(mx, n);
+  }
+  *max_faces = mx;
+  return DR_OK;
+}
+
+template <typename OutT>
+int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+             const dr_raster_settings* s, int64_t* p2f, OutT* zbuf, OutT* bary, OutT* dists, void* ws, size_t ws_bytes,
+             cudaStream_t st) {
+  Plan p;
+  int rc = make_plan(N, F, s, p);
+  if (rc) return rc;
+  if (!first || !num || !p2f || !zbuf || !bary || !dists || (F > 0 && !fv))
+    return fail(DR_ERR_USAGE, "null input/output pointer");
+  if (!ws || ws_bytes < p.total)
+    return fail(DR_ERR_OOM, "workspace too small: %zu bytes given, %zu needed", ws_bytes, p.total);
+  int64_t max_faces = 0;
+  rc = read_ranges(first, num, N, F, st, &max_faces);
+  if (rc) return rc;
+
+  char* base = static_cast<char*>(ws);
+  int4* ibbox = reinterpret_cast<int4*>(base + p.off_ibbox);
+  int* counts = reinterpret_cast<int*>(base + p.off_counts);
+  int32_t* lists = reinterpret_cast<int32_t*>(base + p.off_lists);
+  const double inflate = std::sqrt(std::max(0.0, s->blur_radius));  // MR:103
+
+  {
+    ProfScope ps(st, KN_SETUP);
+    drb::launch_face_setup(fv, F, p.H, p.W, inflate, s->znear, s->clip_nonpositive_z, s->cull_backfaces, ibbox, st);
+  }
+  if (p.binned) {
+    {
+      ProfScope ps(st, KN_MEMSET);
+      cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)N * p.nbx * p.nby, st);
+    }
+    ProfScope ps(st, KN_BIN);
+    drb::launch_bin_faces(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, p.cap, counts, lists, st);
+  }
+  drb::FineArgs<OutT> A;
+  A.fv = fv;
+  A.ibbox = ibbox;
+  A.first = first;
+  A.num = num;
+  A.bin_counts = counts;
+  A.bin_lists = lists;
+  A.binned = p.binned ? 1 : 0;
+  A.cap = p.cap;
+  A.bs = p.bs;
+  A.nbx = p.nbx;
+  A.nby = p.nby;
+  A.H = p.H;
+  A.W = p.W;
+  A.K = p.K;
+  A.blur = s->blur_radius;
+  A.znear = s->znear;
+  A.persp = s->perspective_correct != 0;
+  A.clip = s->clip_barycentric_coords != 0;
+  // sub-tile: 16x16 pixels (8 warps) by default; narrower for small bins and for large K (shared-memory top-K)
+  int stw = std::min(16, (p.bs + 7) / 8 * 8), sth = std::min(16, (p.bs + 3) / 4 * 4);
+  if (p.K > 16) {
+    // K * threads * 12 B of top-K storage must fit next to the staged faces
+    while (stw * sth > 32 && (size_t)p.K * stw * sth * 12 + (size_t)stw * sth * drb::staged_face_bytes() > 200 * 1024) {
+      if (sth >= stw && sth > 4) sth /= 2;
+      else if (stw > 8) stw /= 2;
+      else break;
+    }
+    if ((size_t)p.K * stw * sth * 12 + (size_t)stw * sth * drb::staged_face_bytes() > 220 * 1024)
+      return fail(DR_ERR_RANGE, "faces_per_pixel=%d too large for the shared-memory top-K", p.K);
+  }
+  A.stw = stw;
+  A.sth = sth;
+  A.staged_bytes = (size_t)stw * sth * drb::staged_face_bytes();
+  A.p2f = p2f;
+  A.zbuf = zbuf;
+  A.bary = bary;
+  A.dists = dists;
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_FINE);
+    e = drb::launch_fine(A, (int64_t)N * p.nbx * p.nby, st);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "rasterize_meshes forward");
+  return DR_OK;
+}
+
+template <typename InT>
+int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+             const dr_raster_settings* s, const int64_t* p2f, const InT* bary, const InT* dz, const InT* db,
+             const InT* dd, double* grad, cudaStream_t st) {
+  Plan p;
+  int rc = make_plan(N, F, s, p);
+  if (rc) return rc;
+  if (!p2f || !bary || !dz || !db || !dd || (F > 0 && (!fv || !grad)))
+    return fail(DR_ERR_USAGE, "null input/output pointer");
+  if (first && num) {
+    int64_t mx;
+    rc = read_ranges(first, num, N, F, st, &mx);
+    if (rc) return rc;
+  }
+  if (F == 0) return DR_OK;
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_MEMSET);
+    e = cudaMemsetAsync(grad, 0, sizeof(double) * 9 * (size_t)F, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "zeroing grad_face_verts");
+  drb::BwdArgs<InT> A;
+  A.fv = fv;
+  A.p2f = p2f;
+  A.bary = bary;
+  A.d_zbuf = dz;
+  A.d_bary = db;
+  A.d_dists = dd;
+  A.grad = grad;
+  A.S = N * (int64_t)p.H * p.W * p.K;
+  A.F = F;
+  A.H = p.H;
+  A.W = p.W;
+  A.K = p.K;
+  A.persp = s->perspective_correct != 0;
+  A.clip = s->clip_barycentric_coords != 0;
+  {
+    ProfScope ps(st, KN_BWD);
+    e = drb::launch_backward(A, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "rasterize_meshes backward");
+  return DR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void dr_raster_settings_default(dr_raster_settings* s) {
+  if (!s) return;
+  std::memset(s, 0, sizeof(*s));
+  s->image_h = s->image_w = 64;  // RasterSettings{} (mesh_raster.hpp:18-23)
+  s->faces_per_pixel = 1;
+  s->bin_size = 16;
+  s->blur_radius = 1e-4;
+  s->znear = 0.1;  // Camera{} (camera.hpp:26)
+  s->clip_nonpositive_z = 1;
+  s->clip_barycentric_coords = 1;
+}
+
+size_t dr_rasterize_meshes_workspace_bytes(int64_t N, int64_t F, const dr_raster_settings* s) {
+  Plan p;
+  if (make_plan(N, F, s, p)) return 0;
+  return p.total;
+}
+
+int dr_rasterize_meshes_fwd(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                            const dr_raster_settings* s, int64_t* p2f, float* zbuf, float* bary, float* dists,
+                            void* ws, size_t ws_bytes, dr_stream_t stream) {
+  return fwd_impl<float>(fv, first, num, N, F, s, p2f, zbuf, bary, dists, ws, ws_bytes,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dr_rasterize_meshes_fwd_f64(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                                const dr_raster_settings* s, int64_t* p2f, double* zbuf, double* bary,
+                                double* dists, void* ws, size_t ws_bytes, dr_stream_t stream) {
+  return fwd_impl<double>(fv, first, num, N, F, s, p2f, zbuf, bary, dists, ws, ws_bytes,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dr_rasterize_meshes_bwd(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                            const dr_raster_settings* s, const int64_t* p2f, const float* bary, const float* dz,
+                            const float* db, const float* dd, double* grad, dr_stream_t stream) {
+  return bwd_impl<float>(fv, first, num, N, F, s, p2f, bary, dz, db, dd, grad, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dr_rasterize_meshes_bwd_f64(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                                const dr_raster_settings* s, const int64_t* p2f, const double* bary,
+                                const double* dz, const double* db, const double* dd, double* grad,
+                                dr_stream_t stream) {
+  return bwd_impl<double>(fv, first, num, N, F, s, p2f, bary, dz, db, dd, grad,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+const char* dr_last_error(void) { return g_err.c_str(); }
+
+int dr_rasterize_meshes_bin_stats(int64_t N, int64_t F, const dr_raster_settings* s, const void* ws,
+                                  dr_stream_t stream, int64_t out[4]) {
+  Plan p;
+  int rc = make_plan(N, F, s, p);
+  if (rc) return rc;
+  if (!p.binned) return fail(DR_ERR_USAGE, "bin_stats: bin_size == 0 (naive path has no bins)");
+  if (!ws || !out) return fail(DR_ERR_USAGE, "null pointer");
+  size_t nb = (size_t)N * p.nbx * p.nby;
+  std::vector<int> h(nb);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(h.data(), static_cast<const char*>(ws) + p.off_counts, sizeof(int) * nb,
+                                  cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "bin_stats");
+  int64_t over = 0, tot = 0, mx = 0;
+  for (int c : h) {
+    over += c > p.cap;
+    tot += c;
+    mx = std::max<int64_t>(mx, c);
+  }
+  out[0] = (int64_t)nb;
+  out[1] = over;
+  out[2] = tot;
+  out[3] = mx;
+  return DR_OK;
+}
+
+uint64_t dr_launch_count(void) { return g_launches.load(); }
+
+void dr_profile_enable(int enable) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& e : g_prof) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  g_prof.clear();
+  g_prof_on.store(enable != 0);
+}
+
+int dr_profile_read(int* kernel_idx, float* ms, int cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  int n = 0;
+  for (auto& e : g_prof) {
+    if (n >= cap) break;
+    cudaEventSynchronize(e.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e.a, e.b);
+    kernel_idx[n] = e.kernel;
+    ms[n] = t;
+    ++n;
+  }
+  return n;
+}
+
+const char* dr_profile_kernel_name(int idx) {
+  if (idx < 0 || idx >= (int)(sizeof(kKernelNames) / sizeof(kKernelNames[0]))) return "";
+  return kKernelNames[idx];
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+// K3: backward of rasterize_meshes on sm_100a (rasterize_backward, MR:329-403, per-slot part MR:345-378).
+//
+// One thread per fragment slot recomputes the slot's NDC triangle and pixel centre, pulls the cotangents on
+// zbuf / bary / dists back through z-interpolation, clamp+renormalise, (optional) perspective correction,
+// the barycentric quotient and the frozen-edge distance envelope, and produces the 9 cotangents of its
+// face's (x_ndc, y_ndc, z_view) x 3 vertices. Lanes of a warp that hit the same face (neighbouring pixels
+// very often do) are grouped with __match_any_sync and summed with a log-depth shuffle reduction, so ONE
+// lane issues the 9 fp64 atomicAdds per (warp, face) instead of one per slot. The reference reduces per
+// vertex in slot order on one thread (MR:380-392); here the order of fp64 additions is not fixed.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "raster_kernels.cuh"
+#include "raster_math.cuh"
+
+namespace drb {
+
+// MR:309-325 (clamp_barycentric_backward)
+__device__ __forceinline__ void clamp_bary_backward(const double wr[3], const double dc[3], double out[3]) {
+  double t0 = clamp01(wr[0]), t1 = clamp01(wr[1]), t2 = clamp01(wr[2]);
+  double s = t0 + t1 + t2;
+  if (s <= 0) {
+    out[0] = out[1] = out[2] = 0.0;
+    return;
+  }
+  double h0 = t0 / s, h1 = t1 / s, h2 = t2 / s;
+  double d = dc[0] * h0 + dc[1] * h1 + dc[2] * h2;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double d_t = (dc[i] - d) / s;
+    out[i] = (wr[i] > 0.0 && wr[i] < 1.0) ? d_t : 0.0;
+  }
+}
+
+// per-slot cotangents -> g[9] = (dx, dy, dz) for vertices a, b, c
+template <typename InT>
+__device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slot, int32_t fid, double g[9]) {
+  const double* q = A.fv + 9 * (int64_t)fid;
+  double v[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) v[k] = __ldg(q + k);
+  const FaceGeom fg = make_face_geom(v);
+  const double z[3] = {fg.z0, fg.z1, fg.z2};
+  const int64_t pix = slot / A.K;
+  const int64_t rem = pix % ((int64_t)A.H * A.W);
+  const int i = (int)(rem / A.W), j = (int)(rem % A.W);
+  const V2 p{pixel_x(A.W, j), pixel_y(A.H, i)};  // MR:357
+
+  const double w_hat[3] = {(double)A.bary[3 * slot], (double)A.bary[3 * slot + 1], (double)A.bary[3 * slot + 2]};
+  const double dz = (double)A.d_zbuf[slot];
+  // MR:363-365: cotangent on the clamped bary = direct input + z-interpolation path
+  const double d_hat[3] = {(double)A.d_bary[3 * slot] + dz * z[0], (double)A.d_bary[3 * slot + 1] + dz * z[1],
+                           (double)A.d_bary[3 * slot + 2] + dz * z[2]};
+  const V2 pa = p - fg.a, pb = p - fg.b, pc = p - fg.c;
+  double w_raw[3];
+  barycentric(fg, pa, pb, pc, w_raw);  // MR:366
+  double d_w[3], dzv[3] = {0.0, 0.0, 0.0};
+  if (A.persp) {  // builder-defined: u = persp_correct(w_raw, z); bary = clamp(u)
+    double u[3], d_u[3], d_top[3];
+    const double den = persp_correct(w_raw, fg.z0, fg.z1, fg.z2, u);
+    if (A.clip) {
+      clamp_bary_backward(u, d_hat, d_u);
+    } else {
+      d_u[0] = d_hat[0];
+      d_u[1] = d_hat[1];
+      d_u[2] = d_hat[2];
+    }
+    if (den > kPerspEps) {
+      const double du_u = d_u[0] * u[0] + d_u[1] * u[1] + d_u[2] * u[2];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) d_top[k] = (d_u[k] - du_u) / den;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) d_top[k] = d_u[k] / kPerspEps;
+    }
+    d_w[0] = d_top[0] * z[1] * z[2];
+    d_w[1] = d_top[1] * z[0] * z[2];
+    d_w[2] = d_top[2] * z[0] * z[1];
+    dzv[0] = d_top[1] * w_raw[1] * z[2] + d_top[2] * w_raw[2] * z[1];
+    dzv[1] = d_top[0] * w_raw[0] * z[2] + d_top[2] * w_raw[2] * z[0];
+    dzv[2] = d_top[0] * w_raw[0] * z[1] + d_top[1] * w_raw[1] * z[0];
+  } else if (A.clip) {
+    clamp_bary_backward(w_raw, d_hat, d_w);  // MR:367
+  } else {
+    d_w[0] = d_hat[0];
+    d_w[1] = d_hat[1];
+    d_w[2] = d_hat[2];
+  }
+
+  // MR:290-306 barycentric_backward (w recomputed there == w_raw)
+  const V2 a = fg.a, b = fg.b, c = fg.c;
+  const V2 grad_d_a = perp(b - c), grad_d_b = perp(c - a), grad_d_c = perp(a - b);
+  const V2 gn0_b = perp(c - p), gn0_c = perp(p - b);
+  const V2 gn1_c = perp(a - p), gn1_a = perp(p - c);
+  const V2 gn2_a = perp(b - p), gn2_b = perp(p - a);
+  const double inv = 1.0 / fg.area;
+  const double wd = w_raw[0] * d_w[0] + w_raw[1] * d_w[1] + w_raw[2] * d_w[2];
+  V2 dxy[3];
+  dxy[0] = ((gn1_a * d_w[1] + gn2_a * d_w[2]) - grad_d_a * wd) * inv;
+  dxy[1] = ((gn0_b * d_w[0] + gn2_b * d_w[2]) - grad_d_b * wd) * inv;
+  dxy[2] = ((gn0_c * d_w[0] + gn1_c * d_w[1]) - grad_d_c * wd) * inv;
+
+  // MR:46-69 point_triangle_dist2_backward: nearest edge (first strict min), t and sign frozen
+  const double d_out = (double)A.d_dists[slot];
+  double t0, t1, t2;
+  const double e0 = seg_dist2(p, a, pa, fg.ab, fg.len_ab, t0);
+  const double e1 = seg_dist2(p, b, pb, fg.bc, fg.len_bc, t1);
+  const double e2 = seg_dist2(p, c, pc, fg.ca, fg.len_ca, t2);
+  int be = 0;
+  double best = e0, bt = t0;
+  if (e1 < best) { best = e1; bt = t1; be = 1; }
+  if (e2 < best) { best = e2; bt = t2; be = 2; }
+  const bool inside = point_triangle_dist2(p, fg, pa, pb, pc).inside;
+  const double sign = inside ? -1.0 : 1.0;
+  const V2 ea = be == 0 ? a : (be == 1 ? b : c);
+  const V2 eb = be == 0 ? b : (be == 1 ? c : a);
+  const V2 qq = ea + (eb - ea) * bt;
+  const V2 gg = (qq - p) * (2.0 * sign * d_out);
+  const V2 g_first = gg * (1.0 - bt), g_second = gg * bt;
+  // grads[be] += g*(1-t); grads[(be+1)%3] += g*t
+  if (be == 0) { dxy[0] = dxy[0] + g_first; dxy[1] = dxy[1] + g_second; }
+  else if (be == 1) { dxy[1] = dxy[1] + g_first; dxy[2] = dxy[2] + g_second; }
+  else { dxy[2] = dxy[2] + g_first; dxy[0] = dxy[0] + g_second; }
+
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g[3 * k + 0] = dxy[k].x;
+    g[3 * k + 1] = dxy[k].y;
+    g[3 * k + 2] = dz * w_hat[k] + dzv[k];  // MR:375
+  }
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(256) k_backward(BwdArgs<InT> A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * 32; base < A.S; base += nwarps * 32) {
+    const int64_t slot = base + lane;
+    int32_t fid = -1;
+    if (slot < A.S) {
+      int64_t f = A.p2f[slot];
+      if (f >= 0 && f < A.F) fid = (int32_t)f;
+    }
+    double g[9];
+    if (fid >= 0) {
+      slot_backward(A, slot, fid, g);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) g[k] = 0.0;
+    }
+    // group lanes by face; empty slots form per-lane singleton groups that never write
+    const int key = fid >= 0 ? fid : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    unsigned rel = __popc(peers & ((1u << lane) - 1u));
+    unsigned rem = peers & ~((2u << lane) - 1u);  // peers above this lane (2u << 31 == 0)
+    while (__any_sync(0xffffffffu, rem != 0)) {
+      const int next = __ffs(rem);  // 1-based lane of the next peer, 0 if none
+      const int src = next ? next - 1 : lane;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const double t = __shfl_sync(0xffffffffu, g[k], src);
+        if (next) g[k] += t;
+      }
+      rem &= ~__ballot_sync(0xffffffffu, rel & 1u);
+      rel >>= 1;
+    }
+    if (fid >= 0 && (peers & ((1u << lane) - 1u)) == 0) {
+      double* out = A.grad + 9 * (int64_t)fid;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) atomicAdd(out + k, g[k]);
+    }
+  }
+}
+
+template <typename InT>
+static cudaError_t launch_backward_t(const BwdArgs<InT>& A, cudaStream_t st) {
+  if (A.S <= 0) return cudaSuccess;
+  int64_t blocks = (A.S + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  k_backward<InT><<<(unsigned)blocks, 256, 0, st>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st) { return launch_backward_t(A, st); }
+cudaError_t launch_backward(const BwdArgs<double>& A, cudaStream_t st) { return launch_backward_t(A, st); }
+
+}  // namespace drb

@@ -1,0 +1,58 @@
+// Kernel argument blocks and launcher declarations shared by raster_fwd.cu, raster_bwd.cu and capi.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace drb {
+
+template <typename OutT>
+struct FineArgs {
+  const double* fv;         // [F,3,3] face_verts
+  const int4* ibbox;        // [F] (i0, i1, j0, j1) exact pixel ranges; empty if i0 > i1
+  const int64_t* first;     // [N] mesh_to_face_first_idx
+  const int64_t* num;       // [N] num_faces_per_mesh
+  const int* bin_counts;    // [N, nby, nbx] entries per bin (may exceed cap: overflow => spill path)
+  const int32_t* bin_lists; // [N, nby, nbx, cap] packed face ids
+  int binned;               // 0 => naive: every CTA scans its whole mesh
+  int cap;                  // max_faces_per_bin
+  int bs, nbx, nby;         // bin (tile) side in pixels, bins per row / column
+  int H, W, K;
+  double blur, znear;
+  bool persp, clip;
+  int stw, sth;             // sub-tile (pixels handled concurrently by the CTA): multiples of 8 x 4
+  size_t staged_bytes;      // dynamic smem for the staged-face ring (blockDim faces)
+  int64_t* p2f;
+  OutT* zbuf;
+  OutT* bary;
+  OutT* dists;
+};
+
+template <typename InT>
+struct BwdArgs {
+  const double* fv;
+  const int64_t* p2f;
+  const InT* bary;
+  const InT* d_zbuf;
+  const InT* d_bary;
+  const InT* d_dists;
+  double* grad;  // [F,3,3]
+  int64_t S;     // slots
+  int64_t F;
+  int H, W, K;
+  bool persp, clip;
+};
+
+void launch_face_setup(const double* fv, int64_t F, int H, int W, double inflate, double znear, int clip_z, int cull,
+                       int4* ibbox, cudaStream_t st);
+void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
+                      int bs, int nbx, int nby, int cap, int* counts, int32_t* lists, cudaStream_t st);
+cudaError_t launch_fine(const FineArgs<float>& A, int64_t nblocks, cudaStream_t st);
+cudaError_t launch_fine(const FineArgs<double>& A, int64_t nblocks, cudaStream_t st);
+cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st);
+cudaError_t launch_backward(const BwdArgs<double>& A, cudaStream_t st);
+size_t staged_face_bytes();
+
+}  // namespace drb

@@ -1,0 +1,258 @@
+"""Host-side mirror of the reference operator surface for the rasterize_meshes hot path.
+
+Python over the C-ABI (include/dr_raster.h); PyTorch provides device memory and streams only.
+
+Reference interface this mirrors (/root/reference/proj):
+  RasterSettings{image_h, image_w, faces_per_pixel, blur_radius, tile_size}   include/dr/mesh_raster.hpp:18-23
+  MeshFragments{pix_to_face, zbuf, bary, dists} as [N,H,W,K(,3)]              include/dr/mesh_raster.hpp:28-39
+  rasterize_meshes / rasterize_meshes_naive                                    include/dr/mesh_raster.hpp:41,44
+  rasterize_backward (cotangents on zbuf/bary/dists -> vertex grads)            include/dr/mesh_raster.hpp:66-69
+  errors: ShapeError / IndexError / RangeError / UsageError                   include/dr/core.hpp:23-49
+on the north-star boundary: packed face_verts [F,3,3] (x_ndc, y_ndc, z_view), mesh_to_face_first_idx and
+num_faces_per_mesh in; pix_to_face, zbuf, bary_coords, pix_dists out.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, replace
+
+import torch
+
+from . import _lib
+
+
+class RasterError(RuntimeError):
+    """Base of the errors the C-ABI reports (dr_status)."""
+
+
+class ShapeError(RasterError, ValueError):
+    """dr::ShapeError (core.hpp:23-25)."""
+
+
+class MeshIndexError(RasterError, IndexError):
+    """dr::IndexError (core.hpp:26-28)."""
+
+
+class RangeError(RasterError, ValueError):
+    """dr::RangeError (core.hpp:38-40)."""
+
+
+class UsageError(RasterError, ValueError):
+    """dr::UsageError (core.hpp:47-49)."""
+
+
+class CudaError(RasterError):
+    pass
+
+
+class WorkspaceError(RasterError, MemoryError):
+    pass
+
+
+_ERRORS = {
+    _lib.DR_ERR_SHAPE: ShapeError,
+    _lib.DR_ERR_INDEX: MeshIndexError,
+    _lib.DR_ERR_RANGE: RangeError,
+    _lib.DR_ERR_CUDA: CudaError,
+    _lib.DR_ERR_OOM: WorkspaceError,
+    _lib.DR_ERR_USAGE: UsageError,
+}
+
+
+def _check(rc: int, what: str):
+    if rc != _lib.DR_OK:
+        raise _ERRORS.get(rc, RasterError)(f"{what}: {_lib.last_error()}")
+
+
+@dataclass
+class RasterSettings:
+    """RasterSettings (mesh_raster.hpp:18-23) + the north-star parameters + the camera fields the boundary
+    needs (znear, clip_nonpositive_z, camera.hpp:26 / camera.cpp:44-47). Defaults are the reference's."""
+
+    image_size: int | tuple = 64
+    faces_per_pixel: int = 1
+    blur_radius: float = 1e-4
+    bin_size: int = 16            # 0 => naive semantics (rasterize_meshes_naive); reference `tile_size`
+    max_faces_per_bin: int = 0    # 0 => automatic; overflow never changes results
+    perspective_correct: bool = False
+    clip_barycentric_coords: bool = True
+    cull_backfaces: bool = False
+    znear: float = 0.1
+    clip_nonpositive_z: bool = True  # perspective camera
+
+    @property
+    def hw(self) -> tuple:
+        if isinstance(self.image_size, int):
+            return (self.image_size, self.image_size)
+        return (int(self.image_size[0]), int(self.image_size[1]))
+
+    def to_c(self) -> _lib.DrRasterSettings:
+        s = _lib.DrRasterSettings()
+        s.image_h, s.image_w = self.hw
+        s.faces_per_pixel = int(self.faces_per_pixel)
+        s.bin_size = int(self.bin_size)
+        s.max_faces_per_bin = int(self.max_faces_per_bin)
+        s.blur_radius = float(self.blur_radius)
+        s.znear = float(self.znear)
+        s.clip_nonpositive_z = int(bool(self.clip_nonpositive_z))
+        s.perspective_correct = int(bool(self.perspective_correct))
+        s.clip_barycentric_coords = int(bool(self.clip_barycentric_coords))
+        s.cull_backfaces = int(bool(self.cull_backfaces))
+        return s
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _inputs(face_verts, first, num):
+    if not isinstance(face_verts, torch.Tensor) or not face_verts.is_cuda:
+        raise UsageError("face_verts must be a CUDA tensor (there is no CPU path)")
+    if face_verts.dim() != 3 or tuple(face_verts.shape[1:]) != (3, 3):
+        raise ShapeError(f"face_verts must be [F,3,3], got {tuple(face_verts.shape)}")
+    dev = face_verts.device
+    fv = face_verts.detach().to(torch.float64).contiguous()
+    first = torch.as_tensor(first, dtype=torch.int64, device=dev).contiguous()
+    num = torch.as_tensor(num, dtype=torch.int64, device=dev).contiguous()
+    if first.dim() != 1 or num.shape != first.shape:
+        raise ShapeError("mesh_to_face_first_idx and num_faces_per_mesh must be 1-D of equal length")
+    return fv, first, num
+
+
+def workspace_bytes(num_meshes: int, num_faces: int, settings: RasterSettings) -> int:
+    s = settings.to_c()
+    n = _lib.load().dr_rasterize_meshes_workspace_bytes(num_meshes, num_faces, C.byref(s))
+    if n == 0:
+        raise RangeError(f"invalid settings: {_lib.last_error()}")
+    return n
+
+
+def rasterize_meshes(face_verts: torch.Tensor, mesh_to_face_first_idx, num_faces_per_mesh,
+                     settings: RasterSettings | None = None, out_dtype=torch.float32, workspace=None,
+                     **kwargs):
+    """Forward. Returns (pix_to_face int64 [N,H,W,K], zbuf [N,H,W,K], bary_coords [N,H,W,K,3],
+    pix_dists [N,H,W,K]) with zbuf/bary/dists in ``out_dtype`` (float32 or float64)."""
+    settings = settings or RasterSettings(**kwargs)
+    L = _lib.load()
+    fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
+    N, F = int(first.numel()), int(fv.shape[0])
+    H, W = settings.hw
+    K = int(settings.faces_per_pixel)
+    s = settings.to_c()
+    dev = fv.device
+    ws_n = L.dr_rasterize_meshes_workspace_bytes(N, F, C.byref(s))
+    if ws_n == 0:
+        _check(_lib.DR_ERR_RANGE if N >= 1 else _lib.DR_ERR_SHAPE, "rasterize_meshes")
+    if workspace is None or workspace.numel() < ws_n:
+        workspace = torch.empty(ws_n, dtype=torch.uint8, device=dev)
+    p2f = torch.empty((N, H, W, K), dtype=torch.int64, device=dev)
+    zbuf = torch.empty((N, H, W, K), dtype=out_dtype, device=dev)
+    bary = torch.empty((N, H, W, K, 3), dtype=out_dtype, device=dev)
+    dists = torch.empty((N, H, W, K), dtype=out_dtype, device=dev)
+    fn = L.dr_rasterize_meshes_fwd if out_dtype == torch.float32 else L.dr_rasterize_meshes_fwd_f64
+    if out_dtype not in (torch.float32, torch.float64):
+        raise UsageError("out_dtype must be float32 or float64")
+    with torch.cuda.device(dev):
+        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), _ptr(p2f), _ptr(zbuf), _ptr(bary), _ptr(dists),
+                _ptr(workspace), workspace.numel(), _stream(dev))
+    _check(rc, "rasterize_meshes")
+    return p2f, zbuf, bary, dists
+
+
+def rasterize_meshes_naive(face_verts, mesh_to_face_first_idx, num_faces_per_mesh,
+                           settings: RasterSettings | None = None, out_dtype=torch.float32, **kwargs):
+    """rasterize_meshes_naive (mesh_raster.hpp:44): the unbinned contract (bin_size = 0)."""
+    settings = replace(settings or RasterSettings(**kwargs), bin_size=0)
+    return rasterize_meshes(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings, out_dtype=out_dtype)
+
+
+def rasterize_meshes_backward(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
+                              pix_to_face, bary_coords, grad_zbuf, grad_bary, grad_dists):
+    """Backward (rasterize_backward's per-slot part, mesh_raster.cpp:345-378): returns grad_face_verts [F,3,3]
+    f64 = d(x_ndc, y_ndc, z_view) per face vertex. Cotangent/bary dtype float32 or float64 (all the same)."""
+    L = _lib.load()
+    fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
+    N, F = int(first.numel()), int(fv.shape[0])
+    H, W = settings.hw
+    K = int(settings.faces_per_pixel)
+    shp = (N, H, W, K)
+    dt = bary_coords.dtype
+    if dt not in (torch.float32, torch.float64):
+        raise UsageError("bary/cotangents must be float32 or float64")
+    tens = [pix_to_face, bary_coords, grad_zbuf, grad_bary, grad_dists]
+    want = [shp, shp + (3,), shp, shp + (3,), shp]
+    for t, w in zip(tens, want):
+        if tuple(t.shape) != w:
+            raise ShapeError(f"rasterize_backward: cotangent shapes do not match fragments: {tuple(t.shape)} vs {w}")
+    p2f = pix_to_face.to(torch.int64).contiguous()
+    others = [t.to(dt).contiguous() for t in tens[1:]]
+    grad = torch.empty((F, 3, 3), dtype=torch.float64, device=fv.device)
+    s = settings.to_c()
+    fn = L.dr_rasterize_meshes_bwd if dt == torch.float32 else L.dr_rasterize_meshes_bwd_f64
+    with torch.cuda.device(fv.device):
+        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), _ptr(p2f), *[_ptr(t) for t in others],
+                _ptr(grad), _stream(fv.device))
+    _check(rc, "rasterize_backward")
+    return grad
+
+
+def bin_stats(num_meshes, num_faces, settings: RasterSettings, workspace: torch.Tensor) -> dict:
+    """Coarse-stage counters left in the workspace by the last forward (synchronises)."""
+    L = _lib.load()
+    out = (C.c_int64 * 4)()
+    s = settings.to_c()
+    rc = L.dr_rasterize_meshes_bin_stats(num_meshes, num_faces, C.byref(s), _ptr(workspace),
+                                         _stream(workspace.device), out)
+    _check(rc, "bin_stats")
+    return dict(bins=out[0], overflowed=out[1], entries=out[2], max_bin=out[3])
+
+
+class RasterizeMeshes(torch.autograd.Function):
+    """Autograd wrapper: face_verts -> (pix_to_face, zbuf, bary_coords, pix_dists)."""
+
+    @staticmethod
+    def forward(ctx, face_verts, first, num, settings: RasterSettings):
+        p2f, zbuf, bary, dists = rasterize_meshes(face_verts, first, num, settings)
+        ctx.settings = settings
+        ctx.save_for_backward(face_verts, torch.as_tensor(first, device=face_verts.device),
+                              torch.as_tensor(num, device=face_verts.device), p2f, bary)
+        ctx.mark_non_differentiable(p2f)
+        return p2f, zbuf, bary, dists
+
+    @staticmethod
+    def backward(ctx, _g_p2f, g_zbuf, g_bary, g_dists):
+        fv, first, num, p2f, bary = ctx.saved_tensors
+        zeros = lambda t, like: torch.zeros_like(like) if t is None else t  # noqa: E731
+        g = rasterize_meshes_backward(fv, first, num, ctx.settings, p2f, bary, zeros(g_zbuf, bary[..., 0]),
+                                      zeros(g_bary, bary), zeros(g_dists, bary[..., 0]))
+        return g.to(fv.dtype), None, None, None
+
+
+def launch_count() -> int:
+    return int(_lib.load().dr_launch_count())
+
+
+class KernelTimer:
+    """Per-kernel CUDA-event timing recorded by the library on the launching stream."""
+
+    def __enter__(self):
+        _lib.load().dr_profile_enable(1)
+        return self
+
+    def __exit__(self, *exc):
+        L = _lib.load()
+        cap = 1 << 16
+        idx = (C.c_int * cap)()
+        ms = (C.c_float * cap)()
+        n = L.dr_profile_read(idx, ms, cap)
+        self.records = [(L.dr_profile_kernel_name(idx[i]).decode(), ms[i]) for i in range(n)]
+        L.dr_profile_enable(0)
+        return False
+
+    def total(self, name: str) -> tuple:
+        t = [ms for k, ms in self.records if k == name]
+        return (sum(t), len(t))
