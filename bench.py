@@ -39,7 +39,7 @@ UNIT = "Mfaces·px/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4", choices=sorted(S.CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -91,6 +91,7 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        time.sleep(0.5)  # let nvidia-smi start sampling before the timed region begins
         return self
 
     def __exit__(self, *exc):
