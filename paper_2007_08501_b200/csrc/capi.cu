@@ -82,7 +82,7 @@ struct Plan {
   int bs = 0;  // bin side used by the fine stage (16 when naive)
   bool binned = false;
   int nbx = 0, nby = 0, cap = 0;
-  size_t off_ibbox = 0, off_counts = 0, off_lists = 0, total = 0;
+  size_t off_ibbox = 0, off_counter = 0, off_counts = 0, off_lists = 0, total = 0;
 };
 
 int auto_cap(int64_t F) { return (int)std::max<int64_t>(1, std::min<int64_t>(F, 4096)); }
@@ -113,6 +113,8 @@ int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
   size_t off = 0;
   p.off_ibbox = off;
   off = align_up(off + sizeof(int4) * (size_t)std::max<int64_t>(F, 1));
+  p.off_counter = off;
+  off = align_up(off + sizeof(unsigned long long));
   p.off_counts = off;
   if (p.binned) {
     off = align_up(off + sizeof(int) * (size_t)N * p.nbx * p.nby);
@@ -196,29 +198,30 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   A.znear = s->znear;
   A.persp = s->perspective_correct != 0;
   A.clip = s->clip_barycentric_coords != 0;
-  // sub-tile: 16x16 pixels (8 warps) by default; narrower for small bins and for large K (shared-memory top-K)
-  int stw = std::min(16, (p.bs + 7) / 8 * 8), sth = std::min(16, (p.bs + 3) / 4 * 4);
-  if (p.K > 16) {
-    // K * threads * 12 B of top-K storage must fit next to the staged faces
-    while (stw * sth > 32 && (size_t)p.K * stw * sth * 12 + (size_t)stw * sth * drb::staged_face_bytes() > 200 * 1024) {
-      if (sth >= stw && sth > 4) sth /= 2;
-      else if (stw > 8) stw /= 2;
-      else break;
+  // K2 is a persistent grid of warps pulling 8x4 micro-tiles; pick the CTA size (warps) that fits the most
+  // warps per SM given each warp's shared memory (staged-face ring + K*32 top-K entries).
+  const size_t per_warp = drb::fine_warp_smem_bytes(p.K);
+  int nw = 0, best = 0;
+  for (int cand : {8, 4, 2, 1}) {
+    size_t cta = (size_t)cand * per_warp + 1024;
+    int ctas = (int)std::min<size_t>(228 * 1024 / cta, 32);
+    if (cand * per_warp > 227 * 1024) ctas = 0;
+    if (ctas * cand > best) {
+      best = ctas * cand;
+      nw = cand;
     }
-    if ((size_t)p.K * stw * sth * 12 + (size_t)stw * sth * drb::staged_face_bytes() > 220 * 1024)
-      return fail(DR_ERR_RANGE, "faces_per_pixel=%d too large for the shared-memory top-K", p.K);
   }
-  A.stw = stw;
-  A.sth = sth;
-  A.staged_bytes = (size_t)stw * sth * drb::staged_face_bytes();
+  if (nw == 0) return fail(DR_ERR_RANGE, "faces_per_pixel=%d too large for the shared-memory top-K", p.K);
+  A.N = (int)N;
+  A.work_counter = reinterpret_cast<unsigned long long*>(base + p.off_counter);
   A.p2f = p2f;
   A.zbuf = zbuf;
   A.bary = bary;
   A.dists = dists;
-  cudaError_t e;
-  {
+  cudaError_t e = cudaMemsetAsync(A.work_counter, 0, sizeof(unsigned long long), st);
+  if (e == cudaSuccess) {
     ProfScope ps(st, KN_FINE);
-    e = drb::launch_fine(A, (int64_t)N * p.nbx * p.nby, st);
+    e = drb::launch_fine(A, nw, st);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "rasterize_meshes forward");

@@ -144,108 +144,92 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
 }
 
 // ------------------------------------------------------------------------------------------------
-// K2: fine rasterization
+// K2: fine rasterization — warp-autonomous, (face, pixel) pairs evaluated lane-parallel
+//
+// Work item = one 8x4 pixel micro-tile of one bin of one mesh. Warps of a persistent grid pull items from a
+// global counter (consecutive items = micro-tiles of the same bin, so concurrently running warps share the
+// bin's list in L1/L2), and never synchronise with each other: no CTA barrier, no idle lanes while a slow
+// neighbour finishes.
+//
+// Per item the warp streams the bin's face list (or the whole mesh: naive mode / overflowed bin) 32 faces
+// at a time: each lane intersects one face's exact integer pixel range (K0) with the micro-tile; faces that
+// touch it are compacted (ballot + popc) into a warp-private ring in shared memory together with their
+// per-face invariants (structure-of-arrays) and their covered pixel rectangle. Every 32 staged faces the warp
+// enumerates their (face, pixel) pairs — prefix sum of the rectangle areas across lanes, then 32 pairs per
+// step, one per lane (binary search over the prefix with shuffles) — so every lane evaluates a pair
+// (MR:166-176) regardless of how small the triangles are. Passing candidates go into the pixel's sorted
+// (z, id) list in shared memory; lanes that hit the same pixel in one step insert one after another
+// (__match_any_sync ranks). Winners' bary / dists are recomputed with the identical operation sequence at
+// emit time (MR:178-197), so the payload carries exactly the bits the candidate test produced.
 
-// Staged face: geometry + invariants (FaceGeom) + integer pixel range. Every lane of a warp reads the same
-// record at the same time (shared-memory broadcast), so array-of-structs costs no bank conflicts.
-struct __align__(16) StagedFace {
-  double ax, ay, bx, by, cx, cy;
-  double z0, z1, z2;
-  double abx, aby, bcx, bcy, cax, cay;
-  double lab, lbc, lca;
-  double area;
-  int32_t fid;
-  int32_t _pad;
-  int4 ib;
+constexpr int kNF = 19;    // staged fp64 fields per face
+constexpr int kRing = 64;  // staged faces per warp (< 32 pending + 32 new)
+
+enum : int {
+  F_AX, F_AY, F_BX, F_BY, F_CX, F_CY, F_Z0, F_Z1, F_Z2,
+  F_ABX, F_ABY, F_BCX, F_BCY, F_CAX, F_CAY, F_LAB, F_LBC, F_LCA, F_AREA
 };
 
-__device__ __forceinline__ void stage_face(StagedFace& s, const double* fv, int32_t fid, int4 ib) {
-  double v[9];
-  const double* p = fv + 9 * (int64_t)fid;
+// one warp's shared memory: staged-face ring (SoA) + top-K lists of its 32 pixels
+struct WarpSmem {
+  double* d;        // [kNF][kRing]
+  int32_t* fid;     // [kRing]
+  uint32_t* rect;   // [kRing] covered rectangle in the micro-tile: r0 | c0<<4 | h<<8 | w<<12 | recip(w)<<16
+  double* tz;       // [K][32]
+  int32_t* tid;     // [K][32]
+
+  __device__ __forceinline__ double get(int f, int k) const { return d[f * kRing + k]; }
+  __device__ __forceinline__ void put(int f, int k, double v) const { d[f * kRing + k] = v; }
+  __device__ __forceinline__ FaceGeom geom(int k) const {
+    FaceGeom g;
+    g.a = V2{get(F_AX, k), get(F_AY, k)};
+    g.b = V2{get(F_BX, k), get(F_BY, k)};
+    g.c = V2{get(F_CX, k), get(F_CY, k)};
+    g.z0 = get(F_Z0, k);
+    g.z1 = get(F_Z1, k);
+    g.z2 = get(F_Z2, k);
+    g.ab = V2{get(F_ABX, k), get(F_ABY, k)};
+    g.bc = V2{get(F_BCX, k), get(F_BCY, k)};
+    g.ca = V2{get(F_CAX, k), get(F_CAY, k)};
+    g.len_ab = get(F_LAB, k);
+    g.len_bc = get(F_LBC, k);
+    g.len_ca = get(F_LCA, k);
+    g.area = get(F_AREA, k);
+    return g;
+  }
+  __device__ __forceinline__ void stage(int k, const double* fv, int32_t f, uint32_t r) const {
+    double v[9];
+    const double* p = fv + 9 * (int64_t)f;
 #pragma unroll
-  for (int k = 0; k < 9; ++k) v[k] = __ldg(p + k);
-  FaceGeom g = make_face_geom(v);
-  s.ax = g.a.x; s.ay = g.a.y; s.bx = g.b.x; s.by = g.b.y; s.cx = g.c.x; s.cy = g.c.y;
-  s.z0 = g.z0; s.z1 = g.z1; s.z2 = g.z2;
-  s.abx = g.ab.x; s.aby = g.ab.y; s.bcx = g.bc.x; s.bcy = g.bc.y; s.cax = g.ca.x; s.cay = g.ca.y;
-  s.lab = g.len_ab; s.lbc = g.len_bc; s.lca = g.len_ca;
-  s.area = g.area;
-  s.fid = fid;
-  s.ib = ib;
+    for (int t = 0; t < 9; ++t) v[t] = __ldg(p + t);
+    const FaceGeom g = make_face_geom(v);
+    put(F_AX, k, g.a.x); put(F_AY, k, g.a.y); put(F_BX, k, g.b.x); put(F_BY, k, g.b.y);
+    put(F_CX, k, g.c.x); put(F_CY, k, g.c.y); put(F_Z0, k, g.z0); put(F_Z1, k, g.z1); put(F_Z2, k, g.z2);
+    put(F_ABX, k, g.ab.x); put(F_ABY, k, g.ab.y); put(F_BCX, k, g.bc.x); put(F_BCY, k, g.bc.y);
+    put(F_CAX, k, g.ca.x); put(F_CAY, k, g.ca.y);
+    put(F_LAB, k, g.len_ab); put(F_LBC, k, g.len_bc); put(F_LCA, k, g.len_ca); put(F_AREA, k, g.area);
+    fid[k] = f;
+    rect[k] = r;
+  }
+};
+
+__host__ __device__ constexpr size_t warp_smem_bytes(int K) {
+  return (size_t)kNF * kRing * sizeof(double) + (size_t)kRing * (sizeof(int32_t) + sizeof(uint32_t)) +
+         (size_t)K * 32 * (sizeof(double) + sizeof(int32_t));
 }
 
-__device__ __forceinline__ FaceGeom load_geom(const StagedFace& s) {
-  FaceGeom g;
-  g.a = V2{s.ax, s.ay}; g.b = V2{s.bx, s.by}; g.c = V2{s.cx, s.cy};
-  g.z0 = s.z0; g.z1 = s.z1; g.z2 = s.z2;
-  g.ab = V2{s.abx, s.aby}; g.bc = V2{s.bcx, s.bcy}; g.ca = V2{s.cax, s.cay};
-  g.len_ab = s.lab; g.len_bc = s.lbc; g.len_ca = s.lca;
-  g.area = s.area;
-  return g;
+// Rectangle of the micro-tile (rows i0..i0+3, cols j0..j0+7, limited to vh x vw existing pixels) covered by
+// the pixel range `ib`; 0 if none. Packed as r0 | c0<<4 | h<<8 | w<<12 | ceil(256/w)<<16: the pair
+// rank -> (rank / w, rank % w) split uses (rank * ceil(256/w)) >> 8, exact for rank < 32 and w <= 8.
+__device__ __forceinline__ uint32_t cover_rect(int4 ib, int i0, int j0, int vh, int vw) {
+  const int r0 = max(ib.x - i0, 0), r1 = min(ib.y - i0, vh - 1);
+  const int c0 = max(ib.z - j0, 0), c1 = min(ib.w - j0, vw - 1);
+  if (ib.x > ib.y || r0 > r1 || c0 > c1) return 0u;
+  const uint32_t h = (uint32_t)(r1 - r0 + 1), w = (uint32_t)(c1 - c0 + 1);
+  return (uint32_t)r0 | ((uint32_t)c0 << 4) | (h << 8) | (w << 12) | (((255u + w) / w) << 16);
 }
 
-// Register-resident bounded sorted list of the K smallest (z, id) keys, KMAX >= K at compile time.
-// Unused slots hold the sentinel (+inf, INT_MAX), which compares greater than any real candidate; all
-// indexing is compile-time (fully unrolled) so the list never spills to local memory.
-template <int KMAX>
-struct RegTopK {
-  double z[KMAX];
-  int32_t id[KMAX];
-  __device__ __forceinline__ void reset() {
-#pragma unroll
-    for (int s = 0; s < KMAX; ++s) {
-      z[s] = __longlong_as_double(0x7ff0000000000000LL);
-      id[s] = INT_MAX;
-    }
-  }
-  // insertion into a sorted array, walking from the tail: slot s takes slot s-1 if the candidate sorts
-  // before it, else the candidate if it sorts before the old slot s. Slots >= K are never written.
-  __device__ __forceinline__ void insert(double zc, int32_t ic, int K) {
-#pragma unroll
-    for (int s = KMAX - 1; s >= 0; --s) {
-      if (s < K) {
-        const int sp = s > 0 ? s - 1 : 0;
-        const bool lt_prev = s > 0 && cand_less(zc, ic, z[sp], id[sp]);
-        const bool lt_cur = cand_less(zc, ic, z[s], id[s]);
-        if (lt_prev) {
-          z[s] = z[sp];
-          id[s] = id[sp];
-        } else if (lt_cur) {
-          z[s] = zc;
-          id[s] = ic;
-        }
-      }
-    }
-  }
-};
-
-// Shared-memory bounded sorted list (large K): column `tid` of [K][nthreads] arrays.
-struct SmemTopK {
-  double* z;
-  int32_t* id;
-  int stride;
-  int n;
-  __device__ __forceinline__ void reset() { n = 0; }
-  __device__ __forceinline__ void insert(double zc, int32_t ic, int K) {
-    int m = n;
-    if (m == K) {
-      if (!cand_less(zc, ic, z[(K - 1) * stride], id[(K - 1) * stride])) return;
-      m = K - 1;
-    }
-    int pos = m;
-    while (pos > 0) {
-      double zp = z[(pos - 1) * stride];
-      int32_t ip = id[(pos - 1) * stride];
-      if (!cand_less(zc, ic, zp, ip)) break;
-      z[pos * stride] = zp;
-      id[pos * stride] = ip;
-      --pos;
-    }
-    z[pos * stride] = zc;
-    id[pos * stride] = ic;
-    n = m + 1;
-  }
-};
+__device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
 template <typename OutT>
 __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot, bool occupied, double z,
@@ -255,7 +239,7 @@ __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot,
     const double* p = A.fv + 9 * (int64_t)fid;
 #pragma unroll
     for (int k = 0; k < 9; ++k) v[k] = __ldg(p + k);
-    FaceGeom g = make_face_geom(v);
+    const FaceGeom g = make_face_geom(v);
     PixelFaceResult r;
     eval_pixel_face<true>(V2{px, py}, g, A.blur, A.znear, A.persp, A.clip, r);  // same ops => same bits
     A.p2f[slot] = fid;
@@ -274,115 +258,164 @@ __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot,
   }
 }
 
-// emit_pixel (MR:178-197): slots in ascending (z, id); bary/dists of the winners are recomputed with the
-// identical operation sequence, so they carry the bits the candidate test produced.
-template <typename OutT, int KMAX>
-__device__ __forceinline__ void emit_pixel(const FineArgs<OutT>& A, const RegTopK<KMAX>& tk, int b, int i, int j,
-                                           double px, double py) {
-  const int64_t slot0 = (((int64_t)b * A.H + i) * A.W + j) * A.K;
-#pragma unroll
-  for (int s = 0; s < KMAX; ++s)
-    if (s < A.K) emit_slot<OutT>(A, slot0 + s, tk.id[s] != INT_MAX, tk.z[s], tk.id[s], px, py);
-}
+// Evaluate the pairs of ring slots [head, head+G) (mod kRing) and insert the survivors.
 template <typename OutT>
-__device__ __forceinline__ void emit_pixel(const FineArgs<OutT>& A, const SmemTopK& tk, int b, int i, int j,
-                                           double px, double py) {
-  const int64_t slot0 = (((int64_t)b * A.H + i) * A.W + j) * A.K;
-  for (int s = 0; s < A.K; ++s) {
-    const bool occ = s < tk.n;
-    emit_slot<OutT>(A, slot0 + s, occ, occ ? tk.z[s * tk.stride] : 0.0, occ ? tk.id[s * tk.stride] : -1, px, py);
+__device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const WarpSmem& ws, int head, int G, int mi0,
+                                              int mj0, int lane) {
+  const int K = A.K;
+  const int slot_l = (head + lane) & (kRing - 1);
+  const uint32_t rl = lane < G ? ws.rect[slot_l] : 0u;
+  const int cnt = (int)(((rl >> 8) & 15u) * ((rl >> 12) & 15u));
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
   }
-}
-
-// One CTA per (mesh b, bin). The bin is covered by sub-tiles of stw x sth pixels; each warp owns an 8x4
-// micro-tile of the sub-tile (compact footprint => lanes share the faces they test). For every sub-tile the
-// CTA streams its candidate faces through shared memory in chunks of blockDim faces, keeping only those
-// whose integer pixel range meets the sub-tile (ballot + popc compaction), then every lane tests the staged
-// faces against its pixel and keeps its top-K.
-template <typename OutT, typename TopK, int KMAX>
-__global__ void __launch_bounds__(256) k_fine(FineArgs<OutT> A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  StagedFace* staged = reinterpret_cast<StagedFace*>(smem_raw);
-  __shared__ int warp_cnt[8];
-
-  const int nbins = A.nbx * A.nby;
-  const int b = blockIdx.x / nbins;
-  const int bin = blockIdx.x % nbins;
-  const int by = bin / A.nbx, bx = bin % A.nbx;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nthreads = blockDim.x;
-  const int nwarps = nthreads >> 5;
-
-  // bin pixel rectangle (clipped to the image)
-  const int bi0 = by * A.bs, bj0 = bx * A.bs;
-  const int bi1 = min(A.H, bi0 + A.bs) - 1, bj1 = min(A.W, bj0 + A.bs) - 1;
-
-  // candidate face source
-  const int64_t f0 = A.first[b], nf = A.num[b];
-  const int32_t* list = nullptr;
-  int64_t nsrc = nf;
-  if (A.binned) {
-    int c = A.bin_counts[(int64_t)b * nbins + bin];
-    if (c <= A.cap) {
-      list = A.bin_lists + ((int64_t)b * nbins + bin) * A.cap;
-      nsrc = c;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int base = 0; base < total; base += 32) {
+    const int j = base + lane;
+    const bool act = j < total;
+    // face lane = first lane whose inclusive prefix exceeds j
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const int pv = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+      if (pv <= j) lo += step;
     }
-  }
-
-  TopK tk;
-  if constexpr (KMAX == 0) {
-    double* zs = reinterpret_cast<double*>(smem_raw + A.staged_bytes);
-    tk.z = zs + tid;
-    tk.id = reinterpret_cast<int32_t*>(zs + (size_t)A.K * nthreads) + tid;
-    tk.stride = nthreads;
-  }
-
-  const int mt_w = A.stw >> 3;  // micro-tiles per sub-tile row
-  for (int si = bi0; si <= bi1; si += A.sth) {
-    for (int sj = bj0; sj <= bj1; sj += A.stw) {
-      const int si1 = min(bi1, si + A.sth - 1), sj1 = min(bj1, sj + A.stw - 1);
-      const int i = si + (wid / mt_w) * 4 + (lane >> 3);
-      const int j = sj + (wid % mt_w) * 8 + (lane & 7);
-      const bool valid = i <= si1 && j <= sj1;
-      const double px = pixel_x(A.W, j), py = pixel_y(A.H, i);
-      tk.reset();
-
-      for (int64_t c0 = 0; c0 < nsrc; c0 += nthreads) {
-        // ---- stage: filter candidates against the sub-tile, compact, load geometry
-        const int64_t ci = c0 + tid;
-        int32_t fid = -1;
-        int4 ib = make_int4(1, 0, 1, 0);
-        if (ci < nsrc) {
-          fid = list ? list[ci] : (int32_t)(f0 + ci);
-          ib = A.ibbox[fid];
-        }
-        const bool keep = ib.x <= ib.y && ib.y >= si && ib.x <= si1 && ib.w >= sj && ib.z <= sj1;
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) warp_cnt[wid] = __popc(bal);
-        __syncthreads();
-        int off = 0, tot = 0;
-        for (int w = 0; w < nwarps; ++w) {
-          int cw = warp_cnt[w];
-          off += w < wid ? cw : 0;
-          tot += cw;
-        }
-        if (keep) stage_face(staged[off + __popc(bal & ((1u << lane) - 1u))], A.fv, fid, ib);
-        __syncthreads();
-        // ---- test the staged faces against this lane's pixel
-        if (valid) {
-          for (int k = 0; k < tot; ++k) {
-            const int4 fb = staged[k].ib;
-            if (i < fb.x || i > fb.y || j < fb.z || j > fb.w) continue;
-            const FaceGeom g = load_geom(staged[k]);
-            PixelFaceResult r;
-            if (eval_pixel_face<false>(V2{px, py}, g, A.blur, A.znear, A.persp, A.clip, r))
-              tk.insert(r.z, staged[k].fid, A.K);
+    lo = min(lo, 31);
+    const int excl = __shfl_sync(0xffffffffu, incl - cnt, lo);
+    const uint32_t r = __shfl_sync(0xffffffffu, rl, lo);
+    bool pass = false;
+    int p = 0;
+    int32_t f = 0;
+    PixelFaceResult res;
+    if (act) {
+      const int rank = j - excl;
+      const int w = (int)((r >> 12) & 15u);
+      const int dr = (rank * (int)(r >> 16)) >> 8;
+      const int row = (int)(r & 15u) + dr;
+      const int col = (int)((r >> 4) & 15u) + (rank - dr * w);
+      p = row * 8 + col;
+      const int k = (head + lo) & (kRing - 1);
+      const FaceGeom fg = ws.geom(k);
+      const V2 pix{pixel_x(A.W, mj0 + col), pixel_y(A.H, mi0 + row)};
+      pass = eval_pixel_face<false>(pix, fg, A.blur, A.znear, A.persp, A.clip, res);
+      f = ws.fid[k];
+    }
+    if (__any_sync(0xffffffffu, pass)) {
+      const unsigned peers = __match_any_sync(0xffffffffu, pass ? p : 32 + lane);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      const int maxr = __reduce_max_sync(0xffffffffu, pass ? rank : 0);
+      for (int rr = 0; rr <= maxr; ++rr) {
+        if (pass && rank == rr) {
+          const double zc = res.z;
+          if (cand_less(zc, f, ws.tz[(K - 1) * 32 + p], ws.tid[(K - 1) * 32 + p])) {
+            int s = K - 1;
+            while (s > 0) {
+              const double zp = ws.tz[(s - 1) * 32 + p];
+              const int32_t ip = ws.tid[(s - 1) * 32 + p];
+              if (!cand_less(zc, f, zp, ip)) break;
+              ws.tz[s * 32 + p] = zp;
+              ws.tid[s * 32 + p] = ip;
+              --s;
+            }
+            ws.tz[s * 32 + p] = zc;
+            ws.tid[s * 32 + p] = f;
           }
         }
-        __syncthreads();
+        __syncwarp();
       }
-      if (valid) emit_pixel(A, tk, b, i, j, px, py);
     }
+  }
+}
+
+template <typename OutT, int NW>
+__global__ void __launch_bounds__(NW * 32) k_fine(FineArgs<OutT> A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int K = A.K;
+  WarpSmem ws;
+  {
+    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(K);
+    ws.d = reinterpret_cast<double*>(base);
+    ws.tz = ws.d + kNF * kRing;
+    ws.fid = reinterpret_cast<int32_t*>(ws.tz + K * 32);
+    ws.tid = ws.fid + kRing;
+    ws.rect = reinterpret_cast<uint32_t*>(ws.tid + K * 32);
+  }
+  const int nbins = A.nbx * A.nby;
+  const int mtx = (A.bs + 7) >> 3, mty = (A.bs + 3) >> 2;  // micro-tiles per bin row / column
+  const int mt_per_bin = mtx * mty;
+  const int64_t n_items = (int64_t)A.N * nbins * mt_per_bin;
+
+  for (;;) {
+    int64_t item = 0;
+    if (lane == 0) item = (int64_t)atomicAdd(A.work_counter, 1ull);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int mt = (int)(item % mt_per_bin);
+    const int64_t bb = item / mt_per_bin;
+    const int bin = (int)(bb % nbins);
+    const int b = (int)(bb / nbins);
+    const int by = bin / A.nbx, bx = bin % A.nbx;
+    const int bi0 = by * A.bs, bj0 = bx * A.bs;
+    const int bi1 = min(A.H, bi0 + A.bs) - 1, bj1 = min(A.W, bj0 + A.bs) - 1;
+    const int mi0 = bi0 + (mt / mtx) * 4, mj0 = bj0 + (mt % mtx) * 8;
+    const int vh = min(4, bi1 - mi0 + 1), vw = min(8, bj1 - mj0 + 1);  // existing pixels of the micro-tile
+    if (vh <= 0 || vw <= 0) continue;
+
+    // candidate faces: the bin list, or the whole mesh (naive mode / overflowed bin)
+    const int64_t f0 = A.first[b], nf = A.num[b];
+    const int32_t* list = nullptr;
+    int64_t nsrc = nf;
+    if (A.binned) {
+      const int c = A.bin_counts[(int64_t)b * nbins + bin];
+      if (c <= A.cap) {
+        list = A.bin_lists + ((int64_t)b * nbins + bin) * A.cap;
+        nsrc = c;
+      }
+    }
+    for (int s = 0; s < K; ++s) {
+      ws.tz[s * 32 + lane] = pos_inf();
+      ws.tid[s * 32 + lane] = INT_MAX;
+    }
+    __syncwarp();
+
+    int head = 0, pending = 0;
+    for (int64_t c0 = 0; c0 < nsrc; c0 += 32) {
+      const int64_t ci = c0 + lane;
+      uint32_t r = 0u;
+      int32_t fid = -1;
+      if (ci < nsrc) {
+        fid = list ? list[ci] : (int32_t)(f0 + ci);
+        r = cover_rect(A.ibbox[fid], mi0, mj0, vh, vw);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, r != 0u);
+      if (r) ws.stage((head + pending + __popc(bal & ((1u << lane) - 1u))) & (kRing - 1), A.fv, fid, r);
+      pending += __popc(bal);
+      __syncwarp();
+      const bool last = c0 + 32 >= nsrc;
+      while (pending >= 32 || (last && pending > 0)) {
+        const int G = min(pending, 32);
+        process_group(A, ws, head, G, mi0, mj0, lane);
+        head = (head + G) & (kRing - 1);
+        pending -= G;
+      }
+    }
+    __syncwarp();
+    // emit this lane's pixel (MR:178-197)
+    const int row = lane >> 3, col = lane & 7;
+    if (row < vh && col < vw) {
+      const int pi = mi0 + row, pj = mj0 + col;
+      const double px = pixel_x(A.W, pj), py = pixel_y(A.H, pi);
+      const int64_t slot0 = (((int64_t)b * A.H + pi) * A.W + pj) * K;
+      for (int s = 0; s < K; ++s) {
+        const int32_t f = ws.tid[s * 32 + lane];
+        emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, px, py);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -405,32 +438,31 @@ void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* nu
 }
 
 template <typename OutT>
-static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int64_t nblocks, cudaStream_t st) {
-  const int nthreads = (A.stw / 8) * (A.sth / 4) * 32;
-  size_t smem = A.staged_bytes;
-  const int K = A.K;
-  auto go = [&](auto kern, size_t extra) -> cudaError_t {
-    size_t total = smem + extra;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)total);
+static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t st) {
+  const size_t smem = (size_t)nw * warp_smem_bytes(A.K);
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)nblocks, nthreads, total, st>>>(A);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    kern<<<(unsigned)(sms * per_sm), nw * 32, smem, st>>>(A);  // persistent: warps pull micro-tiles
     return cudaGetLastError();
   };
-  if (K <= 1) return go(k_fine<OutT, RegTopK<1>, 1>, 0);
-  if (K <= 2) return go(k_fine<OutT, RegTopK<2>, 2>, 0);
-  if (K <= 4) return go(k_fine<OutT, RegTopK<4>, 4>, 0);
-  if (K <= 8) return go(k_fine<OutT, RegTopK<8>, 8>, 0);
-  if (K <= 16) return go(k_fine<OutT, RegTopK<16>, 16>, 0);
-  return go(k_fine<OutT, SmemTopK, 0>, (size_t)K * nthreads * (sizeof(double) + sizeof(int32_t)));
+  switch (nw) {
+    case 8: return go(k_fine<OutT, 8>);
+    case 4: return go(k_fine<OutT, 4>);
+    case 2: return go(k_fine<OutT, 2>);
+    default: return go(k_fine<OutT, 1>);
+  }
 }
 
-cudaError_t launch_fine(const FineArgs<float>& A, int64_t nblocks, cudaStream_t st) {
-  return launch_fine_t(A, nblocks, st);
-}
-cudaError_t launch_fine(const FineArgs<double>& A, int64_t nblocks, cudaStream_t st) {
-  return launch_fine_t(A, nblocks, st);
-}
+size_t fine_warp_smem_bytes(int K) { return warp_smem_bytes(K); }
 
-size_t staged_face_bytes() { return sizeof(StagedFace); }
+cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st) { return launch_fine_t(A, nwarps, st); }
+cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st) { return launch_fine_t(A, nwarps, st); }
 
 }  // namespace drb

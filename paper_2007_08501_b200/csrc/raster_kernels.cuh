@@ -22,8 +22,8 @@ struct FineArgs {
   int H, W, K;
   double blur, znear;
   bool persp, clip;
-  int stw, sth;             // sub-tile (pixels handled concurrently by the CTA): multiples of 8 x 4
-  size_t staged_bytes;      // dynamic smem for the staged-face ring (blockDim faces)
+  int N;
+  unsigned long long* work_counter;  // zeroed before launch; warps pull micro-tiles from it
   int64_t* p2f;
   OutT* zbuf;
   OutT* bary;
@@ -49,10 +49,10 @@ void launch_face_setup(const double* fv, int64_t F, int H, int W, double inflate
                        int4* ibbox, cudaStream_t st);
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
                       int bs, int nbx, int nby, int cap, int* counts, int32_t* lists, cudaStream_t st);
-cudaError_t launch_fine(const FineArgs<float>& A, int64_t nblocks, cudaStream_t st);
-cudaError_t launch_fine(const FineArgs<double>& A, int64_t nblocks, cudaStream_t st);
+cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);
+cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st);
 cudaError_t launch_backward(const BwdArgs<double>& A, cudaStream_t st);
-size_t staged_face_bytes();
+size_t fine_warp_smem_bytes(int K);  // shared memory one warp of K2 needs
 
 }  // namespace drb
