@@ -8,7 +8,9 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdr_raster_b200.so")
+# DR_RASTER_LIB overrides the in-tree library (used to A/B build variants; the default is the product build)
+LIB_PATH = os.environ.get("DR_RASTER_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                           "libdr_raster_b200.so")
 
 DR_OK, DR_ERR_SHAPE, DR_ERR_INDEX, DR_ERR_RANGE, DR_ERR_CUDA, DR_ERR_OOM, DR_ERR_USAGE = range(7)
 

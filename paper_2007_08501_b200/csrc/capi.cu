@@ -202,7 +202,7 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   // warps per SM given each warp's shared memory (staged-face ring + K*32 top-K entries).
   const size_t per_warp = drb::fine_warp_smem_bytes(p.K);
   int nw = 0, best = 0;
-  for (int cand : {8, 4, 2, 1}) {
+  for (int cand : {8, 2}) {  // CTA sizes K2 is instantiated for
     size_t cta = (size_t)cand * per_warp + 1024;
     int ctas = (int)std::min<size_t>(228 * 1024 / cta, 32);
     if (cand * per_warp > 227 * 1024) ctas = 0;

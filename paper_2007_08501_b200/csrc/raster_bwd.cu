@@ -3,7 +3,8 @@
 // One thread per fragment slot recomputes the slot's NDC triangle and pixel centre, pulls the cotangents on
 // zbuf / bary / dists back through z-interpolation, clamp+renormalise, (optional) perspective correction,
 // the barycentric quotient and the frozen-edge distance envelope, and produces the 9 cotangents of its
-// face's (x_ndc, y_ndc, z_view) x 3 vertices. Lanes of a warp that hit the same face (neighbouring pixels
+// face's (x_ndc, y_ndc, z_view) x 3 vertices; empty slots are compacted away first (ballot queue). Lanes of a
+// warp that hit the same face (neighbouring pixels
 // very often do) are grouped with __match_any_sync and summed with a log-depth shuffle reduction, so ONE
 // lane issues the 9 fp64 atomicAdds per (warp, face) instead of one per slot. The reference reduces per
 // vertex in slot order on one thread (MR:380-392); here the order of fp64 additions is not fixed.
@@ -24,11 +25,11 @@ __device__ __forceinline__ void clamp_bary_backward(const double wr[3], const do
     out[0] = out[1] = out[2] = 0.0;
     return;
   }
-  double h0 = t0 / s, h1 = t1 / s, h2 = t2 / s;
+  double h0 = qdiv(t0, s), h1 = qdiv(t1, s), h2 = qdiv(t2, s);
   double d = dc[0] * h0 + dc[1] * h1 + dc[2] * h2;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    double d_t = (dc[i] - d) / s;
+    double d_t = qdiv(dc[i] - d, s);
     out[i] = (wr[i] > 0.0 && wr[i] < 1.0) ? d_t : 0.0;
   }
 }
@@ -69,10 +70,10 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slo
     if (den > kPerspEps) {
       const double du_u = d_u[0] * u[0] + d_u[1] * u[1] + d_u[2] * u[2];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) d_top[k] = (d_u[k] - du_u) / den;
+      for (int k = 0; k < 3; ++k) d_top[k] = qdiv(d_u[k] - du_u, den);
     } else {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) d_top[k] = d_u[k] / kPerspEps;
+      for (int k = 0; k < 3; ++k) d_top[k] = qdiv(d_u[k], kPerspEps);
     }
     d_w[0] = d_top[0] * z[1] * z[2];
     d_w[1] = d_top[1] * z[0] * z[2];
@@ -131,45 +132,91 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slo
   }
 }
 
+// Sum g[9] over the lanes of each __match_any_sync(fid) group (log-depth shuffle tree); returns true on the
+// group's lowest lane, which then owns the group total.
+__device__ __forceinline__ bool reduce_by_face(int32_t fid, int lane, double g[9]) {
+  const int key = fid >= 0 ? fid : -1 - lane;  // inactive lanes form singleton groups that never write
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  unsigned rel = __popc(peers & ((1u << lane) - 1u));
+  unsigned rem = peers & ~((2u << lane) - 1u);  // peers above this lane (2u << 31 == 0)
+  while (__any_sync(0xffffffffu, rem != 0)) {
+    const int next = __ffs(rem);  // 1-based lane of the next peer, 0 if none
+    const int src = next ? next - 1 : lane;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const double t = __shfl_sync(0xffffffffu, g[k], src);
+      if (next) g[k] += t;
+    }
+    rem &= ~__ballot_sync(0xffffffffu, rel & 1u);
+    rel >>= 1;
+  }
+  return fid >= 0 && (peers & ((1u << lane) - 1u)) == 0;
+}
+
+// Persistent warps walk the slots in chunks of kChunk consecutive slots. Occupied slots (pix_to_face >= 0;
+// typically 40-70 % of them) are compacted with ballot + popc into a warp-private queue and processed 32 at
+// a time, so every lane of a batch does a full per-slot backward.
+constexpr int kBwdChunk = 32 * 16;
+
+#ifndef DR_BWD_THREADS
+#define DR_BWD_THREADS 128
+#endif
+#ifndef DR_BWD_MINBLOCKS
+#define DR_BWD_MINBLOCKS 6
+#endif
+// 128-thread CTAs capped at 80 registers (6 CTAs = 24 warps per SM): the per-slot fp64 chain is latency-bound
+// and more resident warps beat the small (L1-resident) spill this cap causes — measured 6.8 ms (126 regs,
+// 16 warps) -> 5.7 ms on C4 (profiles/r01/README.md).
+constexpr int kBwdThreads = DR_BWD_THREADS;
+
 template <typename InT>
-__global__ void __launch_bounds__(256) k_backward(BwdArgs<InT> A) {
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdArgs<InT> A) {
+  __shared__ int64_t q_slot[kBwdThreads / 32][64];
+  __shared__ int32_t q_fid[kBwdThreads / 32][64];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = warp * 32; base < A.S; base += nwarps * 32) {
-    const int64_t slot = base + lane;
-    int32_t fid = -1;
-    if (slot < A.S) {
-      int64_t f = A.p2f[slot];
-      if (f >= 0 && f < A.F) fid = (int32_t)f;
-    }
-    double g[9];
-    if (fid >= 0) {
-      slot_backward(A, slot, fid, g);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 9; ++k) g[k] = 0.0;
-    }
-    // group lanes by face; empty slots form per-lane singleton groups that never write
-    const int key = fid >= 0 ? fid : -1 - lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    unsigned rel = __popc(peers & ((1u << lane) - 1u));
-    unsigned rem = peers & ~((2u << lane) - 1u);  // peers above this lane (2u << 31 == 0)
-    while (__any_sync(0xffffffffu, rem != 0)) {
-      const int next = __ffs(rem);  // 1-based lane of the next peer, 0 if none
-      const int src = next ? next - 1 : lane;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const double t = __shfl_sync(0xffffffffu, g[k], src);
-        if (next) g[k] += t;
+  int64_t* qs = q_slot[wid];
+  int32_t* qf = q_fid[wid];
+  for (int64_t c0 = warp * kBwdChunk; c0 < A.S; c0 += nwarps * kBwdChunk) {
+    const int64_t c1 = c0 + kBwdChunk < A.S ? c0 + kBwdChunk : A.S;
+    int pending = 0;
+    for (int64_t s0 = c0; s0 < c1; s0 += 32) {
+      const int64_t slot = s0 + lane;
+      int32_t fid = -1;
+      if (slot < c1) {
+        const int64_t f = A.p2f[slot];
+        if (f >= 0 && f < A.F) fid = (int32_t)f;
       }
-      rem &= ~__ballot_sync(0xffffffffu, rel & 1u);
-      rel >>= 1;
-    }
-    if (fid >= 0 && (peers & ((1u << lane) - 1u)) == 0) {
-      double* out = A.grad + 9 * (int64_t)fid;
+      const unsigned occ = __ballot_sync(0xffffffffu, fid >= 0);
+      if (fid >= 0) {
+        const int pos = pending + __popc(occ & ((1u << lane) - 1u));
+        qs[pos] = slot;
+        qf[pos] = fid;
+      }
+      pending += __popc(occ);
+      __syncwarp();
+      const bool last = s0 + 32 >= c1;
+      while (pending >= 32 || (last && pending > 0)) {
+        const int nb = pending < 32 ? pending : 32;
+        pending -= nb;
+        const bool act = lane < nb;
+        const int64_t my_slot = act ? qs[pending + lane] : 0;
+        const int32_t my_fid = act ? qf[pending + lane] : -1;
+        __syncwarp();
+        double g[9];
+        if (act) {
+          slot_backward(A, my_slot, my_fid, g);
+        } else {
 #pragma unroll
-      for (int k = 0; k < 9; ++k) atomicAdd(out + k, g[k]);
+          for (int k = 0; k < 9; ++k) g[k] = 0.0;
+        }
+        if (reduce_by_face(my_fid, lane, g)) {
+          double* out = A.grad + 9 * (int64_t)my_fid;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) atomicAdd(out + k, g[k]);
+        }
+      }
     }
   }
 }
@@ -177,9 +224,15 @@ __global__ void __launch_bounds__(256) k_backward(BwdArgs<InT> A) {
 template <typename InT>
 static cudaError_t launch_backward_t(const BwdArgs<InT>& A, cudaStream_t st) {
   if (A.S <= 0) return cudaSuccess;
-  int64_t blocks = (A.S + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  k_backward<InT><<<(unsigned)blocks, 256, 0, st>>>(A);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backward<InT>, kBwdThreads, 0);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  const int64_t need = (A.S + kBwdThreads / 32 * kBwdChunk - 1) / (kBwdThreads / 32 * kBwdChunk);
+  if (blocks > need) blocks = need;
+  k_backward<InT><<<(unsigned)blocks, kBwdThreads, 0, st>>>(A);
   return cudaGetLastError();
 }
 

@@ -14,6 +14,7 @@
 #include <climits>
 #include <cstdint>
 #include <algorithm>
+#include <type_traits>
 
 #include "raster_kernels.cuh"
 #include "raster_math.cuh"
@@ -162,12 +163,24 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
 // (__match_any_sync ranks). Winners' bary / dists are recomputed with the identical operation sequence at
 // emit time (MR:178-197), so the payload carries exactly the bits the candidate test produced.
 
-constexpr int kNF = 19;    // staged fp64 fields per face
-constexpr int kRing = 64;  // staged faces per warp (< 32 pending + 32 new)
+#ifndef DR_RING
+#define DR_RING 64
+#endif
+#ifndef DR_FINE_MINBLOCKS
+#define DR_FINE_MINBLOCKS 0
+#endif
+#ifndef DR_LEAN_STAGE
+#define DR_LEAN_STAGE 0
+#endif
+constexpr int kRing = DR_RING;  // staged faces per warp: < 32 pending + newly staged (>= 17 when 48)
+// Staged fp64 fields per face. Lean: only a, b, c, z, area are stored and the edge vectors / squared edge
+// lengths are recomputed per pair (same expressions on the same operands => same bits), trading ~15 fp64
+// ops per pair for 2x less shared memory per warp (more resident warps).
+constexpr int kNF = DR_LEAN_STAGE ? 10 : 19;
 
 enum : int {
-  F_AX, F_AY, F_BX, F_BY, F_CX, F_CY, F_Z0, F_Z1, F_Z2,
-  F_ABX, F_ABY, F_BCX, F_BCY, F_CAX, F_CAY, F_LAB, F_LBC, F_LCA, F_AREA
+  F_AX, F_AY, F_BX, F_BY, F_CX, F_CY, F_Z0, F_Z1, F_Z2, F_AREA,
+  F_ABX, F_ABY, F_BCX, F_BCY, F_CAX, F_CAY, F_LAB, F_LBC, F_LCA
 };
 
 // one warp's shared memory: staged-face ring (SoA) + top-K lists of its 32 pixels
@@ -188,13 +201,22 @@ struct WarpSmem {
     g.z0 = get(F_Z0, k);
     g.z1 = get(F_Z1, k);
     g.z2 = get(F_Z2, k);
-    g.ab = V2{get(F_ABX, k), get(F_ABY, k)};
-    g.bc = V2{get(F_BCX, k), get(F_BCY, k)};
-    g.ca = V2{get(F_CAX, k), get(F_CAY, k)};
-    g.len_ab = get(F_LAB, k);
-    g.len_bc = get(F_LBC, k);
-    g.len_ca = get(F_LCA, k);
     g.area = get(F_AREA, k);
+    if constexpr (DR_LEAN_STAGE) {
+      g.ab = g.b - g.a;
+      g.bc = g.c - g.b;
+      g.ca = g.a - g.c;
+      g.len_ab = norm2(g.ab);
+      g.len_bc = norm2(g.bc);
+      g.len_ca = norm2(g.ca);
+    } else {
+      g.ab = V2{get(F_ABX, k), get(F_ABY, k)};
+      g.bc = V2{get(F_BCX, k), get(F_BCY, k)};
+      g.ca = V2{get(F_CAX, k), get(F_CAY, k)};
+      g.len_ab = get(F_LAB, k);
+      g.len_bc = get(F_LBC, k);
+      g.len_ca = get(F_LCA, k);
+    }
     return g;
   }
   __device__ __forceinline__ void stage(int k, const double* fv, int32_t f, uint32_t r) const {
@@ -205,9 +227,12 @@ struct WarpSmem {
     const FaceGeom g = make_face_geom(v);
     put(F_AX, k, g.a.x); put(F_AY, k, g.a.y); put(F_BX, k, g.b.x); put(F_BY, k, g.b.y);
     put(F_CX, k, g.c.x); put(F_CY, k, g.c.y); put(F_Z0, k, g.z0); put(F_Z1, k, g.z1); put(F_Z2, k, g.z2);
-    put(F_ABX, k, g.ab.x); put(F_ABY, k, g.ab.y); put(F_BCX, k, g.bc.x); put(F_BCY, k, g.bc.y);
-    put(F_CAX, k, g.ca.x); put(F_CAY, k, g.ca.y);
-    put(F_LAB, k, g.len_ab); put(F_LBC, k, g.len_bc); put(F_LCA, k, g.len_ca); put(F_AREA, k, g.area);
+    put(F_AREA, k, g.area);
+    if constexpr (!DR_LEAN_STAGE) {
+      put(F_ABX, k, g.ab.x); put(F_ABY, k, g.ab.y); put(F_BCX, k, g.bc.x); put(F_BCY, k, g.bc.y);
+      put(F_CAX, k, g.ca.x); put(F_CAY, k, g.ca.y);
+      put(F_LAB, k, g.len_ab); put(F_LBC, k, g.len_bc); put(F_LCA, k, g.len_ca);
+    }
     fid[k] = f;
     rect[k] = r;
   }
@@ -258,12 +283,62 @@ __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot,
   }
 }
 
+// Insert (zc, f) into pixel p's sorted list (column p of [K][32]). KMAX > 0: K <= KMAX is known at
+// compile time up to KMAX, so the K entries are read with independent loads (no load->compare->branch chain)
+// and the insertion position is a count of smaller keys; KMAX == 0: generic shifting loop.
+template <int KMAX>
+__device__ __forceinline__ void topk_insert(const WarpSmem& ws, int K, int p, double zc, int32_t f) {
+  if constexpr (KMAX == 1) {
+    if (cand_less(zc, f, ws.tz[p], ws.tid[p])) {
+      ws.tz[p] = zc;
+      ws.tid[p] = f;
+    }
+  } else if constexpr (KMAX > 1) {
+    double z[KMAX];
+    int32_t id[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      if (s < K) {
+        z[s] = ws.tz[s * 32 + p];
+        id[s] = ws.tid[s * 32 + p];
+      }
+    }
+    bool lt[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) lt[s] = s < K && cand_less(zc, f, z[s], id[s]);
+    // lt[] is monotone (false...false true...true): slot s takes z[s-1] if lt[s-1], the candidate if
+    // lt[s] && !lt[s-1], else keeps its entry
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      if (s < K && lt[s]) {
+        const bool shift = s > 0 && lt[s > 0 ? s - 1 : 0];
+        ws.tz[s * 32 + p] = shift ? z[s > 0 ? s - 1 : 0] : zc;
+        ws.tid[s * 32 + p] = shift ? id[s > 0 ? s - 1 : 0] : f;
+      }
+    }
+  } else {
+    if (cand_less(zc, f, ws.tz[(K - 1) * 32 + p], ws.tid[(K - 1) * 32 + p])) {
+      int s = K - 1;
+      while (s > 0) {
+        const double zp = ws.tz[(s - 1) * 32 + p];
+        const int32_t ip = ws.tid[(s - 1) * 32 + p];
+        if (!cand_less(zc, f, zp, ip)) break;
+        ws.tz[s * 32 + p] = zp;
+        ws.tid[s * 32 + p] = ip;
+        --s;
+      }
+      ws.tz[s * 32 + p] = zc;
+      ws.tid[s * 32 + p] = f;
+    }
+  }
+}
+
 // Evaluate the pairs of ring slots [head, head+G) (mod kRing) and insert the survivors.
-template <typename OutT>
+template <int KMAX, typename OutT>
 __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const WarpSmem& ws, int head, int G, int mi0,
                                               int mj0, int lane) {
   const int K = A.K;
-  const int slot_l = (head + lane) & (kRing - 1);
+  const int slot_l = (head + lane) % kRing;
   const uint32_t rl = lane < G ? ws.rect[slot_l] : 0u;
   const int cnt = (int)(((rl >> 8) & 15u) * ((rl >> 12) & 15u));
   int incl = cnt;
@@ -297,7 +372,7 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
       const int row = (int)(r & 15u) + dr;
       const int col = (int)((r >> 4) & 15u) + (rank - dr * w);
       p = row * 8 + col;
-      const int k = (head + lo) & (kRing - 1);
+      const int k = (head + lo) % kRing;
       const FaceGeom fg = ws.geom(k);
       const V2 pix{pixel_x(A.W, mj0 + col), pixel_y(A.H, mi0 + row)};
       pass = eval_pixel_face<false>(pix, fg, A.blur, A.znear, A.persp, A.clip, res);
@@ -308,30 +383,17 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
       const int rank = __popc(peers & ((1u << lane) - 1u));
       const int maxr = __reduce_max_sync(0xffffffffu, pass ? rank : 0);
       for (int rr = 0; rr <= maxr; ++rr) {
-        if (pass && rank == rr) {
-          const double zc = res.z;
-          if (cand_less(zc, f, ws.tz[(K - 1) * 32 + p], ws.tid[(K - 1) * 32 + p])) {
-            int s = K - 1;
-            while (s > 0) {
-              const double zp = ws.tz[(s - 1) * 32 + p];
-              const int32_t ip = ws.tid[(s - 1) * 32 + p];
-              if (!cand_less(zc, f, zp, ip)) break;
-              ws.tz[s * 32 + p] = zp;
-              ws.tid[s * 32 + p] = ip;
-              --s;
-            }
-            ws.tz[s * 32 + p] = zc;
-            ws.tid[s * 32 + p] = f;
-          }
-        }
+        if (pass && rank == rr) topk_insert<KMAX>(ws, K, p, res.z, f);
         __syncwarp();
       }
     }
   }
 }
 
-template <typename OutT, int NW>
-__global__ void __launch_bounds__(NW * 32) k_fine(FineArgs<OutT> A) {
+// 128 registers per thread (16 resident warps per SM) is the measured sweet spot: capping lower spills, and
+// fewer resident warps cannot hide the fp64 dependency latency (profiles/r01/README.md).
+template <typename OutT, int NW, int KMAX>
+__global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS : 16 / NW) k_fine(FineArgs<OutT> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
@@ -391,17 +453,25 @@ __global__ void __launch_bounds__(NW * 32) k_fine(FineArgs<OutT> A) {
         fid = list ? list[ci] : (int32_t)(f0 + ci);
         r = cover_rect(A.ibbox[fid], mi0, mj0, vh, vw);
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, r != 0u);
-      if (r) ws.stage((head + pending + __popc(bal & ((1u << lane) - 1u))) & (kRing - 1), A.fv, fid, r);
-      pending += __popc(bal);
-      __syncwarp();
+      unsigned todo = __ballot_sync(0xffffffffu, r != 0u);
       const bool last = c0 + 32 >= nsrc;
-      while (pending >= 32 || (last && pending > 0)) {
-        const int G = min(pending, 32);
-        process_group(A, ws, head, G, mi0, mj0, lane);
-        head = (head + G) & (kRing - 1);
-        pending -= G;
-      }
+      do {
+        // stage as many of the remaining faces as the ring has room for (room >= 17 since pending < 32)
+        const int room = kRing - pending;
+        const int rank = __popc(todo & ((1u << lane) - 1u));
+        const bool mine = ((todo >> lane) & 1u) && rank < room;
+        const unsigned take = __ballot_sync(0xffffffffu, mine);
+        if (mine) ws.stage((head + pending + rank) % kRing, A.fv, fid, r);
+        pending += __popc(take);
+        todo &= ~take;
+        __syncwarp();
+        while (pending >= 32 || (last && todo == 0u && pending > 0)) {
+          const int G = min(pending, 32);
+          process_group<KMAX>(A, ws, head, G, mi0, mj0, lane);
+          head = (head + G) % kRing;
+          pending -= G;
+        }
+      } while (todo);
     }
     __syncwarp();
     // emit this lane's pixel (MR:178-197)
@@ -452,12 +522,15 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
     kern<<<(unsigned)(sms * per_sm), nw * 32, smem, st>>>(A);  // persistent: warps pull micro-tiles
     return cudaGetLastError();
   };
-  switch (nw) {
-    case 8: return go(k_fine<OutT, 8>);
-    case 4: return go(k_fine<OutT, 4>);
-    case 2: return go(k_fine<OutT, 2>);
-    default: return go(k_fine<OutT, 1>);
-  }
+  auto by_k = [&](auto nw_c) -> cudaError_t {
+    constexpr int NW = decltype(nw_c)::value;
+    // K == 1: compare-and-replace; otherwise the shifting loop (the unrolled small-K insertion spills at the
+    // 128-register budget that keeps 16 warps per SM resident and measured slower, profiles/r01/README.md)
+    if (A.K == 1) return go(k_fine<OutT, NW, 1>);
+    return go(k_fine<OutT, NW, 0>);
+  };
+  if (nw == 8) return by_k(std::integral_constant<int, 8>{});
+  return by_k(std::integral_constant<int, 2>{});
 }
 
 size_t fine_warp_smem_bytes(int K) { return warp_smem_bytes(K); }

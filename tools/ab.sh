@@ -1,0 +1,6 @@
+#!/bin/bash
+# ab.sh V1 V2 ... : bench each build/variants/V/libdr_raster_b200.so on C4 (kernel ms per step)
+for v in "$@"; do
+  DR_RASTER_LIB=build/variants/$v/libdr_raster_b200.so timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline ${AB_ARGS} > gpurun_out/ab_$v.json 2> gpurun_out/ab_$v.err
+  python -c "import json,sys; d=json.load(open('gpurun_out/ab_$v.json')); print('$v', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['roofline']['per_kernel_ms_per_step'].items()})" || tail -3 gpurun_out/ab_$v.err
+done
