@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
 #define DR_FINE_MINBLOCKS 0
 #endif
 #ifndef DR_LEAN_STAGE
-#define DR_LEAN_STAGE 0
+#define DR_LEAN_STAGE 1
 #endif
 constexpr int kRing = DR_RING;  // staged faces per warp: < 32 pending + newly staged (>= 17 when 48)
 // Staged fp64 fields per face. Lean: only a, b, c, z, area are stored and the edge vectors / squared edge
@@ -188,8 +188,11 @@ struct WarpSmem {
   double* d;        // [kNF][kRing]
   int32_t* fid;     // [kRing]
   uint32_t* rect;   // [kRing] covered rectangle in the micro-tile: r0 | c0<<4 | h<<8 | w<<12 | recip(w)<<16
-  double* tz;       // [K][32]
+  double* tz;       // [K][32]      sorted top-K lists, column p = pixel p of the micro-tile
   int32_t* tid;     // [K][32]
+  double* bz;       // [kBuf][32]   unsorted per-pixel candidate buffers (merged by the owner lane)
+  int32_t* bid;     // [kBuf][32]
+  int32_t* bcnt;    // [32]
 
   __device__ __forceinline__ double get(int f, int k) const { return d[f * kRing + k]; }
   __device__ __forceinline__ void put(int f, int k, double v) const { d[f * kRing + k] = v; }
@@ -238,9 +241,12 @@ struct WarpSmem {
   }
 };
 
+constexpr int kBuf = 8;  // buffered candidates per pixel before the owner lane merges them into its list
+
 __host__ __device__ constexpr size_t warp_smem_bytes(int K) {
   return (size_t)kNF * kRing * sizeof(double) + (size_t)kRing * (sizeof(int32_t) + sizeof(uint32_t)) +
-         (size_t)K * 32 * (sizeof(double) + sizeof(int32_t));
+         (size_t)K * 32 * (sizeof(double) + sizeof(int32_t)) + (size_t)kBuf * 32 * (sizeof(double) + sizeof(int32_t)) +
+         32 * sizeof(int32_t);
 }
 
 // Rectangle of the micro-tile (rows i0..i0+3, cols j0..j0+7, limited to vh x vw existing pixels) covered by
@@ -283,53 +289,67 @@ __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot,
   }
 }
 
-// Insert (zc, f) into pixel p's sorted list (column p of [K][32]). KMAX > 0: K <= KMAX is known at
-// compile time up to KMAX, so the K entries are read with independent loads (no load->compare->branch chain)
-// and the insertion position is a count of smaller keys; KMAX == 0: generic shifting loop.
+// Insert (zc, f) into pixel p's sorted list (column p of [K][32]) in shared memory: shifting loop.
+__device__ __forceinline__ void list_insert(const WarpSmem& ws, int K, int p, double zc, int32_t f) {
+  if (cand_less(zc, f, ws.tz[(K - 1) * 32 + p], ws.tid[(K - 1) * 32 + p])) {
+    int s = K - 1;
+    while (s > 0) {
+      const double zp = ws.tz[(s - 1) * 32 + p];
+      const int32_t ip = ws.tid[(s - 1) * 32 + p];
+      if (!cand_less(zc, f, zp, ip)) break;
+      ws.tz[s * 32 + p] = zp;
+      ws.tid[s * 32 + p] = ip;
+      --s;
+    }
+    ws.tz[s * 32 + p] = zc;
+    ws.tid[s * 32 + p] = f;
+  }
+}
+
+// Every lane merges the buffered candidates of ITS pixel (p = lane) into its sorted list: all 32 lanes work
+// at once, and for K <= KMAX the list lives in registers during the merge (fully unrolled insertion: no
+// shared-memory load -> compare -> branch chain). The merge runs outside the fp64 evaluation, so these
+// registers do not add to the evaluation's pressure.
 template <int KMAX>
-__device__ __forceinline__ void topk_insert(const WarpSmem& ws, int K, int p, double zc, int32_t f) {
-  if constexpr (KMAX == 1) {
-    if (cand_less(zc, f, ws.tz[p], ws.tid[p])) {
-      ws.tz[p] = zc;
-      ws.tid[p] = f;
-    }
-  } else if constexpr (KMAX > 1) {
-    double z[KMAX];
-    int32_t id[KMAX];
+__device__ __forceinline__ void merge_buffers(const WarpSmem& ws, int K, int lane) {
+  const int n = ws.bcnt[lane];
+  if (n > 0) {
+    if constexpr (KMAX == 0) {
+      for (int c = 0; c < n; ++c) list_insert(ws, K, lane, ws.bz[c * 32 + lane], ws.bid[c * 32 + lane]);
+    } else {
+      double z[KMAX];
+      int32_t id[KMAX];
 #pragma unroll
-    for (int s = 0; s < KMAX; ++s) {
-      if (s < K) {
-        z[s] = ws.tz[s * 32 + p];
-        id[s] = ws.tid[s * 32 + p];
+      for (int s = 0; s < KMAX; ++s) {
+        z[s] = s < K ? ws.tz[s * 32 + lane] : pos_inf();
+        id[s] = s < K ? ws.tid[s * 32 + lane] : INT_MAX;
+      }
+      for (int c = 0; c < n; ++c) {
+        const double zc = ws.bz[c * 32 + lane];
+        const int32_t ic = ws.bid[c * 32 + lane];
+#pragma unroll
+        for (int s = KMAX - 1; s >= 0; --s) {
+          const int sp = s > 0 ? s - 1 : 0;
+          const bool lt_prev = s > 0 && cand_less(zc, ic, z[sp], id[sp]);
+          const bool lt_cur = cand_less(zc, ic, z[s], id[s]);
+          if (lt_prev) {
+            z[s] = z[sp];
+            id[s] = id[sp];
+          } else if (lt_cur) {
+            z[s] = zc;
+            id[s] = ic;
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (s < K) {
+          ws.tz[s * 32 + lane] = z[s];
+          ws.tid[s * 32 + lane] = id[s];
+        }
       }
     }
-    bool lt[KMAX];
-#pragma unroll
-    for (int s = 0; s < KMAX; ++s) lt[s] = s < K && cand_less(zc, f, z[s], id[s]);
-    // lt[] is monotone (false...false true...true): slot s takes z[s-1] if lt[s-1], the candidate if
-    // lt[s] && !lt[s-1], else keeps its entry
-#pragma unroll
-    for (int s = 0; s < KMAX; ++s) {
-      if (s < K && lt[s]) {
-        const bool shift = s > 0 && lt[s > 0 ? s - 1 : 0];
-        ws.tz[s * 32 + p] = shift ? z[s > 0 ? s - 1 : 0] : zc;
-        ws.tid[s * 32 + p] = shift ? id[s > 0 ? s - 1 : 0] : f;
-      }
-    }
-  } else {
-    if (cand_less(zc, f, ws.tz[(K - 1) * 32 + p], ws.tid[(K - 1) * 32 + p])) {
-      int s = K - 1;
-      while (s > 0) {
-        const double zp = ws.tz[(s - 1) * 32 + p];
-        const int32_t ip = ws.tid[(s - 1) * 32 + p];
-        if (!cand_less(zc, f, zp, ip)) break;
-        ws.tz[s * 32 + p] = zp;
-        ws.tid[s * 32 + p] = ip;
-        --s;
-      }
-      ws.tz[s * 32 + p] = zc;
-      ws.tid[s * 32 + p] = f;
-    }
+    ws.bcnt[lane] = 0;
   }
 }
 
@@ -379,11 +399,29 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
       f = ws.fid[k];
     }
     if (__any_sync(0xffffffffu, pass)) {
+      // append to the pixel's buffer; merge every buffer first if one would overflow
       const unsigned peers = __match_any_sync(0xffffffffu, pass ? p : 32 + lane);
       const int rank = __popc(peers & ((1u << lane) - 1u));
-      const int maxr = __reduce_max_sync(0xffffffffu, pass ? rank : 0);
-      for (int rr = 0; rr <= maxr; ++rr) {
-        if (pass && rank == rr) topk_insert<KMAX>(ws, K, p, res.z, f);
+      const int n_same = __popc(peers);
+      int base = pass ? ws.bcnt[p] : 0;
+      if (__any_sync(0xffffffffu, pass && base + n_same > kBuf)) {
+        __syncwarp();
+        merge_buffers<KMAX>(ws, K, lane);
+        __syncwarp();
+        base = 0;
+      }
+      if (pass) {
+        if (rank < kBuf) {
+          ws.bz[(base + rank) * 32 + p] = res.z;
+          ws.bid[(base + rank) * 32 + p] = f;
+        }
+        if (rank == 0) ws.bcnt[p] = base + min(n_same, kBuf);
+      }
+      __syncwarp();
+      // more than kBuf candidates for one pixel in one step (rare): insert the excess directly, one at a time
+      const int extra = __reduce_max_sync(0xffffffffu, pass ? n_same - kBuf : 0);
+      for (int rr = 0; rr < extra; ++rr) {
+        if (pass && rank == kBuf + rr) list_insert(ws, K, p, res.z, f);
         __syncwarp();
       }
     }
@@ -405,6 +443,11 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     ws.fid = reinterpret_cast<int32_t*>(ws.tz + K * 32);
     ws.tid = ws.fid + kRing;
     ws.rect = reinterpret_cast<uint32_t*>(ws.tid + K * 32);
+    ws.bz = reinterpret_cast<double*>(base + (size_t)kNF * kRing * sizeof(double) + (size_t)K * 32 * sizeof(double) +
+                                      (size_t)kRing * (sizeof(int32_t) + sizeof(uint32_t)) +
+                                      (size_t)K * 32 * sizeof(int32_t));
+    ws.bid = reinterpret_cast<int32_t*>(ws.bz + kBuf * 32);
+    ws.bcnt = ws.bid + kBuf * 32;
   }
   const int nbins = A.nbx * A.nby;
   const int mtx = (A.bs + 7) >> 3, mty = (A.bs + 3) >> 2;  // micro-tiles per bin row / column
@@ -442,6 +485,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       ws.tz[s * 32 + lane] = pos_inf();
       ws.tid[s * 32 + lane] = INT_MAX;
     }
+    ws.bcnt[lane] = 0;
     __syncwarp();
 
     int head = 0, pending = 0;
@@ -473,6 +517,8 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
         }
       } while (todo);
     }
+    __syncwarp();
+    merge_buffers<KMAX>(ws, K, lane);
     __syncwarp();
     // emit this lane's pixel (MR:178-197)
     const int row = lane >> 3, col = lane & 7;
@@ -524,9 +570,10 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
   };
   auto by_k = [&](auto nw_c) -> cudaError_t {
     constexpr int NW = decltype(nw_c)::value;
-    // K == 1: compare-and-replace; otherwise the shifting loop (the unrolled small-K insertion spills at the
-    // 128-register budget that keeps 16 warps per SM resident and measured slower, profiles/r01/README.md)
+    // register-resident merge for small K, shared-memory shifting loop otherwise
     if (A.K == 1) return go(k_fine<OutT, NW, 1>);
+    if (A.K <= 4) return go(k_fine<OutT, NW, 4>);
+    if (A.K <= 8) return go(k_fine<OutT, NW, 8>);
     return go(k_fine<OutT, NW, 0>);
   };
   if (nw == 8) return by_k(std::integral_constant<int, 8>{});
