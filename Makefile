@@ -6,12 +6,13 @@ ARCH = -gencode arch=compute_100a,code=sm_100a
 # -fmad=false: no FMA contraction anywhere in the kernels (bit-exact pix_to_face, SURVEY.md §7 hard part 1)
 NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v
 PKG = paper_2007_08501_b200
-SRCS = $(PKG)/csrc/raster_fwd.cu $(PKG)/csrc/raster_bwd.cu $(PKG)/csrc/capi.cu
-HDRS = $(PKG)/csrc/raster_math.cuh $(PKG)/csrc/raster_kernels.cuh include/dr_raster.h
+SRCS = $(PKG)/csrc/raster_fwd.cu $(PKG)/csrc/raster_bwd.cu $(PKG)/csrc/raster_camera.cu $(PKG)/csrc/capi.cu \
+       $(PKG)/csrc/adaptor.cu
+HDRS = $(PKG)/csrc/raster_math.cuh $(PKG)/csrc/raster_kernels.cuh include/dr_raster.h include/dr_b200/mesh_raster.hpp
 LIB = $(PKG)/libdr_raster_b200.so
 OBJS = $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 
-all: $(LIB) oracle
+all: $(LIB) oracle cpptest
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build
@@ -24,7 +25,16 @@ oracle:
 	$(MAKE) -C oracle liboracle.so
 	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; fi
 
+# C++ mirror parity test (tests/cpp): links the product library and the reference library (oracle/_ref)
+CPPTEST = build/test_raster_cpp
+cpptest: $(LIB) oracle
+	@if [ -d /root/reference/proj/include ]; then \
+	  mkdir -p build && g++ -std=gnu++20 -O2 -ffp-contract=off -Iinclude -I/root/reference/proj/include \
+	    tests/cpp/test_raster_cpp.cpp -o $(CPPTEST) -L$(PKG) -ldr_raster_b200 -Loracle/_ref -ldr3d_ref \
+	    -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -L/usr/local/cuda/lib64 -lcudart; \
+	fi
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all oracle clean
+.PHONY: all oracle cpptest clean

@@ -110,6 +110,33 @@ int dr_rasterize_meshes_bwd_f64(const double* face_verts, const int64_t* mesh_to
                                 const double* bary_coords, const double* grad_zbuf, const double* grad_bary,
                                 const double* grad_dists, double* grad_face_verts, dr_stream_t stream);
 
+/* ---- camera side of the path: MeshBatch + Camera <-> face_verts on the GPU ---- */
+
+/* dr::Camera (camera.hpp:19-35). */
+typedef struct dr_camera {
+  int32_t perspective;        /* 1 = ProjectionKind::Perspective, 0 = Orthographic */
+  int32_t _reserved0;
+  double rotation[9];         /* world -> view, row-major */
+  double translation[3];      /* world -> view */
+  double focal_length;        /* perspective */
+  double principal_point[2];  /* perspective, NDC units */
+  double ortho_scale[2];      /* orthographic, per axis */
+  double znear, zfar;
+} dr_camera;
+
+/* world_to_ndc (camera.cpp:36-70) of every packed vertex gathered per face (prepare_faces,
+ * mesh_raster.cpp:100-122): verts [V,3] world space, faces [F,3] packed GLOBAL vertex indices
+ * (MeshBatch::faces_packed) -> face_verts [F,3,3] (x_ndc, y_ndc, z_view); a clipped vertex (perspective,
+ * z_view <= 0) gets xy = (0,0) like the reference. Bit-identical to the reference's NdcPoints.
+ * Out-of-range vertex indices -> DR_ERR_INDEX (synchronises the stream to report it). */
+int dr_world_to_face_verts(const double* verts, int64_t V, const int64_t* faces, int64_t F, const dr_camera* cam,
+                           double* face_verts, dr_stream_t stream);
+
+/* Reverse of the above (mesh_raster.cpp:380-401): grad_face_verts [F,3,3] scattered to vertices and pulled
+ * through world_to_ndc_backward (camera.cpp:72-85) -> grad_verts [V,3] world space (overwritten). */
+int dr_face_verts_backward(const double* verts, int64_t V, const int64_t* faces, int64_t F, const dr_camera* cam,
+                           const double* grad_face_verts, double* grad_verts, dr_stream_t stream);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* dr_last_error(void);
 

@@ -20,5 +20,7 @@ from .raster import (  # noqa: F401
     rasterize_meshes,
     rasterize_meshes_backward,
     rasterize_meshes_naive,
+    face_verts_backward,
     workspace_bytes,
+    world_to_face_verts,
 )

@@ -22,6 +22,8 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_meshes_fwd_f64",
     "dr_rasterize_meshes_bwd",
     "dr_rasterize_meshes_bwd_f64",
+    "dr_world_to_face_verts",
+    "dr_face_verts_backward",
     "dr_last_error",
     "dr_rasterize_meshes_bin_stats",
     "dr_launch_count",
@@ -40,6 +42,16 @@ class DrRasterSettings(C.Structure):
         ("blur_radius", C.c_double), ("znear", C.c_double),
         ("clip_nonpositive_z", C.c_uint8), ("perspective_correct", C.c_uint8),
         ("clip_barycentric_coords", C.c_uint8), ("cull_backfaces", C.c_uint8), ("_reserved1", C.c_uint8 * 4),
+    ]
+
+
+class DrCamera(C.Structure):
+    """dr_camera (include/dr_raster.h) = dr::Camera (camera.hpp:19-35)."""
+
+    _fields_ = [
+        ("perspective", C.c_int32), ("_reserved0", C.c_int32), ("rotation", C.c_double * 9),
+        ("translation", C.c_double * 3), ("focal_length", C.c_double), ("principal_point", C.c_double * 2),
+        ("ortho_scale", C.c_double * 2), ("znear", C.c_double), ("zfar", C.c_double),
     ]
 
 
@@ -66,6 +78,11 @@ def load() -> C.CDLL:
     bwd_args = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.dr_rasterize_meshes_bwd.argtypes = bwd_args
     L.dr_rasterize_meshes_bwd_f64.argtypes = bwd_args
+    cp = C.POINTER(DrCamera)
+    L.dr_world_to_face_verts.argtypes = [_vp, C.c_int64, _vp, C.c_int64, cp, _vp, _vp]
+    L.dr_face_verts_backward.argtypes = [_vp, C.c_int64, _vp, C.c_int64, cp, _vp, _vp, _vp]
+    L.dr_world_to_face_verts.restype = C.c_int
+    L.dr_face_verts_backward.restype = C.c_int
     L.dr_last_error.restype = C.c_char_p
     L.dr_rasterize_meshes_bin_stats.argtypes = [C.c_int64, C.c_int64, sp, _vp, _vp, C.POINTER(C.c_int64)]
     L.dr_launch_count.restype = C.c_uint64

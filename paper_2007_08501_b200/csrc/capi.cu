@@ -42,8 +42,8 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 // ---- optional per-kernel timing ring ----
-const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine", "k_backward", "memset"};
-enum { KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4 };
+const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine", "k_backward", "memset", "k_camera"};
+enum { KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5 };
 struct ProfEntry {
   int kernel;
   cudaEvent_t a, b;
@@ -320,6 +320,58 @@ int dr_rasterize_meshes_bwd_f64(const double* fv, const int64_t* first, const in
                                 dr_stream_t stream) {
   return bwd_impl<double>(fv, first, num, N, F, s, p2f, bary, dz, db, dd, grad,
                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+static drb::CameraArgs camera_args(const dr_camera* cam) {
+  drb::CameraArgs a;
+  for (int i = 0; i < 9; ++i) a.r[i] = cam->rotation[i];
+  for (int i = 0; i < 3; ++i) a.t[i] = cam->translation[i];
+  a.focal = cam->focal_length;
+  a.pp[0] = cam->principal_point[0];
+  a.pp[1] = cam->principal_point[1];
+  a.ortho[0] = cam->ortho_scale[0];
+  a.ortho[1] = cam->ortho_scale[1];
+  a.perspective = cam->perspective != 0;
+  return a;
+}
+
+int dr_world_to_face_verts(const double* verts, int64_t V, const int64_t* faces, int64_t F, const dr_camera* cam,
+                           double* face_verts, dr_stream_t stream) {
+  if (!cam) return fail(DR_ERR_USAGE, "camera pointer is null");
+  if (V < 0 || F < 0) return fail(DR_ERR_SHAPE, "negative vertex/face count");
+  if (F == 0) return DR_OK;
+  if (!verts || !faces || !face_verts) return fail(DR_ERR_USAGE, "null input/output pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int* flag = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+  if (e == cudaSuccess) {
+    ProfScope ps(st, KN_CAMERA);
+    e = drb::launch_world_to_face_verts(verts, V, faces, F, camera_args(cam), face_verts, flag, st);
+  }
+  int bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (flag) cudaFreeAsync(flag, st);
+  if (e != cudaSuccess) return cuda_fail(e, "world_to_face_verts");
+  if (bad) return fail(DR_ERR_INDEX, "face vertex index out of range [0, %lld)", (long long)V);
+  return DR_OK;
+}
+
+int dr_face_verts_backward(const double* verts, int64_t V, const int64_t* faces, int64_t F, const dr_camera* cam,
+                           const double* gfv, double* gverts, dr_stream_t stream) {
+  if (!cam) return fail(DR_ERR_USAGE, "camera pointer is null");
+  if (V < 0 || F < 0) return fail(DR_ERR_SHAPE, "negative vertex/face count");
+  if (V == 0) return DR_OK;
+  if (!verts || !gverts || (F > 0 && (!faces || !gfv))) return fail(DR_ERR_USAGE, "null input/output pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_CAMERA);
+    e = drb::launch_face_verts_backward(verts, V, faces, F, camera_args(cam), gfv, gverts, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "face_verts_backward");
+  return DR_OK;
 }
 
 const char* dr_last_error(void) { return g_err.c_str(); }

@@ -45,6 +45,20 @@ struct BwdArgs {
   bool persp, clip;
 };
 
+// Camera (dr_camera / dr::Camera, camera.hpp:19-35) as kernel arguments.
+struct CameraArgs {
+  double r[9];      // world -> view rotation, row-major
+  double t[3];      // world -> view translation
+  double focal;     // perspective focal length
+  double pp[2];     // principal point (NDC)
+  double ortho[2];  // orthographic scale
+  int perspective;
+};
+
+cudaError_t launch_world_to_face_verts(const double* verts, int64_t V, const int64_t* faces, int64_t F,
+                                       const CameraArgs& c, double* fv, int* bad_index, cudaStream_t st);
+cudaError_t launch_face_verts_backward(const double* verts, int64_t V, const int64_t* faces, int64_t F,
+                                       const CameraArgs& c, const double* gfv, double* gverts, cudaStream_t st);
 void launch_face_setup(const double* fv, int64_t F, int H, int W, double inflate, double znear, int clip_z, int cull,
                        int4* ibbox, cudaStream_t st);
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,

@@ -232,6 +232,55 @@ class RasterizeMeshes(torch.autograd.Function):
         return g.to(fv.dtype), None, None, None
 
 
+def _camera_c(cam) -> _lib.DrCamera:
+    """scenes.Camera (or any object with the dr::Camera fields) -> dr_camera."""
+    c = _lib.DrCamera()
+    c.perspective = int(bool(cam.perspective))
+    rot = [float(x) for row in cam.rotation for x in row]
+    for i in range(9):
+        c.rotation[i] = rot[i]
+    for i in range(3):
+        c.translation[i] = float(cam.translation[i])
+    c.focal_length = float(cam.focal_length)
+    c.principal_point[0], c.principal_point[1] = (float(x) for x in cam.principal_point)
+    c.ortho_scale[0], c.ortho_scale[1] = (float(x) for x in cam.ortho_scale)
+    c.znear, c.zfar = float(cam.znear), float(cam.zfar)
+    return c
+
+
+def world_to_face_verts(verts: torch.Tensor, faces: torch.Tensor, camera) -> torch.Tensor:
+    """world_to_ndc (camera.cpp:36-70) + per-face gather on the GPU: verts [V,3] f64 world space, faces [F,3] packed
+    global vertex ids -> face_verts [F,3,3] (x_ndc, y_ndc, z_view), bit-identical to the reference."""
+    L = _lib.load()
+    if not verts.is_cuda:
+        raise UsageError("verts must be a CUDA tensor (there is no CPU path)")
+    v = verts.detach().to(torch.float64).contiguous()
+    f = faces.to(device=v.device, dtype=torch.int64).contiguous()
+    out = torch.empty((f.shape[0], 3, 3), dtype=torch.float64, device=v.device)
+    cam = _camera_c(camera)
+    with torch.cuda.device(v.device):
+        rc = L.dr_world_to_face_verts(_ptr(v), v.shape[0], _ptr(f), f.shape[0], C.byref(cam), _ptr(out),
+                                      _stream(v.device))
+    _check(rc, "world_to_face_verts")
+    return out
+
+
+def face_verts_backward(verts: torch.Tensor, faces: torch.Tensor, camera, grad_face_verts: torch.Tensor):
+    """grad_face_verts [F,3,3] -> world-space grad_verts [V,3] (vertex scatter + world_to_ndc_backward,
+    mesh_raster.cpp:380-401, camera.cpp:72-85)."""
+    L = _lib.load()
+    v = verts.detach().to(torch.float64).contiguous()
+    f = faces.to(device=v.device, dtype=torch.int64).contiguous()
+    g = grad_face_verts.to(device=v.device, dtype=torch.float64).contiguous()
+    out = torch.empty((v.shape[0], 3), dtype=torch.float64, device=v.device)
+    cam = _camera_c(camera)
+    with torch.cuda.device(v.device):
+        rc = L.dr_face_verts_backward(_ptr(v), v.shape[0], _ptr(f), f.shape[0], C.byref(cam), _ptr(g), _ptr(out),
+                                      _stream(v.device))
+    _check(rc, "face_verts_backward")
+    return out
+
+
 def launch_count() -> int:
     return int(_lib.load().dr_launch_count())
 

@@ -330,3 +330,49 @@ def test_full_config_properties_and_mesh_sample(cfg, oracle, cuda):
             g_g = gpu_bwd(fv, f_, n_, rs, cuda, got[0], got[2], dz, db, dd)
             sl = slice(int(f_[0]), int(f_[0] + n_[0]))
             assert rel_err(g_g[sl], g_w[sl]) < GRAD_RTOL
+
+
+# -------------------------------------------------------------------------------------------------
+# camera side (world_to_ndc + gather, scatter + world_to_ndc_backward) on the GPU
+
+
+def test_world_to_face_verts_bit_exact(cuda):
+    from paper_2007_08501_b200 import MeshIndexError, world_to_face_verts
+
+    m = S.config_meshes("C2")
+    for cam in (S.bench_camera(), S.Camera.look_from_distance(3.0, False),
+                S.Camera(rotation=S.axis_angle((0.3, -1.0, 0.2), 0.7), translation=(0.1, -0.2, 1.2),
+                         focal_length=1.7, principal_point=(0.05, -0.02))):
+        got = world_to_face_verts(torch.as_tensor(m.verts_packed(), device=cuda),
+                                  torch.as_tensor(m.faces_packed(), device=cuda), cam).cpu().numpy()
+        assert np.array_equal(got, S.face_verts(m, cam))
+    with pytest.raises(MeshIndexError):
+        bad = m.faces_packed().copy()
+        bad[5, 1] = len(m.verts_packed())
+        world_to_face_verts(torch.as_tensor(m.verts_packed(), device=cuda), torch.as_tensor(bad, device=cuda),
+                            S.bench_camera())
+
+
+def test_face_verts_backward_matches_host_chain(cuda):
+    from paper_2007_08501_b200 import face_verts_backward
+
+    m = S.config_meshes("C2")
+    g = np.random.default_rng(7).standard_normal((len(m.faces_packed()), 3, 3))
+    for cam in (S.bench_camera(), S.Camera.look_from_distance(3.0, False)):
+        got = face_verts_backward(torch.as_tensor(m.verts_packed(), device=cuda),
+                                  torch.as_tensor(m.faces_packed(), device=cuda), cam,
+                                  torch.as_tensor(g, device=cuda)).cpu().numpy()
+        want = S.scatter_face_grads(m, cam, g)
+        assert rel_err(got, want) < 1e-12
+
+
+def test_div_free_paths_and_rerun_backward_tolerance(cuda, oracle):
+    """Backward on C1-like scene with fp64 inputs: GPU vs oracle to accumulation order only."""
+    m, cam = S.ico_sphere(3), S.bench_camera()
+    fv, first, num = boundary(m, cam)
+    o = orc_settings(64, 4, 5e-3, cam)
+    fr = oracle.forward(fv, first, num, o)
+    dz, db, dd = fast_cotangents(fr[0].size, 11)
+    want = oracle.backward(fv, first, num, o, fr[0], fr[2], dz, db, dd)
+    got = gpu_bwd(fv, first, num, raster_settings(64, 4, 5e-3, cam), cuda, fr[0], fr[2], dz, db, dd, torch.float64)
+    assert rel_err(got, want) < 1e-12
