@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-faces", type=float, default=0.06,
+    ap.add_argument("--cpu-sample-faces", type=float, default=0.25,
                     help="fraction of the batch's faces the CPU sample covers")
     return ap.parse_args()
 
@@ -131,6 +131,21 @@ def measured_peaks():
             return json.load(f), "measured"
     except OSError:
         return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic(cfg, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed ncu --set full capture of this
+    bench command (profiles/*/ncu_*_summary.json, newest round first); None if there is none."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_*_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            return float(d[cfg][kernel]["traffic_bytes"])
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 # -------------------------------------------------------------------------------------------------
@@ -311,10 +326,11 @@ def main():
     else:
         alg_bytes = 72 * F + 16 * F
     peaks, peak_kind = measured_peaks()
+    traffic = ncu_traffic(cfg, dom)
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
     step_ms_sum = sum(v[0] for v in shares.values()) / args.steps
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom,
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "kernel": dom,
                 "kernel_ms": dom_ms, "kernel_share_of_step": shares[dom][0] / args.steps / max(step_ms_sum, 1e-9),
                 "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
                 "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in shares.items()}}
