@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
 #ifndef DR_FINE_MINBLOCKS
 #define DR_FINE_MINBLOCKS 0
 #endif
+#ifndef DR_EMIT_PREFETCH
+#define DR_EMIT_PREFETCH 1
+#endif
 #ifndef DR_LEAN_STAGE
 #define DR_LEAN_STAGE 1
 #endif
@@ -264,12 +267,8 @@ __device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0
 
 template <typename OutT>
 __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot, bool occupied, double z,
-                                          int32_t fid, double px, double py) {
+                                          int32_t fid, const double* v, double px, double py) {
   if (occupied) {
-    double v[9];
-    const double* p = A.fv + 9 * (int64_t)fid;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) v[k] = __ldg(p + k);
     const FaceGeom g = make_face_geom(v);
     PixelFaceResult r;
     eval_pixel_face<true>(V2{px, py}, g, A.blur, A.znear, A.persp, A.clip, r);  // same ops => same bits
@@ -520,16 +519,43 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     __syncwarp();
     merge_buffers<KMAX>(ws, K, lane);
     __syncwarp();
-    // emit this lane's pixel (MR:178-197)
+    // emit this lane's pixel (MR:178-197); the next occupied slot's face_verts are fetched before the current
+    // slot is evaluated so the global-load latency overlaps the fp64 work
     const int row = lane >> 3, col = lane & 7;
     if (row < vh && col < vw) {
       const int pi = mi0 + row, pj = mj0 + col;
       const double px = pixel_x(A.W, pj), py = pixel_y(A.H, pi);
       const int64_t slot0 = (((int64_t)b * A.H + pi) * A.W + pj) * K;
+#if DR_EMIT_PREFETCH
+      double vnext[9];
+      int32_t fnext = ws.tid[lane];
+      if (fnext != INT_MAX) {
+#pragma unroll
+        for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
+      }
+      for (int s = 0; s < K; ++s) {
+        const int32_t f = fnext;
+        double v[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) v[t] = vnext[t];
+        fnext = s + 1 < K ? ws.tid[(s + 1) * 32 + lane] : INT_MAX;
+        if (fnext != INT_MAX) {
+#pragma unroll
+          for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
+        }
+        emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, v, px, py);
+      }
+#else
       for (int s = 0; s < K; ++s) {
         const int32_t f = ws.tid[s * 32 + lane];
-        emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, px, py);
+        double v[9];
+        if (f != INT_MAX) {
+#pragma unroll
+          for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)f + t);
+        }
+        emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, v, px, py);
       }
+#endif
     }
     __syncwarp();
   }

@@ -4,10 +4,11 @@ set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
 out=build/variants/$name; mkdir -p $out
-for f in raster_fwd raster_bwd capi; do
+SRCS=$(cd paper_2007_08501_b200/csrc && ls *.cu | sed 's/\.cu$//')
+for f in $SRCS; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v "$@" \
     -c paper_2007_08501_b200/csrc/$f.cu -o $out/$f.o 2> $out/$f.ptxas.txt &
 done
 wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libdr_raster_b200.so $out/raster_fwd.o $out/raster_bwd.o $out/capi.o -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libdr_raster_b200.so $(for f in $SRCS; do echo $out/$f.o; done) -lcudart
 grep -B1 -A3 "Compiling entry function '_ZN3drb6k_fineIfLi8ELi8\|Compiling entry function '_ZN3drb6k_fineIfLi8ELi0" $out/raster_fwd.ptxas.txt | grep -E "registers|spill" | tr '\n' ' '; echo " [$name]"
