@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-groups", type=int, default=8, help="mesh groups the host pipeline streams")
     ap.add_argument("--cpu-sample-faces", type=float, default=0.25,
                     help="fraction of the batch's faces the CPU sample covers")
     return ap.parse_args()
@@ -335,44 +336,30 @@ def main():
                 "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
                 "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in shares.items()}}
 
-    # end to end through the public API with host buffers (pinned), copies inside the timed region
+    # end to end through the public API with host buffers (pinned), copies inside the timed region: the
+    # HostPipeline streams groups of meshes so H2D / kernels / D2H overlap (paper_2007_08501_b200/pipeline.py)
     e2e = None
     if not args.no_e2e:
+        from paper_2007_08501_b200.pipeline import HostPipeline
+
+        del ws  # the pipeline owns its own device buffers
+        torch.cuda.empty_cache()
+        pipe = HostPipeline(first_np, num_np, rs, F, dev, n_groups=args.e2e_groups, backward=c["backward"])
         h_fv = torch.from_numpy(fv_np).pin_memory()
-        h_dz = dz.cpu().pin_memory()
-        h_db = db.cpu().pin_memory()
-        h_dd = dd.cpu().pin_memory()
-        d_fv = torch.empty_like(fv)
-        d_dz, d_db, d_dd = torch.empty_like(dz), torch.empty_like(db), torch.empty_like(dd)
-        o_p2f = torch.empty((N, H, W, K), dtype=torch.int64).pin_memory()
-        o_z = torch.empty((N, H, W, K), dtype=torch.float32).pin_memory()
-        o_b = torch.empty((N, H, W, K, 3), dtype=torch.float32).pin_memory()
-        o_d = torch.empty((N, H, W, K), dtype=torch.float32).pin_memory()
-        o_g = torch.empty((F, 3, 3), dtype=torch.float64).pin_memory()
-        h2d = h_fv.numel() * 8 + (h_dz.numel() + h_db.numel() + h_dd.numel()) * 4 * bool(c["backward"])
+        cot_h = tuple(t.cpu().pin_memory() for t in (dz, db, dd)) if c["backward"] else None
+        out_h = (torch.empty((N, H, W, K), dtype=torch.int64).pin_memory(),
+                 torch.empty((N, H, W, K), dtype=torch.float32).pin_memory(),
+                 torch.empty((N, H, W, K, 3), dtype=torch.float32).pin_memory(),
+                 torch.empty((N, H, W, K), dtype=torch.float32).pin_memory())
+        grad_h = torch.empty((F, 3, 3), dtype=torch.float64).pin_memory() if c["backward"] else None
+        h2d = h_fv.numel() * 8 + (sum(t.numel() for t in cot_h) * 4 if c["backward"] else 0)
         d2h = S_ * 28 + (F * 72 if c["backward"] else 0)
-
-        def e2e_step():
-            d_fv.copy_(h_fv, non_blocking=True)
-            if c["backward"]:
-                d_dz.copy_(h_dz, non_blocking=True)
-                d_db.copy_(h_db, non_blocking=True)
-                d_dd.copy_(h_dd, non_blocking=True)
-            p2f, zbuf, bary, dists = rasterize_meshes(d_fv, first, num, rs, workspace=ws)
-            o_p2f.copy_(p2f, non_blocking=True)
-            o_z.copy_(zbuf, non_blocking=True)
-            o_b.copy_(bary, non_blocking=True)
-            o_d.copy_(dists, non_blocking=True)
-            if c["backward"]:
-                g = rasterize_meshes_backward(d_fv, first, num, rs, p2f, bary, d_dz, d_db, d_dd)
-                o_g.copy_(g, non_blocking=True)
-
         e2e_steps = max(1, min(args.steps, 5))
-        e2e_step()
+        pipe.run(h_fv, out_h, cot_h, grad_h)
         barrier()
         e0.record(st)
         for _ in range(e2e_steps):
-            e2e_step()
+            pipe.run(h_fv, out_h, cot_h, grad_h)
         e1.record(st)
         barrier()
         ems = e0.elapsed_time(e1) / e2e_steps
@@ -381,7 +368,9 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": total_fpx / (ems * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": ems,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "pcie_gbs": (h2d + d2h) / (ems * 1e-3) / 1e9, "groups": len(pipe.groups),
+               "api": "paper_2007_08501_b200.pipeline.HostPipeline.run (pinned host in/out)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -94,8 +94,11 @@ int dr_rasterize_meshes_fwd_f64(const double* face_verts, const int64_t* mesh_to
                                 size_t workspace_bytes, dr_stream_t stream);
 
 /* Backward (rasterize_backward, mesh_raster.cpp:345-378): cotangents on zbuf [N,H,W,K], bary [N,H,W,K,3],
- * dists [N,H,W,K] pulled back to grad_face_verts [F,3,3] = d(x_ndc, y_ndc, z_view) per face vertex
- * (overwritten). bary_coords is the forward's output (the reference reads frag.bary, mesh_raster.cpp:359).
+ * dists [N,H,W,K] pulled back to grad_face_verts [F,3,3] = d(x_ndc, y_ndc, z_view) per face vertex.
+ * The rows of the batch's face ranges are overwritten; rows of faces outside every mesh range are left
+ * untouched (so disjoint groups of meshes of one packed buffer can be processed by separate calls).
+ * pix_to_face / bary_coords are the forward's outputs for the same batch (the reference reads frag.bary,
+ * mesh_raster.cpp:359).
  * Accumulation uses fp64 atomics: the summation order is not fixed, results agree to ~1e-15 relative. */
 int dr_rasterize_meshes_bwd(const double* face_verts, const int64_t* mesh_to_face_first_idx,
                             const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
@@ -109,6 +112,20 @@ int dr_rasterize_meshes_bwd_f64(const double* face_verts, const int64_t* mesh_to
                                 const dr_raster_settings* s, const int64_t* pix_to_face,
                                 const double* bary_coords, const double* grad_zbuf, const double* grad_bary,
                                 const double* grad_dists, double* grad_face_verts, dr_stream_t stream);
+
+/* Asynchronous variants: identical contracts, plus HOST copies of mesh_to_face_first_idx / num_faces_per_mesh
+ * (validation and grid sizing then need no device read-back, so the call does not synchronise `stream` and
+ * can be enqueued ahead in a copy/compute pipeline). The device arrays must hold the same values. */
+int dr_rasterize_meshes_fwd_hr(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                               const int64_t* num_faces_per_mesh, int64_t N, int64_t F, const dr_raster_settings* s,
+                               int64_t* pix_to_face, float* zbuf, float* bary_coords, float* pix_dists,
+                               void* workspace, size_t workspace_bytes, dr_stream_t stream,
+                               const int64_t* host_first, const int64_t* host_num);
+int dr_rasterize_meshes_bwd_hr(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                               const int64_t* num_faces_per_mesh, int64_t N, int64_t F, const dr_raster_settings* s,
+                               const int64_t* pix_to_face, const float* bary_coords, const float* grad_zbuf,
+                               const float* grad_bary, const float* grad_dists, double* grad_face_verts,
+                               dr_stream_t stream, const int64_t* host_first, const int64_t* host_num);
 
 /* ---- camera side of the path: MeshBatch + Camera <-> face_verts on the GPU ---- */
 

@@ -22,6 +22,8 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_meshes_fwd_f64",
     "dr_rasterize_meshes_bwd",
     "dr_rasterize_meshes_bwd_f64",
+    "dr_rasterize_meshes_fwd_hr",
+    "dr_rasterize_meshes_bwd_hr",
     "dr_world_to_face_verts",
     "dr_face_verts_backward",
     "dr_last_error",
@@ -83,6 +85,10 @@ def load() -> C.CDLL:
     L.dr_face_verts_backward.argtypes = [_vp, C.c_int64, _vp, C.c_int64, cp, _vp, _vp, _vp]
     L.dr_world_to_face_verts.restype = C.c_int
     L.dr_face_verts_backward.restype = C.c_int
+    L.dr_rasterize_meshes_fwd_hr.argtypes = fwd_args + [_vp, _vp]
+    L.dr_rasterize_meshes_bwd_hr.argtypes = bwd_args + [_vp, _vp]
+    L.dr_rasterize_meshes_fwd_hr.restype = C.c_int
+    L.dr_rasterize_meshes_bwd_hr.restype = C.c_int
     L.dr_last_error.restype = C.c_char_p
     L.dr_rasterize_meshes_bin_stats.argtypes = [C.c_int64, C.c_int64, sp, _vp, _vp, C.POINTER(C.c_int64)]
     L.dr_launch_count.restype = C.c_uint64
@@ -91,7 +97,9 @@ def load() -> C.CDLL:
     L.dr_profile_kernel_name.argtypes = [C.c_int]
     L.dr_profile_kernel_name.restype = C.c_char_p
     for fn in ("dr_rasterize_meshes_fwd", "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
-               "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_bin_stats"):
+               "dr_rasterize_meshes_bwd_f64",
+    "dr_rasterize_meshes_fwd_hr",
+    "dr_rasterize_meshes_bwd_hr", "dr_rasterize_meshes_bin_stats"):
         getattr(L, fn).restype = C.c_int
     _lib = L
     return L

@@ -126,13 +126,21 @@ int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
 }
 
 // host copy of the mesh ranges: validation + grid sizing (N is small; one D2H per call)
+// `host_first/host_num`: optional host copies of the same arrays (the *_hr entry points); without them the
+// device arrays are read back, which synchronises `st`.
 int read_ranges(const int64_t* first, const int64_t* num, int64_t N, int64_t F, cudaStream_t st,
-                int64_t* max_faces) {
+                int64_t* max_faces, std::vector<int64_t>* out = nullptr, const int64_t* host_first = nullptr,
+                const int64_t* host_num = nullptr) {
   std::vector<int64_t> h(2 * (size_t)N);
-  cudaError_t e = cudaMemcpyAsync(h.data(), first, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data() + N, num, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return cuda_fail(e, "reading mesh_to_face_first_idx / num_faces_per_mesh");
+  if (host_first && host_num) {
+    std::memcpy(h.data(), host_first, sizeof(int64_t) * N);
+    std::memcpy(h.data() + N, host_num, sizeof(int64_t) * N);
+  } else {
+    cudaError_t e = cudaMemcpyAsync(h.data(), first, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data() + N, num, sizeof(int64_t) * N, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "reading mesh_to_face_first_idx / num_faces_per_mesh");
+  }
   int64_t mx = 0;
   for (int64_t b = 0; b < N; ++b) {
     int64_t f0 = h[b], n = h[N + b];
@@ -143,13 +151,33 @@ int read_ranges(const int64_t* first, const int64_t* num, int64_t N, int64_t F, 
     mx = std::max(mx, n);
   }
   *max_faces = mx;
+  if (out) *out = std::move(h);
   return DR_OK;
+}
+
+// Zero grad_face_verts on the union of the batch's face ranges only (merged intervals), so a caller may run the
+// backward on disjoint groups of meshes of one packed buffer (e.g. a copy/compute pipeline) concurrently.
+cudaError_t zero_face_ranges(double* grad, const std::vector<int64_t>& h, int64_t N, cudaStream_t st) {
+  std::vector<std::pair<int64_t, int64_t>> iv;
+  for (int64_t b = 0; b < N; ++b)
+    if (h[N + b] > 0) iv.push_back({h[b], h[b] + h[N + b]});
+  std::sort(iv.begin(), iv.end());
+  size_t i = 0;
+  while (i < iv.size()) {
+    int64_t lo = iv[i].first, hi = iv[i].second;
+    size_t j = i + 1;
+    while (j < iv.size() && iv[j].first <= hi) hi = std::max(hi, iv[j++].second);
+    cudaError_t e = cudaMemsetAsync(grad + 9 * lo, 0, sizeof(double) * 9 * (size_t)(hi - lo), st);
+    if (e != cudaSuccess) return e;
+    i = j;
+  }
+  return cudaSuccess;
 }
 
 template <typename OutT>
 int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
              const dr_raster_settings* s, int64_t* p2f, OutT* zbuf, OutT* bary, OutT* dists, void* ws, size_t ws_bytes,
-             cudaStream_t st) {
+             cudaStream_t st, const int64_t* host_first = nullptr, const int64_t* host_num = nullptr) {
   Plan p;
   int rc = make_plan(N, F, s, p);
   if (rc) return rc;
@@ -158,8 +186,16 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   if (!ws || ws_bytes < p.total)
     return fail(DR_ERR_OOM, "workspace too small: %zu bytes given, %zu needed", ws_bytes, p.total);
   int64_t max_faces = 0;
-  rc = read_ranges(first, num, N, F, st, &max_faces);
+  std::vector<int64_t> ranges;
+  rc = read_ranges(first, num, N, F, st, &max_faces, &ranges, host_first, host_num);
   if (rc) return rc;
+  // K0 only needs the faces the batch's meshes own: [lowest first, highest end)
+  int64_t f_lo = F, f_hi = 0;
+  for (int64_t b = 0; b < N; ++b)
+    if (ranges[N + b] > 0) {
+      f_lo = std::min(f_lo, ranges[b]);
+      f_hi = std::max(f_hi, ranges[b] + ranges[N + b]);
+    }
 
   char* base = static_cast<char*>(ws);
   int4* ibbox = reinterpret_cast<int4*>(base + p.off_ibbox);
@@ -169,7 +205,9 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
 
   {
     ProfScope ps(st, KN_SETUP);
-    drb::launch_face_setup(fv, F, p.H, p.W, inflate, s->znear, s->clip_nonpositive_z, s->cull_backfaces, ibbox, st);
+    if (f_hi > f_lo)
+      drb::launch_face_setup(fv, f_lo, f_hi, p.H, p.W, inflate, s->znear, s->clip_nonpositive_z, s->cull_backfaces,
+                             ibbox, st);
   }
   if (p.binned) {
     {
@@ -231,22 +269,22 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
 template <typename InT>
 int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
              const dr_raster_settings* s, const int64_t* p2f, const InT* bary, const InT* dz, const InT* db,
-             const InT* dd, double* grad, cudaStream_t st) {
+             const InT* dd, double* grad, cudaStream_t st, const int64_t* host_first = nullptr,
+             const int64_t* host_num = nullptr) {
   Plan p;
   int rc = make_plan(N, F, s, p);
   if (rc) return rc;
-  if (!p2f || !bary || !dz || !db || !dd || (F > 0 && (!fv || !grad)))
+  if (!first || !num || !p2f || !bary || !dz || !db || !dd || (F > 0 && (!fv || !grad)))
     return fail(DR_ERR_USAGE, "null input/output pointer");
-  if (first && num) {
-    int64_t mx;
-    rc = read_ranges(first, num, N, F, st, &mx);
-    if (rc) return rc;
-  }
+  int64_t mx;
+  std::vector<int64_t> ranges;
+  rc = read_ranges(first, num, N, F, st, &mx, &ranges, host_first, host_num);
+  if (rc) return rc;
   if (F == 0) return DR_OK;
   cudaError_t e;
   {
     ProfScope ps(st, KN_MEMSET);
-    e = cudaMemsetAsync(grad, 0, sizeof(double) * 9 * (size_t)F, st);
+    e = zero_face_ranges(grad, ranges, N, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "zeroing grad_face_verts");
   drb::BwdArgs<InT> A;
@@ -299,6 +337,24 @@ int dr_rasterize_meshes_fwd(const double* fv, const int64_t* first, const int64_
                             void* ws, size_t ws_bytes, dr_stream_t stream) {
   return fwd_impl<float>(fv, first, num, N, F, s, p2f, zbuf, bary, dists, ws, ws_bytes,
                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dr_rasterize_meshes_fwd_hr(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                               const dr_raster_settings* s, int64_t* p2f, float* zbuf, float* bary, float* dists,
+                               void* ws, size_t ws_bytes, dr_stream_t stream, const int64_t* host_first,
+                               const int64_t* host_num) {
+  if (!host_first || !host_num) return fail(DR_ERR_USAGE, "host ranges are null");
+  return fwd_impl<float>(fv, first, num, N, F, s, p2f, zbuf, bary, dists, ws, ws_bytes,
+                         reinterpret_cast<cudaStream_t>(stream), host_first, host_num);
+}
+
+int dr_rasterize_meshes_bwd_hr(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                               const dr_raster_settings* s, const int64_t* p2f, const float* bary, const float* dz,
+                               const float* db, const float* dd, double* grad, dr_stream_t stream,
+                               const int64_t* host_first, const int64_t* host_num) {
+  if (!host_first || !host_num) return fail(DR_ERR_USAGE, "host ranges are null");
+  return bwd_impl<float>(fv, first, num, N, F, s, p2f, bary, dz, db, dd, grad, reinterpret_cast<cudaStream_t>(stream),
+                         host_first, host_num);
 }
 
 int dr_rasterize_meshes_fwd_f64(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,

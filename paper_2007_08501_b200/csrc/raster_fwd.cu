@@ -60,11 +60,11 @@ __device__ __forceinline__ int last_row_ge(double L, int H) {
 // ------------------------------------------------------------------------------------------------
 // K0: face setup
 
-__global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ fv, int64_t F, int H, int W,
-                                                    double inflate, double znear, int clip_nonpositive_z,
+__global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ fv, int64_t f_lo, int64_t f_hi, int H,
+                                                    int W, double inflate, double znear, int clip_nonpositive_z,
                                                     int cull_backfaces, int4* __restrict__ ibbox) {
-  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= F) return;
+  int64_t f = f_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= f_hi) return;
   const double* p = fv + 9 * f;
   double v[9];
 #pragma unroll
@@ -564,11 +564,11 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 // ------------------------------------------------------------------------------------------------
 // host-side launchers (called from capi.cu)
 
-void launch_face_setup(const double* fv, int64_t F, int H, int W, double inflate, double znear, int clip_z,
-                       int cull, int4* ibbox, cudaStream_t st) {
-  if (F <= 0) return;
-  unsigned grid = (unsigned)((F + 255) / 256);
-  k_face_setup<<<grid, 256, 0, st>>>(fv, F, H, W, inflate, znear, clip_z, cull, ibbox);
+void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int W, double inflate, double znear,
+                       int clip_z, int cull, int4* ibbox, cudaStream_t st) {
+  if (f_hi <= f_lo) return;
+  unsigned grid = (unsigned)((f_hi - f_lo + 255) / 256);
+  k_face_setup<<<grid, 256, 0, st>>>(fv, f_lo, f_hi, H, W, inflate, znear, clip_z, cull, ibbox);
 }
 
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,

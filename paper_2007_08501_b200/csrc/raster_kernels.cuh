@@ -59,8 +59,8 @@ cudaError_t launch_world_to_face_verts(const double* verts, int64_t V, const int
                                        const CameraArgs& c, double* fv, int* bad_index, cudaStream_t st);
 cudaError_t launch_face_verts_backward(const double* verts, int64_t V, const int64_t* faces, int64_t F,
                                        const CameraArgs& c, const double* gfv, double* gverts, cudaStream_t st);
-void launch_face_setup(const double* fv, int64_t F, int H, int W, double inflate, double znear, int clip_z, int cull,
-                       int4* ibbox, cudaStream_t st);
+void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int W, double inflate, double znear,
+                       int clip_z, int cull, int4* ibbox, cudaStream_t st);
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
                       int bs, int nbx, int nby, int cap, int* counts, int32_t* lists, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);

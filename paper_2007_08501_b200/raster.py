@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, replace
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -132,10 +133,12 @@ def workspace_bytes(num_meshes: int, num_faces: int, settings: RasterSettings) -
 
 
 def rasterize_meshes(face_verts: torch.Tensor, mesh_to_face_first_idx, num_faces_per_mesh,
-                     settings: RasterSettings | None = None, out_dtype=torch.float32, workspace=None,
-                     **kwargs):
+                     settings: RasterSettings | None = None, out_dtype=torch.float32, workspace=None, out=None,
+                     host_ranges=None, **kwargs):
     """Forward. Returns (pix_to_face int64 [N,H,W,K], zbuf [N,H,W,K], bary_coords [N,H,W,K,3],
-    pix_dists [N,H,W,K]) with zbuf/bary/dists in ``out_dtype`` (float32 or float64)."""
+    pix_dists [N,H,W,K]) with zbuf/bary/dists in ``out_dtype`` (float32 or float64). ``out`` = optional
+    preallocated (pix_to_face, zbuf, bary_coords, pix_dists), contiguous, written in place. ``host_ranges`` =
+    optional (first, num) int64 numpy copies of the mesh ranges: the call then does not synchronise (fp32 only)."""
     settings = settings or RasterSettings(**kwargs)
     L = _lib.load()
     fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
@@ -149,16 +152,31 @@ def rasterize_meshes(face_verts: torch.Tensor, mesh_to_face_first_idx, num_faces
         _check(_lib.DR_ERR_RANGE if N >= 1 else _lib.DR_ERR_SHAPE, "rasterize_meshes")
     if workspace is None or workspace.numel() < ws_n:
         workspace = torch.empty(ws_n, dtype=torch.uint8, device=dev)
-    p2f = torch.empty((N, H, W, K), dtype=torch.int64, device=dev)
-    zbuf = torch.empty((N, H, W, K), dtype=out_dtype, device=dev)
-    bary = torch.empty((N, H, W, K, 3), dtype=out_dtype, device=dev)
-    dists = torch.empty((N, H, W, K), dtype=out_dtype, device=dev)
+    if out is not None:
+        p2f, zbuf, bary, dists = out
+        want = [((N, H, W, K), torch.int64), ((N, H, W, K), out_dtype), ((N, H, W, K, 3), out_dtype),
+                ((N, H, W, K), out_dtype)]
+        for t, (shp, dt) in zip(out, want):
+            if tuple(t.shape) != shp or t.dtype != dt or not t.is_contiguous() or t.device != dev:
+                raise ShapeError(f"out tensor {tuple(t.shape)} {t.dtype} does not match {shp} {dt}")
+    else:
+        p2f = torch.empty((N, H, W, K), dtype=torch.int64, device=dev)
+        zbuf = torch.empty((N, H, W, K), dtype=out_dtype, device=dev)
+        bary = torch.empty((N, H, W, K, 3), dtype=out_dtype, device=dev)
+        dists = torch.empty((N, H, W, K), dtype=out_dtype, device=dev)
     fn = L.dr_rasterize_meshes_fwd if out_dtype == torch.float32 else L.dr_rasterize_meshes_fwd_f64
     if out_dtype not in (torch.float32, torch.float64):
         raise UsageError("out_dtype must be float32 or float64")
     with torch.cuda.device(dev):
-        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), _ptr(p2f), _ptr(zbuf), _ptr(bary), _ptr(dists),
-                _ptr(workspace), workspace.numel(), _stream(dev))
+        if host_ranges is not None and out_dtype == torch.float32:
+            hf, hn = (np.ascontiguousarray(x, dtype=np.int64) for x in host_ranges)
+            rc = L.dr_rasterize_meshes_fwd_hr(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), _ptr(p2f),
+                                              _ptr(zbuf), _ptr(bary), _ptr(dists), _ptr(workspace), workspace.numel(),
+                                              _stream(dev), hf.ctypes.data_as(C.c_void_p),
+                                              hn.ctypes.data_as(C.c_void_p))
+        else:
+            rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), _ptr(p2f), _ptr(zbuf), _ptr(bary),
+                    _ptr(dists), _ptr(workspace), workspace.numel(), _stream(dev))
     _check(rc, "rasterize_meshes")
     return p2f, zbuf, bary, dists
 
@@ -171,9 +189,11 @@ def rasterize_meshes_naive(face_verts, mesh_to_face_first_idx, num_faces_per_mes
 
 
 def rasterize_meshes_backward(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
-                              pix_to_face, bary_coords, grad_zbuf, grad_bary, grad_dists):
+                              pix_to_face, bary_coords, grad_zbuf, grad_bary, grad_dists, out=None,
+                              host_ranges=None):
     """Backward (rasterize_backward's per-slot part, mesh_raster.cpp:345-378): returns grad_face_verts [F,3,3]
-    f64 = d(x_ndc, y_ndc, z_view) per face vertex. Cotangent/bary dtype float32 or float64 (all the same)."""
+    f64 = d(x_ndc, y_ndc, z_view) per face vertex. Cotangent/bary dtype float32 or float64 (all the same).
+    With ``out`` (a contiguous [F,3,3] f64 tensor) only the rows of the batch's face ranges are written."""
     L = _lib.load()
     fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
     N, F = int(first.numel()), int(fv.shape[0])
@@ -190,12 +210,23 @@ def rasterize_meshes_backward(face_verts, mesh_to_face_first_idx, num_faces_per_
             raise ShapeError(f"rasterize_backward: cotangent shapes do not match fragments: {tuple(t.shape)} vs {w}")
     p2f = pix_to_face.to(torch.int64).contiguous()
     others = [t.to(dt).contiguous() for t in tens[1:]]
-    grad = torch.empty((F, 3, 3), dtype=torch.float64, device=fv.device)
+    if out is not None:
+        if tuple(out.shape) != (F, 3, 3) or out.dtype != torch.float64 or not out.is_contiguous():
+            raise ShapeError(f"out must be a contiguous [F,3,3] float64 tensor, got {tuple(out.shape)}")
+        grad = out
+    else:
+        grad = torch.zeros((F, 3, 3), dtype=torch.float64, device=fv.device)
     s = settings.to_c()
     fn = L.dr_rasterize_meshes_bwd if dt == torch.float32 else L.dr_rasterize_meshes_bwd_f64
     with torch.cuda.device(fv.device):
-        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), _ptr(p2f), *[_ptr(t) for t in others],
-                _ptr(grad), _stream(fv.device))
+        if host_ranges is not None and dt == torch.float32:
+            hf, hn = (np.ascontiguousarray(x, dtype=np.int64) for x in host_ranges)
+            rc = L.dr_rasterize_meshes_bwd_hr(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), _ptr(p2f),
+                                              *[_ptr(t) for t in others], _ptr(grad), _stream(fv.device),
+                                              hf.ctypes.data_as(C.c_void_p), hn.ctypes.data_as(C.c_void_p))
+        else:
+            rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), _ptr(p2f), *[_ptr(t) for t in others],
+                    _ptr(grad), _stream(fv.device))
     _check(rc, "rasterize_backward")
     return grad
 

@@ -376,3 +376,33 @@ def test_div_free_paths_and_rerun_backward_tolerance(cuda, oracle):
     want = oracle.backward(fv, first, num, o, fr[0], fr[2], dz, db, dd)
     got = gpu_bwd(fv, first, num, raster_settings(64, 4, 5e-3, cam), cuda, fr[0], fr[2], dz, db, dd, torch.float64)
     assert rel_err(got, want) < 1e-12
+
+
+def test_host_pipeline_matches_device_calls(cuda):
+    """HostPipeline (pinned host in/out, mesh groups streamed over 3 CUDA streams) == plain device calls."""
+    from paper_2007_08501_b200 import rasterize_meshes, rasterize_meshes_backward
+    from paper_2007_08501_b200.pipeline import HostPipeline
+
+    m, cam = S.config_meshes("C2"), S.bench_camera()
+    fv, first, num = boundary(m, cam)
+    rs = raster_settings(128, 8, 1e-4, cam)
+    N, F = len(num), len(fv)
+    g = np.random.default_rng(3)
+    cot = [torch.as_tensor(g.standard_normal(s), dtype=torch.float32) for s in
+           ((N, 128, 128, 8), (N, 128, 128, 8, 3), (N, 128, 128, 8))]
+    pipe = HostPipeline(first, num, rs, F, cuda, n_groups=3)
+    out_h = (torch.empty((N, 128, 128, 8), dtype=torch.int64).pin_memory(),
+             torch.empty((N, 128, 128, 8), dtype=torch.float32).pin_memory(),
+             torch.empty((N, 128, 128, 8, 3), dtype=torch.float32).pin_memory(),
+             torch.empty((N, 128, 128, 8), dtype=torch.float32).pin_memory())
+    grad_h = torch.empty((F, 3, 3), dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        pipe.run(torch.as_tensor(fv).pin_memory(), out_h, tuple(c.pin_memory() for c in cot), grad_h)
+        torch.cuda.synchronize()
+    fvd = torch.as_tensor(fv, device=cuda)
+    ref = rasterize_meshes(fvd, torch.as_tensor(first, device=cuda), torch.as_tensor(num, device=cuda), rs)
+    for a, b in zip(out_h, ref):
+        assert torch.equal(a, b.cpu())
+    gref = rasterize_meshes_backward(fvd, torch.as_tensor(first, device=cuda), torch.as_tensor(num, device=cuda), rs,
+                                     ref[0], ref[2], *(c.to(cuda) for c in cot))
+    assert rel_err(grad_h.numpy(), gref.cpu().numpy()) < 1e-12
