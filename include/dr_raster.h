@@ -154,6 +154,19 @@ int dr_world_to_face_verts(const double* verts, int64_t V, const int64_t* faces,
 int dr_face_verts_backward(const double* verts, int64_t V, const int64_t* faces, int64_t F, const dr_camera* cam,
                            const double* grad_face_verts, double* grad_verts, dr_stream_t stream);
 
+/* ---- packed <-> padded batch bookkeeping (batching.hpp:20-27, 48-75) on the GPU ---- */
+
+/* padded[b, j, :] = packed[first[b] + j, :] for j < num[b], else pad_row (NULL = zeros). Rows are opaque
+ * row_bytes-byte records; padded is [N, max_count, row_bytes]. first/num are device arrays. */
+int dr_packed_to_padded(const void* packed, const int64_t* first, const int64_t* num, int64_t N, int64_t max_count,
+                        int64_t row_bytes, const void* pad_row, void* padded, dr_stream_t stream);
+/* packed[first[b] + j, :] = padded[b, j, :] for j < num[b]. */
+int dr_padded_to_packed(const void* padded, const int64_t* first, const int64_t* num, int64_t N, int64_t max_count,
+                        int64_t row_bytes, void* packed, dr_stream_t stream);
+/* out[i] = the batch element owning packed row i (PackedView::item_to_element), -1 for rows in no range. */
+int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
+                              dr_stream_t stream);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* dr_last_error(void);
 

@@ -26,6 +26,9 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_meshes_bwd_hr",
     "dr_world_to_face_verts",
     "dr_face_verts_backward",
+    "dr_packed_to_padded",
+    "dr_padded_to_packed",
+    "dr_packed_item_to_element",
     "dr_last_error",
     "dr_rasterize_meshes_bin_stats",
     "dr_launch_count",
@@ -89,6 +92,11 @@ def load() -> C.CDLL:
     L.dr_rasterize_meshes_bwd_hr.argtypes = bwd_args + [_vp, _vp]
     L.dr_rasterize_meshes_fwd_hr.restype = C.c_int
     L.dr_rasterize_meshes_bwd_hr.restype = C.c_int
+    L.dr_packed_to_padded.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp]
+    L.dr_padded_to_packed.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, C.c_int64, _vp, _vp]
+    L.dr_packed_item_to_element.argtypes = [_vp, _vp, C.c_int64, C.c_int64, _vp, _vp]
+    for fn in ("dr_packed_to_padded", "dr_padded_to_packed", "dr_packed_item_to_element"):
+        getattr(L, fn).restype = C.c_int
     L.dr_last_error.restype = C.c_char_p
     L.dr_rasterize_meshes_bin_stats.argtypes = [C.c_int64, C.c_int64, sp, _vp, _vp, C.POINTER(C.c_int64)]
     L.dr_launch_count.restype = C.c_uint64

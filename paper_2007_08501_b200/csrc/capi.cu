@@ -42,8 +42,8 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 // ---- optional per-kernel timing ring ----
-const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine", "k_backward", "memset", "k_camera"};
-enum { KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5 };
+const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine", "k_backward", "memset", "k_camera", "k_batching"};
+enum { KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5, KN_BATCH = 6 };
 struct ProfEntry {
   int kernel;
   cudaEvent_t a, b;
@@ -428,6 +428,53 @@ int dr_face_verts_backward(const double* verts, int64_t V, const int64_t* faces,
   }
   if (e != cudaSuccess) return cuda_fail(e, "face_verts_backward");
   return DR_OK;
+}
+
+int dr_packed_to_padded(const void* packed, const int64_t* first, const int64_t* num, int64_t N, int64_t max_count,
+                        int64_t row_bytes, const void* pad_row, void* padded, dr_stream_t stream) {
+  if (N < 0 || max_count < 0 || row_bytes <= 0) return fail(DR_ERR_SHAPE, "packed_to_padded: bad sizes");
+  if (row_bytes > drb::kMaxPadRow && pad_row)
+    return fail(DR_ERR_RANGE, "packed_to_padded: pad row larger than %d bytes", drb::kMaxPadRow);
+  if (N * max_count > 0 && (!first || !num || !packed || !padded))
+    return fail(DR_ERR_USAGE, "packed_to_padded: null pointer");
+  drb::PadRow pad;
+  std::memset(pad.bytes, 0, sizeof(pad.bytes));
+  if (pad_row) std::memcpy(pad.bytes, pad_row, (size_t)row_bytes);
+  else if (row_bytes > drb::kMaxPadRow) return fail(DR_ERR_RANGE, "packed_to_padded: rows above 256 bytes unsupported");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_BATCH);
+    e = drb::launch_packed_to_padded(packed, first, num, N, max_count, row_bytes, pad, padded, st);
+  }
+  return e == cudaSuccess ? DR_OK : cuda_fail(e, "packed_to_padded");
+}
+
+int dr_padded_to_packed(const void* padded, const int64_t* first, const int64_t* num, int64_t N, int64_t max_count,
+                        int64_t row_bytes, void* packed, dr_stream_t stream) {
+  if (N < 0 || max_count < 0 || row_bytes <= 0) return fail(DR_ERR_SHAPE, "padded_to_packed: bad sizes");
+  if (N * max_count > 0 && (!first || !num || !packed || !padded))
+    return fail(DR_ERR_USAGE, "padded_to_packed: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_BATCH);
+    e = drb::launch_padded_to_packed(padded, first, num, N, max_count, row_bytes, packed, st);
+  }
+  return e == cudaSuccess ? DR_OK : cuda_fail(e, "padded_to_packed");
+}
+
+int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
+                              dr_stream_t stream) {
+  if (N < 0 || total < 0) return fail(DR_ERR_SHAPE, "item_to_element: bad sizes");
+  if ((N > 0 && (!first || !num)) || (total > 0 && !out)) return fail(DR_ERR_USAGE, "item_to_element: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_BATCH);
+    e = drb::launch_item_to_element(first, num, N, total, out, st);
+  }
+  return e == cudaSuccess ? DR_OK : cuda_fail(e, "item_to_element");
 }
 
 const char* dr_last_error(void) { return g_err.c_str(); }

@@ -59,6 +59,19 @@ cudaError_t launch_world_to_face_verts(const double* verts, int64_t V, const int
                                        const CameraArgs& c, double* fv, int* bad_index, cudaStream_t st);
 cudaError_t launch_face_verts_backward(const double* verts, int64_t V, const int64_t* faces, int64_t F,
                                        const CameraArgs& c, const double* gfv, double* gverts, cudaStream_t st);
+// pad row of packed_to_padded (passed by value in the kernel parameters)
+constexpr int kMaxPadRow = 256;
+struct PadRow {
+  unsigned char bytes[kMaxPadRow];
+};
+cudaError_t launch_packed_to_padded(const void* packed, const int64_t* first, const int64_t* num, int64_t N,
+                                    int64_t max_count, int64_t row_bytes, const PadRow& pad, void* padded,
+                                    cudaStream_t st);
+cudaError_t launch_padded_to_packed(const void* padded, const int64_t* first, const int64_t* num, int64_t N,
+                                    int64_t max_count, int64_t row_bytes, void* packed, cudaStream_t st);
+cudaError_t launch_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
+                                   cudaStream_t st);
+
 void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int W, double inflate, double znear,
                        int clip_z, int cull, int4* ibbox, cudaStream_t st);
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,

@@ -1,0 +1,33 @@
+"""GPU: packed <-> padded bookkeeping (batching.hpp:20-27, 48-75) against numpy restatements."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2007_08501_b200 import scenes as S
+
+pytestmark = pytest.mark.gpu
+
+
+def np_packed_to_padded(packed, first, num, M, pad):
+    out = np.full((len(num), M) + packed.shape[1:], pad, dtype=packed.dtype)
+    for b, (f, n) in enumerate(zip(first, num)):
+        out[b, :n] = packed[f:f + n]
+    return out
+
+
+def test_packed_padded_round_trip(cuda):
+    from paper_2007_08501_b200.batching import item_to_element, packed_to_padded, padded_to_packed
+
+    m = S.config_meshes("C2")
+    fv = S.face_verts(m, S.bench_camera())
+    first, num = m.mesh_to_face_first_idx(), m.num_faces_per_mesh()
+    for arr, pad in ((fv, -7.5), (m.faces_packed(), -1), (m.faces_packed()[:, 0].astype(np.int32), 3),
+                     (np.arange(len(fv) * 3, dtype=np.uint8).reshape(-1, 3), 9)):
+        t = torch.as_tensor(np.ascontiguousarray(arr), device=cuda)
+        got = packed_to_padded(t, first, num, pad_value=pad).cpu().numpy()
+        want = np_packed_to_padded(arr, first, num, int(num.max()), pad)
+        assert np.array_equal(got, want)
+        back = padded_to_packed(torch.as_tensor(got, device=cuda), first, num, total=len(arr)).cpu().numpy()
+        assert np.array_equal(back, arr)
+    ite = item_to_element(first, num, len(fv) + 5, cuda).cpu().numpy()
+    assert np.array_equal(ite[:len(fv)], np.repeat(np.arange(len(num)), num)) and np.all(ite[len(fv):] == -1)
