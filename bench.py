@@ -314,7 +314,7 @@ def main():
 
     # roofline of the dominant kernel (per-launch averages from the library's event timing)
     shares = {}
-    for name in ("k_face_setup", "k_bin_faces", "k_fine", "k_backward"):
+    for name in ("k_face_setup", "k_bin_faces", "k_sort_bins", "k_fine", "k_backward"):
         tot, n = kt.total(name)
         if n:
             shares[name] = (tot, n)

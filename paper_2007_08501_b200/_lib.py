@@ -105,9 +105,8 @@ def load() -> C.CDLL:
     L.dr_profile_kernel_name.argtypes = [C.c_int]
     L.dr_profile_kernel_name.restype = C.c_char_p
     for fn in ("dr_rasterize_meshes_fwd", "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
-               "dr_rasterize_meshes_bwd_f64",
-    "dr_rasterize_meshes_fwd_hr",
-    "dr_rasterize_meshes_bwd_hr", "dr_rasterize_meshes_bin_stats"):
+               "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_fwd_hr", "dr_rasterize_meshes_bwd_hr",
+               "dr_rasterize_meshes_bin_stats"):
         getattr(L, fn).restype = C.c_int
     _lib = L
     return L

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -42,8 +43,9 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 // ---- optional per-kernel timing ring ----
-const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine", "k_backward", "memset", "k_camera", "k_batching"};
-enum { KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5, KN_BATCH = 6 };
+const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine",     "k_backward",
+                              "memset",       "k_camera",    "k_batching", "k_sort_bins"};
+enum { KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5, KN_BATCH = 6, KN_SORT = 7 };
 struct ProfEntry {
   int kernel;
   cudaEvent_t a, b;
@@ -82,8 +84,18 @@ struct Plan {
   int bs = 0;  // bin side used by the fine stage (16 when naive)
   bool binned = false;
   int nbx = 0, nby = 0, cap = 0;
-  size_t off_ibbox = 0, off_counter = 0, off_counts = 0, off_lists = 0, total = 0;
+  bool zsort = false;  // depth-ordered bins + K-th-depth culling (clip_barycentric_coords only)
+  size_t off_ibbox = 0, off_zkey = 0, off_counter = 0, off_counts = 0, off_lists = 0, off_keys = 0, total = 0;
 };
+
+// DR_ZSORT=0 disables the depth-ordered fine stage (A/B measurements; results are identical either way)
+bool zsort_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DR_ZSORT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int auto_cap(int64_t F) { return (int)std::max<int64_t>(1, std::min<int64_t>(F, 4096)); }
 
@@ -110,9 +122,12 @@ int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
   p.nbx = (p.W + p.bs - 1) / p.bs;
   p.nby = (p.H + p.bs - 1) / p.bs;
   p.cap = p.binned ? (s->max_faces_per_bin > 0 ? s->max_faces_per_bin : auto_cap(F)) : 0;
+  p.zsort = s->clip_barycentric_coords != 0 && zsort_enabled();
   size_t off = 0;
   p.off_ibbox = off;
   off = align_up(off + sizeof(int4) * (size_t)std::max<int64_t>(F, 1));
+  p.off_zkey = off;
+  off = align_up(off + sizeof(float) * (size_t)std::max<int64_t>(F, 1));
   p.off_counter = off;
   off = align_up(off + sizeof(unsigned long long));
   p.off_counts = off;
@@ -120,6 +135,10 @@ int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
     off = align_up(off + sizeof(int) * (size_t)N * p.nbx * p.nby);
     p.off_lists = off;
     off = align_up(off + sizeof(int32_t) * (size_t)N * p.nbx * p.nby * (size_t)p.cap);
+    if (p.zsort) {
+      p.off_keys = off;
+      off = align_up(off + sizeof(float) * (size_t)N * p.nbx * p.nby * (size_t)p.cap);
+    }
   }
   p.total = off;
   return DR_OK;
@@ -201,21 +220,29 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   int4* ibbox = reinterpret_cast<int4*>(base + p.off_ibbox);
   int* counts = reinterpret_cast<int*>(base + p.off_counts);
   int32_t* lists = reinterpret_cast<int32_t*>(base + p.off_lists);
+  float* zkey = reinterpret_cast<float*>(base + p.off_zkey);
+  float* bin_keys = p.zsort && p.binned ? reinterpret_cast<float*>(base + p.off_keys) : nullptr;
   const double inflate = std::sqrt(std::max(0.0, s->blur_radius));  // MR:103
 
   {
     ProfScope ps(st, KN_SETUP);
     if (f_hi > f_lo)
       drb::launch_face_setup(fv, f_lo, f_hi, p.H, p.W, inflate, s->znear, s->clip_nonpositive_z, s->cull_backfaces,
-                             ibbox, st);
+                             ibbox, zkey, st);
   }
   if (p.binned) {
     {
       ProfScope ps(st, KN_MEMSET);
       cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)N * p.nbx * p.nby, st);
     }
-    ProfScope ps(st, KN_BIN);
-    drb::launch_bin_faces(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, p.cap, counts, lists, st);
+    {
+      ProfScope ps(st, KN_BIN);
+      drb::launch_bin_faces(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, p.cap, counts, lists, st);
+    }
+    if (p.zsort) {
+      ProfScope ps(st, KN_SORT);
+      drb::launch_sort_bins(counts, lists, bin_keys, zkey, N * (int64_t)p.nbx * p.nby, p.cap, st);
+    }
   }
   drb::FineArgs<OutT> A;
   A.fv = fv;
@@ -224,6 +251,9 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   A.num = num;
   A.bin_counts = counts;
   A.bin_lists = lists;
+  A.zkey = zkey;
+  A.bin_keys = bin_keys;
+  A.zsort = p.zsort ? 1 : 0;
   A.binned = p.binned ? 1 : 0;
   A.cap = p.cap;
   A.bs = p.bs;

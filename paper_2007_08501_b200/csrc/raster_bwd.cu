@@ -25,11 +25,12 @@ __device__ __forceinline__ void clamp_bary_backward(const double wr[3], const do
     out[0] = out[1] = out[2] = 0.0;
     return;
   }
-  double h0 = qdiv(t0, s), h1 = qdiv(t1, s), h2 = qdiv(t2, s);
+  const double rs = fdiv(1.0, s);  // tolerance path: fast reciprocal (raster_math.cuh fdiv)
+  double h0 = t0 * rs, h1 = t1 * rs, h2 = t2 * rs;
   double d = dc[0] * h0 + dc[1] * h1 + dc[2] * h2;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    double d_t = qdiv(dc[i] - d, s);
+    double d_t = (dc[i] - d) * rs;
     out[i] = (wr[i] > 0.0 && wr[i] < 1.0) ? d_t : 0.0;
   }
 }
@@ -55,11 +56,11 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slo
                            (double)A.d_bary[3 * slot + 2] + dz * z[2]};
   const V2 pa = p - fg.a, pb = p - fg.b, pc = p - fg.c;
   double w_raw[3];
-  barycentric(fg, pa, pb, pc, w_raw);  // MR:366
+  barycentric<false>(fg, pa, pb, pc, w_raw);  // MR:366
   double d_w[3], dzv[3] = {0.0, 0.0, 0.0};
   if (A.persp) {  // builder-defined: u = persp_correct(w_raw, z); bary = clamp(u)
     double u[3], d_u[3], d_top[3];
-    const double den = persp_correct(w_raw, fg.z0, fg.z1, fg.z2, u);
+    const double den = persp_correct<false>(w_raw, fg.z0, fg.z1, fg.z2, u);
     if (A.clip) {
       clamp_bary_backward(u, d_hat, d_u);
     } else {
@@ -68,12 +69,13 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slo
       d_u[2] = d_hat[2];
     }
     if (den > kPerspEps) {
+      const double rden = fdiv(1.0, den);
       const double du_u = d_u[0] * u[0] + d_u[1] * u[1] + d_u[2] * u[2];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) d_top[k] = qdiv(d_u[k] - du_u, den);
+      for (int k = 0; k < 3; ++k) d_top[k] = (d_u[k] - du_u) * rden;
     } else {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) d_top[k] = qdiv(d_u[k], kPerspEps);
+      for (int k = 0; k < 3; ++k) d_top[k] = d_u[k] * (1.0 / kPerspEps);
     }
     d_w[0] = d_top[0] * z[1] * z[2];
     d_w[1] = d_top[1] * z[0] * z[2];
@@ -95,7 +97,7 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slo
   const V2 gn0_b = perp(c - p), gn0_c = perp(p - b);
   const V2 gn1_c = perp(a - p), gn1_a = perp(p - c);
   const V2 gn2_a = perp(b - p), gn2_b = perp(p - a);
-  const double inv = 1.0 / fg.area;
+  const double inv = fdiv(1.0, fg.area);
   const double wd = w_raw[0] * d_w[0] + w_raw[1] * d_w[1] + w_raw[2] * d_w[2];
   V2 dxy[3];
   dxy[0] = ((gn1_a * d_w[1] + gn2_a * d_w[2]) - grad_d_a * wd) * inv;
@@ -105,14 +107,14 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slo
   // MR:46-69 point_triangle_dist2_backward: nearest edge (first strict min), t and sign frozen
   const double d_out = (double)A.d_dists[slot];
   double t0, t1, t2;
-  const double e0 = seg_dist2(p, a, pa, fg.ab, fg.len_ab, t0);
-  const double e1 = seg_dist2(p, b, pb, fg.bc, fg.len_bc, t1);
-  const double e2 = seg_dist2(p, c, pc, fg.ca, fg.len_ca, t2);
+  const double e0 = seg_dist2<false>(p, a, pa, fg.ab, fg.len_ab, t0);
+  const double e1 = seg_dist2<false>(p, b, pb, fg.bc, fg.len_bc, t1);
+  const double e2 = seg_dist2<false>(p, c, pc, fg.ca, fg.len_ca, t2);
   int be = 0;
   double best = e0, bt = t0;
   if (e1 < best) { best = e1; bt = t1; be = 1; }
   if (e2 < best) { best = e2; bt = t2; be = 2; }
-  const bool inside = point_triangle_dist2(p, fg, pa, pb, pc).inside;
+  const bool inside = point_triangle_dist2<false>(p, fg, pa, pb, pc).inside;
   const double sign = inside ? -1.0 : 1.0;
   const V2 ea = be == 0 ? a : (be == 1 ? b : c);
   const V2 eb = be == 0 ? b : (be == 1 ? c : a);

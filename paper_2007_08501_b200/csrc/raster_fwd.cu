@@ -19,6 +19,17 @@
 #include "raster_kernels.cuh"
 #include "raster_math.cuh"
 
+#ifndef DR_STATS
+#define DR_STATS 0
+#endif
+#if DR_STATS
+// debug build only (tools/fine_stats.py): work counters of K2
+__device__ unsigned long long g_stats[8];
+#define STAT_ADD(i, v) do { const unsigned long long sv_ = (unsigned long long)(v); if ((threadIdx.x & 31) == 0) atomicAdd(&g_stats[i], sv_); } while (0)
+#else
+#define STAT_ADD(i, v) do { } while (0)
+#endif
+
 namespace drb {
 
 // ------------------------------------------------------------------------------------------------
@@ -62,7 +73,8 @@ __device__ __forceinline__ int last_row_ge(double L, int H) {
 
 __global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ fv, int64_t f_lo, int64_t f_hi, int H,
                                                     int W, double inflate, double znear, int clip_nonpositive_z,
-                                                    int cull_backfaces, int4* __restrict__ ibbox) {
+                                                    int cull_backfaces, int4* __restrict__ ibbox,
+                                                    float* __restrict__ zkey) {
   int64_t f = f_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= f_hi) return;
   const double* p = fv + 9 * f;
@@ -70,6 +82,7 @@ __global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ f
 #pragma unroll
   for (int k = 0; k < 9; ++k) v[k] = __ldg(p + k);
   int4 out = make_int4(1, 0, 1, 0);  // empty
+  float key = __int_as_float(0x7f800000);  // +inf: culled faces are never candidates
   bool keep = true;
 #pragma unroll
   for (int k = 0; k < 9; ++k) keep = keep && isfinite(v[k]);  // builder-defined: non-finite faces are culled
@@ -97,9 +110,16 @@ __global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ f
       int j0 = first_col_ge(bx0, W), j1 = last_col_le(bx1, W);
       int i0 = first_row_le(by1, H), i1 = last_row_ge(by0, H);
       if (j0 <= j1 && i0 <= i1) out = make_int4(i0, i1, j0, j1);
+      // Depth key: with clamped barycentrics (MR:172) every candidate z = RN(RN(w0 z0) + RN(w1 z1)) + RN(w2 z2)
+      // (MR:173) has w_i >= 0 and |sum w_i - 1| <= 4 ulp, so z >= zmin - 8 ulp(|zmin|) - (underflow, 3 * 2^-1074);
+      // the key subtracts a far larger margin and rounds down to fp32, so it is a strict lower bound.
+      double zmin = z0 < z1 ? z0 : z1;
+      zmin = z2 < zmin ? z2 : zmin;
+      key = __double2float_rd(zmin - fabs(zmin) * 1e-9 - 1e-300);
     }
   }
   ibbox[f] = out;
+  if (zkey) zkey[f] = key;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -145,6 +165,66 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
 }
 
 // ------------------------------------------------------------------------------------------------
+// K1b: depth-order each bin list (ascending zkey, ties by face id) so K2 meets the nearest faces first and can
+// stop streaming a list once every pixel of its micro-tile holds K candidates nearer than the next key.
+// One CTA per bin, bitonic sort of (orderable key bits << 32 | face id) in shared memory. The selection K2
+// makes is order-independent (strict total order, MR:138-140): sorting changes only how much work it skips.
+
+__device__ __forceinline__ uint32_t float_order_bits(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float float_from_order_bits(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+constexpr int kSortThreads = 256;
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restrict__ counts, int32_t* __restrict__ lists,
+                                                            float* __restrict__ keys, const float* __restrict__ zkey,
+                                                            int64_t nbins_total, int cap) {
+  __shared__ unsigned long long s[kSortMax];
+  for (int64_t bin = blockIdx.x; bin < nbins_total; bin += gridDim.x) {
+    const int c = counts[bin];
+    if (c <= 0 || c > cap || c > kSortMax) continue;  // empty, overflowed (spill path) or too long: unsorted
+    int32_t* L = lists + bin * (int64_t)cap;
+    float* Kb = keys + bin * (int64_t)cap;
+    int P = 1;
+    while (P < c) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += kSortThreads) {
+      unsigned long long e = ~0ull;
+      if (i < c) {
+        const int32_t f = L[i];
+        e = ((unsigned long long)float_order_bits(__ldg(zkey + f)) << 32) | (uint32_t)f;
+      }
+      s[i] = e;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = threadIdx.x; t < (P >> 1); t += kSortThreads) {
+          const int lo = 2 * t - (t & (j - 1));  // index with bit j clear
+          const int hi = lo + j;
+          const unsigned long long a = s[lo], b = s[hi];
+          const bool up = (lo & k) == 0;
+          if ((a > b) == up) {
+            s[lo] = b;
+            s[hi] = a;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = threadIdx.x; i < c; i += kSortThreads) {
+      const unsigned long long e = s[i];
+      L[i] = (int32_t)(uint32_t)e;
+      Kb[i] = float_from_order_bits((uint32_t)(e >> 32));
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // K2: fine rasterization — warp-autonomous, (face, pixel) pairs evaluated lane-parallel
 //
 // Work item = one 8x4 pixel micro-tile of one bin of one mesh. Warps of a persistent grid pull items from a
@@ -164,13 +244,16 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
 // emit time (MR:178-197), so the payload carries exactly the bits the candidate test produced.
 
 #ifndef DR_RING
-#define DR_RING 64
+#define DR_RING 48
 #endif
 #ifndef DR_FINE_MINBLOCKS
 #define DR_FINE_MINBLOCKS 0
 #endif
 #ifndef DR_EMIT_PREFETCH
 #define DR_EMIT_PREFETCH 1
+#endif
+#ifndef DR_COMPACT
+#define DR_COMPACT 1  // compact the pairs the K-th-depth cull leaves before evaluating them
 #endif
 #ifndef DR_LEAN_STAGE
 #define DR_LEAN_STAGE 1
@@ -191,11 +274,14 @@ struct WarpSmem {
   double* d;        // [kNF][kRing]
   int32_t* fid;     // [kRing]
   uint32_t* rect;   // [kRing] covered rectangle in the micro-tile: r0 | c0<<4 | h<<8 | w<<12 | recip(w)<<16
+  float* fkey;      // [kRing] depth key (zkey) of the staged face
   double* tz;       // [K][32]      sorted top-K lists, column p = pixel p of the micro-tile
   int32_t* tid;     // [K][32]
   double* bz;       // [kBuf][32]   unsorted per-pixel candidate buffers (merged by the owner lane)
   int32_t* bid;     // [kBuf][32]
   int32_t* bcnt;    // [32]
+  double* pxy;      // [12] pixel-centre NDC coordinates of the micro-tile: x of its 8 columns, y of its 4 rows
+  uint32_t* pairq;  // [64] queued (ring slot << 5 | pixel) pairs awaiting evaluation
 
   __device__ __forceinline__ double get(int f, int k) const { return d[f * kRing + k]; }
   __device__ __forceinline__ void put(int f, int k, double v) const { d[f * kRing + k] = v; }
@@ -225,7 +311,7 @@ struct WarpSmem {
     }
     return g;
   }
-  __device__ __forceinline__ void stage(int k, const double* fv, int32_t f, uint32_t r) const {
+  __device__ __forceinline__ void stage(int k, const double* fv, int32_t f, uint32_t r, float key) const {
     double v[9];
     const double* p = fv + 9 * (int64_t)f;
 #pragma unroll
@@ -241,15 +327,18 @@ struct WarpSmem {
     }
     fid[k] = f;
     rect[k] = r;
+    fkey[k] = key;
   }
 };
 
 constexpr int kBuf = 8;  // buffered candidates per pixel before the owner lane merges them into its list
 
+// per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt
 __host__ __device__ constexpr size_t warp_smem_bytes(int K) {
-  return (size_t)kNF * kRing * sizeof(double) + (size_t)kRing * (sizeof(int32_t) + sizeof(uint32_t)) +
-         (size_t)K * 32 * (sizeof(double) + sizeof(int32_t)) + (size_t)kBuf * 32 * (sizeof(double) + sizeof(int32_t)) +
-         32 * sizeof(int32_t);
+  return (size_t)kNF * kRing * sizeof(double) + (size_t)K * 32 * sizeof(double) + (size_t)kBuf * 32 * sizeof(double) +
+         12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) + (size_t)K * 32 * sizeof(int32_t) +
+         (size_t)kBuf * 32 * sizeof(int32_t) + (size_t)kRing * (sizeof(uint32_t) + sizeof(float)) +
+         32 * sizeof(int32_t) + 64 * sizeof(uint32_t) + 8;  // + pad keeps the next warp's base 8-byte aligned
 }
 
 // Rectangle of the micro-tile (rows i0..i0+3, cols j0..j0+7, limited to vh x vw existing pixels) covered by
@@ -266,12 +355,22 @@ __device__ __forceinline__ uint32_t cover_rect(int4 ib, int i0, int j0, int vh, 
 __device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
 template <typename OutT>
-__device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot, bool occupied, double z,
+#ifndef DR_EMIT_INLINE
+#define DR_EMIT_INLINE 1
+#endif
+#if DR_EMIT_INLINE
+#define DR_EMIT_ATTR __forceinline__
+#else
+#define DR_EMIT_ATTR __noinline__
+#endif
+__device__ DR_EMIT_ATTR void emit_slot(const FineArgs<OutT>& A, int64_t slot, bool occupied, double z,
                                           int32_t fid, const double* v, double px, double py) {
   if (occupied) {
     const FaceGeom g = make_face_geom(v);
     PixelFaceResult r;
-    eval_pixel_face<true>(V2{px, py}, g, A.blur, A.znear, A.persp, A.clip, r);  // same ops => same bits
+    // fp64 payload: the identical operation sequence => the bits the candidate test produced; fp32 payload: the
+    // same formulas with fast (<= 1 ulp) divisions, rounded once to fp32 (selection is already decided)
+    eval_pixel_face<true, std::is_same<OutT, double>::value>(V2{px, py}, g, A.blur, A.znear, A.persp, A.clip, r);
     A.p2f[slot] = fid;
     A.zbuf[slot] = (OutT)z;
     A.bary[3 * slot + 0] = (OutT)r.bary[0];
@@ -309,8 +408,16 @@ __device__ __forceinline__ void list_insert(const WarpSmem& ws, int K, int p, do
 // at once, and for K <= KMAX the list lives in registers during the merge (fully unrolled insertion: no
 // shared-memory load -> compare -> branch chain). The merge runs outside the fp64 evaluation, so these
 // registers do not add to the evaluation's pressure.
+#ifndef DR_MERGE_INLINE
+#define DR_MERGE_INLINE 1
+#endif
+#if DR_MERGE_INLINE
+#define DR_MERGE_ATTR __forceinline__
+#else
+#define DR_MERGE_ATTR __noinline__
+#endif
 template <int KMAX>
-__device__ __forceinline__ void merge_buffers(const WarpSmem& ws, int K, int lane) {
+__device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane) {
   const int n = ws.bcnt[lane];
   if (n > 0) {
     if constexpr (KMAX == 0) {
@@ -326,6 +433,7 @@ __device__ __forceinline__ void merge_buffers(const WarpSmem& ws, int K, int lan
       for (int c = 0; c < n; ++c) {
         const double zc = ws.bz[c * 32 + lane];
         const int32_t ic = ws.bid[c * 32 + lane];
+        if (!cand_less(zc, ic, z[KMAX - 1], id[KMAX - 1])) continue;  // not below the list tail
 #pragma unroll
         for (int s = KMAX - 1; s >= 0; --s) {
           const int sp = s > 0 ? s - 1 : 0;
@@ -352,10 +460,64 @@ __device__ __forceinline__ void merge_buffers(const WarpSmem& ws, int K, int lan
   }
 }
 
-// Evaluate the pairs of ring slots [head, head+G) (mod kRing) and insert the survivors.
+// Evaluate the first n (<= 32) queued (face slot, pixel) pairs, one per lane, and insert the survivors.
 template <int KMAX, typename OutT>
-__device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const WarpSmem& ws, int head, int G, int mi0,
-                                              int mj0, int lane) {
+__device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSmem& ws, int n, int lane) {
+  const int K = A.K;
+  const uint32_t e = lane < n ? ws.pairq[lane] : 0x80000000u;
+  const bool act = !(e >> 31);  // bit 31: culled (DR_COMPACT=0 keeps culled pairs in place)
+  bool pass = false;
+  int p = 0;
+  int32_t f = 0;
+  PixelFaceResult res;
+  if (act) {
+    const int k = (int)(e >> 5);
+    p = (int)(e & 31u);
+    const FaceGeom fg = ws.geom(k);
+    const V2 pix{ws.pxy[p & 7], ws.pxy[8 + (p >> 3)]};
+    pass = eval_pixel_face<false>(pix, fg, A.blur, A.znear, A.persp, A.clip, res);
+    f = ws.fid[k];
+  }
+  STAT_ADD(3, __popc(__ballot_sync(0xffffffffu, act)));
+  STAT_ADD(4, __popc(__ballot_sync(0xffffffffu, pass)));
+  STAT_ADD(7, 1);
+  if (__any_sync(0xffffffffu, pass)) {
+    // append to the pixel's buffer; merge every buffer first if one would overflow
+    const unsigned peers = __match_any_sync(0xffffffffu, pass ? p : 32 + lane);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    const int n_same = __popc(peers);
+    int base = pass ? ws.bcnt[p] : 0;
+    if (__any_sync(0xffffffffu, pass && base + n_same > kBuf)) {
+      __syncwarp();
+      merge_buffers<KMAX>(ws, K, lane);
+      __syncwarp();
+      base = 0;
+    }
+    if (pass) {
+      if (rank < kBuf) {
+        ws.bz[(base + rank) * 32 + p] = res.z;
+        ws.bid[(base + rank) * 32 + p] = f;
+      }
+      if (rank == 0) ws.bcnt[p] = base + min(n_same, kBuf);
+    }
+    __syncwarp();
+    // more than kBuf candidates for one pixel in one step (rare): insert the excess directly, one at a time
+    const int extra = __reduce_max_sync(0xffffffffu, pass ? n_same - kBuf : 0);
+    for (int rr = 0; rr < extra; ++rr) {
+      if (pass && rank == kBuf + rr) list_insert(ws, K, p, res.z, f);
+      __syncwarp();
+    }
+  }
+}
+
+// Enumerate the (face, pixel) pairs of ring slots [head, head+G) (mod kRing): prefix sum of the covered
+// rectangle areas across lanes, then 32 pairs per step, one per lane (binary search over the prefix with
+// shuffles). Pairs the K-th-depth cull cannot rule out are compacted (ballot) into the warp's pair queue and
+// evaluated 32 at a time, so culled pairs cost no fp64 work and evaluation steps keep every lane busy. The
+// queue is drained before returning (its entries name ring slots the caller recycles).
+template <int KMAX, typename OutT>
+__device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const WarpSmem& ws, int head, int G,
+                                              int lane) {
   const int K = A.K;
   const int slot_l = (head + lane) % kRing;
   const uint32_t rl = lane < G ? ws.rect[slot_l] : 0u;
@@ -367,63 +529,64 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
     if (lane >= d) incl += t;
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
-  for (int base = 0; base < total; base += 32) {
-    const int j = base + lane;
-    const bool act = j < total;
-    // face lane = first lane whose inclusive prefix exceeds j
-    int lo = 0;
+  int qn = 0;  // queued pairs (< 32 between steps)
+  int base = 0;
+  // one loop, one inlined copy of eval_pairs (instruction-cache footprint is a first-order cost here)
+  for (;;) {
+    if (base < total) {
+      const int j = base + lane;
+      const bool act = j < total;
+      // face lane = first lane whose inclusive prefix exceeds j
+      int lo = 0;
 #pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-      const int pv = __shfl_sync(0xffffffffu, incl, lo + step - 1);
-      if (pv <= j) lo += step;
-    }
-    lo = min(lo, 31);
-    const int excl = __shfl_sync(0xffffffffu, incl - cnt, lo);
-    const uint32_t r = __shfl_sync(0xffffffffu, rl, lo);
-    bool pass = false;
-    int p = 0;
-    int32_t f = 0;
-    PixelFaceResult res;
-    if (act) {
-      const int rank = j - excl;
-      const int w = (int)((r >> 12) & 15u);
-      const int dr = (rank * (int)(r >> 16)) >> 8;
-      const int row = (int)(r & 15u) + dr;
-      const int col = (int)((r >> 4) & 15u) + (rank - dr * w);
-      p = row * 8 + col;
-      const int k = (head + lo) % kRing;
-      const FaceGeom fg = ws.geom(k);
-      const V2 pix{pixel_x(A.W, mj0 + col), pixel_y(A.H, mi0 + row)};
-      pass = eval_pixel_face<false>(pix, fg, A.blur, A.znear, A.persp, A.clip, res);
-      f = ws.fid[k];
-    }
-    if (__any_sync(0xffffffffu, pass)) {
-      // append to the pixel's buffer; merge every buffer first if one would overflow
-      const unsigned peers = __match_any_sync(0xffffffffu, pass ? p : 32 + lane);
-      const int rank = __popc(peers & ((1u << lane) - 1u));
-      const int n_same = __popc(peers);
-      int base = pass ? ws.bcnt[p] : 0;
-      if (__any_sync(0xffffffffu, pass && base + n_same > kBuf)) {
-        __syncwarp();
-        merge_buffers<KMAX>(ws, K, lane);
-        __syncwarp();
-        base = 0;
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int pv = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+        if (pv <= j) lo += step;
       }
-      if (pass) {
-        if (rank < kBuf) {
-          ws.bz[(base + rank) * 32 + p] = res.z;
-          ws.bid[(base + rank) * 32 + p] = f;
-        }
-        if (rank == 0) ws.bcnt[p] = base + min(n_same, kBuf);
+      lo = min(lo, 31);
+      const int excl = __shfl_sync(0xffffffffu, incl - cnt, lo);
+      const uint32_t r = __shfl_sync(0xffffffffu, rl, lo);
+      bool keep = false;
+      uint32_t entry = 0;
+      if (act) {
+        const int rank = j - excl;
+        const int w = (int)((r >> 12) & 15u);
+        const int dr = (rank * (int)(r >> 16)) >> 8;
+        const int row = (int)(r & 15u) + dr;
+        const int col = (int)((r >> 4) & 15u) + (rank - dr * w);
+        const int p = row * 8 + col;
+        const int k = (head + lo) % kRing;
+        // K-th-depth cull: every z this face can produce is > its key; if the key already exceeds the pixel's
+        // current K-th candidate the face cannot enter the pixel's list (strict (z, id) order, MR:138-140)
+        keep = !A.zsort || !((double)ws.fkey[k] > ws.tz[(K - 1) * 32 + p]);
+        entry = ((uint32_t)k << 5) | (uint32_t)p;
+      }
+      STAT_ADD(2, __popc(__ballot_sync(0xffffffffu, act)));
+#if DR_COMPACT
+      const unsigned kb = __ballot_sync(0xffffffffu, keep);
+#else
+      const unsigned kb = __ballot_sync(0xffffffffu, act);
+      if (!keep) entry |= 0x80000000u;
+      keep = act;
+#endif
+      if (keep) ws.pairq[qn + __popc(kb & ((1u << lane) - 1u))] = entry;
+      qn += __popc(kb);
+      base += 32;
+      __syncwarp();
+    }
+    const bool drain = base >= total;
+    if (qn >= 32 || (drain && qn > 0)) {
+      const int n = min(qn, 32);
+      eval_pairs<KMAX>(A, ws, n, lane);
+      qn -= n;
+      if (qn > 0) {  // move the remainder to the front
+        const uint32_t t = lane < qn ? ws.pairq[32 + lane] : 0u;
+        __syncwarp();
+        if (lane < qn) ws.pairq[lane] = t;
       }
       __syncwarp();
-      // more than kBuf candidates for one pixel in one step (rare): insert the excess directly, one at a time
-      const int extra = __reduce_max_sync(0xffffffffu, pass ? n_same - kBuf : 0);
-      for (int rr = 0; rr < extra; ++rr) {
-        if (pass && rank == kBuf + rr) list_insert(ws, K, p, res.z, f);
-        __syncwarp();
-      }
     }
+    if (drain && qn == 0) break;
   }
 }
 
@@ -439,14 +602,15 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(K);
     ws.d = reinterpret_cast<double*>(base);
     ws.tz = ws.d + kNF * kRing;
-    ws.fid = reinterpret_cast<int32_t*>(ws.tz + K * 32);
+    ws.bz = ws.tz + K * 32;
+    ws.pxy = ws.bz + kBuf * 32;
+    ws.fid = reinterpret_cast<int32_t*>(ws.pxy + 12);
     ws.tid = ws.fid + kRing;
-    ws.rect = reinterpret_cast<uint32_t*>(ws.tid + K * 32);
-    ws.bz = reinterpret_cast<double*>(base + (size_t)kNF * kRing * sizeof(double) + (size_t)K * 32 * sizeof(double) +
-                                      (size_t)kRing * (sizeof(int32_t) + sizeof(uint32_t)) +
-                                      (size_t)K * 32 * sizeof(int32_t));
-    ws.bid = reinterpret_cast<int32_t*>(ws.bz + kBuf * 32);
-    ws.bcnt = ws.bid + kBuf * 32;
+    ws.bid = ws.tid + K * 32;
+    ws.rect = reinterpret_cast<uint32_t*>(ws.bid + kBuf * 32);
+    ws.fkey = reinterpret_cast<float*>(ws.rect + kRing);
+    ws.bcnt = reinterpret_cast<int32_t*>(ws.fkey + kRing);
+    ws.pairq = reinterpret_cast<uint32_t*>(ws.bcnt + 32);
   }
   const int nbins = A.nbx * A.nby;
   const int mtx = (A.bs + 7) >> 3, mty = (A.bs + 3) >> 2;  // micro-tiles per bin row / column
@@ -468,6 +632,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     const int mi0 = bi0 + (mt / mtx) * 4, mj0 = bj0 + (mt % mtx) * 8;
     const int vh = min(4, bi1 - mi0 + 1), vw = min(8, bj1 - mj0 + 1);  // existing pixels of the micro-tile
     if (vh <= 0 || vw <= 0) continue;
+    STAT_ADD(5, 1);
 
     // candidate faces: the bin list, or the whole mesh (naive mode / overflowed bin)
     const int64_t f0 = A.first[b], nf = A.num[b];
@@ -485,16 +650,30 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       ws.tid[s * 32 + lane] = INT_MAX;
     }
     ws.bcnt[lane] = 0;
+    if (lane < 8) ws.pxy[lane] = pixel_x(A.W, mj0 + lane);               // camera.cpp:100-102, once per
+    else if (lane < 12) ws.pxy[lane] = pixel_y(A.H, mi0 + (lane - 8));   // micro-tile instead of per pair
     __syncwarp();
 
+    // depth-ordered list (K1b) => once the next key exceeds every pixel's K-th depth, no later face can enter
+    const float* keys = nullptr;
+    if (A.zsort && list && nsrc <= kSortMax) keys = A.bin_keys + ((int64_t)b * nbins + bin) * A.cap;
+    const bool valid_px = (lane >> 3) < vh && (lane & 7) < vw;
+    double T = pos_inf();  // max over the micro-tile's pixels of the K-th candidate depth (+inf: a list not full)
     int head = 0, pending = 0;
     for (int64_t c0 = 0; c0 < nsrc; c0 += 32) {
       const int64_t ci = c0 + lane;
       uint32_t r = 0u;
       int32_t fid = -1;
+      float key = 0.f;
+      if (keys && (double)keys[c0] > T) {
+        STAT_ADD(6, 1);
+        break;
+      }
+      STAT_ADD(0, __popc(__ballot_sync(0xffffffffu, ci < nsrc)));
       if (ci < nsrc) {
         fid = list ? list[ci] : (int32_t)(f0 + ci);
-        r = cover_rect(A.ibbox[fid], mi0, mj0, vh, vw);
+        if (A.zsort) key = keys ? keys[ci] : A.zkey[fid];
+        if (!A.zsort || !((double)key > T)) r = cover_rect(A.ibbox[fid], mi0, mj0, vh, vw);
       }
       unsigned todo = __ballot_sync(0xffffffffu, r != 0u);
       const bool last = c0 + 32 >= nsrc;
@@ -504,17 +683,35 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
         const int rank = __popc(todo & ((1u << lane) - 1u));
         const bool mine = ((todo >> lane) & 1u) && rank < room;
         const unsigned take = __ballot_sync(0xffffffffu, mine);
-        if (mine) ws.stage((head + pending + rank) % kRing, A.fv, fid, r);
+        if (mine) ws.stage((head + pending + rank) % kRing, A.fv, fid, r, key);
         pending += __popc(take);
+        STAT_ADD(1, __popc(take));
         todo &= ~take;
         __syncwarp();
+        bool ran = false;
         while (pending >= 32 || (last && todo == 0u && pending > 0)) {
           const int G = min(pending, 32);
-          process_group<KMAX>(A, ws, head, G, mi0, mj0, lane);
+          process_group<KMAX>(A, ws, head, G, lane);
           head = (head + G) % kRing;
           pending -= G;
+          ran = true;
+        }
+        if (A.zsort && ran) {  // refresh T: merge the buffered candidates, then max of the K-th depths
+          __syncwarp();
+          merge_buffers<KMAX>(ws, K, lane);
+          __syncwarp();
+          double t = valid_px ? ws.tz[(K - 1) * 32 + lane] : -pos_inf();
+#pragma unroll
+          for (int d = 16; d >= 1; d >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, d));
+          T = t;
         }
       } while (todo);
+    }
+    while (pending > 0) {  // faces staged before an early exit
+      const int G = min(pending, 32);
+      process_group<KMAX>(A, ws, head, G, lane);
+      head = (head + G) % kRing;
+      pending -= G;
     }
     __syncwarp();
     merge_buffers<KMAX>(ws, K, lane);
@@ -565,10 +762,10 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 // host-side launchers (called from capi.cu)
 
 void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int W, double inflate, double znear,
-                       int clip_z, int cull, int4* ibbox, cudaStream_t st) {
+                       int clip_z, int cull, int4* ibbox, float* zkey, cudaStream_t st) {
   if (f_hi <= f_lo) return;
   unsigned grid = (unsigned)((f_hi - f_lo + 255) / 256);
-  k_face_setup<<<grid, 256, 0, st>>>(fv, f_lo, f_hi, H, W, inflate, znear, clip_z, cull, ibbox);
+  k_face_setup<<<grid, 256, 0, st>>>(fv, f_lo, f_hi, H, W, inflate, znear, clip_z, cull, ibbox, zkey);
 }
 
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
@@ -577,6 +774,13 @@ void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* nu
   unsigned gx = (unsigned)std::min<int64_t>((max_faces + 255) / 256, 65535);
   dim3 grid(gx, (unsigned)N);
   k_bin_faces<<<grid, 256, 0, st>>>(ibbox, first, num, bs, nbx, nby, cap, counts, lists);
+}
+
+void launch_sort_bins(const int* counts, int32_t* lists, float* keys, const float* zkey, int64_t nbins_total, int cap,
+                      cudaStream_t st) {
+  if (nbins_total <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(nbins_total, 148 * 16);
+  k_sort_bins<<<grid, kSortThreads, 0, st>>>(counts, lists, keys, zkey, nbins_total, cap);
 }
 
 template <typename OutT>
@@ -612,3 +816,15 @@ cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st) {
 cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st) { return launch_fine_t(A, nwarps, st); }
 
 }  // namespace drb
+
+#if DR_STATS
+extern "C" int dr_debug_stats(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_stats, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

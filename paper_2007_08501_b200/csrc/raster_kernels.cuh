@@ -16,6 +16,9 @@ struct FineArgs {
   const int64_t* num;       // [N] num_faces_per_mesh
   const int* bin_counts;    // [N, nby, nbx] entries per bin (may exceed cap: overflow => spill path)
   const int32_t* bin_lists; // [N, nby, nbx, cap] packed face ids
+  const float* zkey;        // [F] lower bound on any z the face can produce at any pixel (zsort only)
+  const float* bin_keys;    // [N, nby, nbx, cap] zkey of each bin entry, entries sorted ascending (zsort only)
+  int zsort;                // 1 => depth-ordered bins + K-th-depth culling (needs clip_barycentric_coords)
   int binned;               // 0 => naive: every CTA scans its whole mesh
   int cap;                  // max_faces_per_bin
   int bs, nbx, nby;         // bin (tile) side in pixels, bins per row / column
@@ -73,7 +76,10 @@ cudaError_t launch_item_to_element(const int64_t* first, const int64_t* num, int
                                    cudaStream_t st);
 
 void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int W, double inflate, double znear,
-                       int clip_z, int cull, int4* ibbox, cudaStream_t st);
+                       int clip_z, int cull, int4* ibbox, float* zkey, cudaStream_t st);
+constexpr int kSortMax = 4096;  // bins longer than this stay unsorted (culling still applies, early exit does not)
+void launch_sort_bins(const int* counts, int32_t* lists, float* keys, const float* zkey, int64_t nbins_total, int cap,
+                      cudaStream_t st);
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
                       int bs, int nbx, int nby, int cap, int* counts, int32_t* lists, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);

@@ -406,3 +406,4 @@ def test_host_pipeline_matches_device_calls(cuda):
     gref = rasterize_meshes_backward(fvd, torch.as_tensor(first, device=cuda), torch.as_tensor(num, device=cuda), rs,
                                      ref[0], ref[2], *(c.to(cuda) for c in cot))
     assert rel_err(grad_h.numpy(), gref.cpu().numpy()) < 1e-12
+
