@@ -104,7 +104,7 @@ struct RasterSettings {
   double blur_radius = 1e-4;     // squared NDC distance
   int tile_size = 16;            // bin side in pixels (north-star `bin_size`)
   // north-star parameters (defaults = the reference's only behaviour)
-  int max_faces_per_bin = 0;     // 0 = automatic; overflow never changes results
+  int max_faces_per_bin = 0;     // 0 = unlimited (exact-size lists); overflow never changes results
   bool perspective_correct = false;
   bool clip_barycentric_coords = true;
   bool cull_backfaces = false;

@@ -56,7 +56,8 @@ typedef struct dr_raster_settings {
   int32_t faces_per_pixel;     /* K >= 1 (RasterSettings.faces_per_pixel) */
   int32_t bin_size;            /* 0 => naive semantics (mesh_raster.cpp:214); > 0 => coarse-to-fine with
                                   bins of bin_size x bin_size pixels (RasterSettings.tile_size) */
-  int32_t max_faces_per_bin;   /* fast-path capacity of one bin list; 0 => automatic. A bin that overflows
+  int32_t max_faces_per_bin;   /* longest bin list the fast path uses; 0 => unlimited (lists are sized
+                                  exactly: count -> scan -> fill). A longer bin (or one past the list pool)
                                   is rasterized by the spill path: results never change (reference bins
                                   are unbounded, mesh_raster.cpp:244) */
   int32_t _reserved0;          /* must be 0 */
@@ -173,7 +174,8 @@ const char* dr_last_error(void);
 /* ---- diagnostics (not part of the reference surface) ---- */
 
 /* Reads the coarse-stage counters a forward left in `workspace` (synchronises `stream`):
- * out[0] = bins, out[1] = bins that overflowed max_faces_per_bin (spill path), out[2] = total bin entries,
+ * out[0] = bins, out[1] = bins on the spill path (longer than max_faces_per_bin or past the list pool),
+ * out[2] = total bin entries,
  * out[3] = largest bin. Returns DR_ERR_USAGE for bin_size == 0. */
 int dr_rasterize_meshes_bin_stats(int64_t N, int64_t F, const dr_raster_settings* s, const void* workspace,
                                   dr_stream_t stream, int64_t out[4]);

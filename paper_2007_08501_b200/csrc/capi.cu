@@ -85,7 +85,9 @@ struct Plan {
   bool binned = false;
   int nbx = 0, nby = 0, cap = 0;
   bool zsort = false;  // depth-ordered bins + K-th-depth culling (clip_barycentric_coords only)
-  size_t off_ibbox = 0, off_zkey = 0, off_counter = 0, off_counts = 0, off_lists = 0, off_keys = 0, total = 0;
+  int64_t nbins_total = 0, pool = 0;  // N * bins; list-pool capacity (entries)
+  size_t off_ibbox = 0, off_zkey = 0, off_counter = 0, off_counts = 0, off_cursor = 0, off_binoff = 0, off_lists = 0,
+         off_keys = 0, total = 0;
 };
 
 // DR_ZSORT=0 disables the depth-ordered fine stage (A/B measurements; results are identical either way)
@@ -97,7 +99,9 @@ bool zsort_enabled() {
   return on;
 }
 
-int auto_cap(int64_t F) { return (int)std::max<int64_t>(1, std::min<int64_t>(F, 4096)); }
+// list-pool capacity: the workspace is planned before the bin counts exist; 8 entries per face covers every
+// benchmark scene (faces touch 1-2 bins on average); bins past the pool take the exact spill path
+int64_t pool_entries(int64_t F) { return 8 * F + 65536; }
 
 int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
   if (!s) return fail(DR_ERR_USAGE, "settings pointer is null");
@@ -121,7 +125,7 @@ int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
   p.bs = p.binned ? s->bin_size : 16;
   p.nbx = (p.W + p.bs - 1) / p.bs;
   p.nby = (p.H + p.bs - 1) / p.bs;
-  p.cap = p.binned ? (s->max_faces_per_bin > 0 ? s->max_faces_per_bin : auto_cap(F)) : 0;
+  p.cap = p.binned ? s->max_faces_per_bin : 0;  // 0 = unlimited (the reference's bins are unbounded, MR:244)
   p.zsort = s->clip_barycentric_coords != 0 && zsort_enabled();
   size_t off = 0;
   p.off_ibbox = off;
@@ -132,12 +136,18 @@ int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
   off = align_up(off + sizeof(unsigned long long));
   p.off_counts = off;
   if (p.binned) {
-    off = align_up(off + sizeof(int) * (size_t)N * p.nbx * p.nby);
+    p.nbins_total = N * (int64_t)p.nbx * p.nby;
+    p.pool = pool_entries(F);
+    off = align_up(off + sizeof(int) * (size_t)p.nbins_total);
+    p.off_cursor = off;
+    off = align_up(off + sizeof(int) * (size_t)p.nbins_total);
+    p.off_binoff = off;
+    off = align_up(off + sizeof(int64_t) * (size_t)p.nbins_total);
     p.off_lists = off;
-    off = align_up(off + sizeof(int32_t) * (size_t)N * p.nbx * p.nby * (size_t)p.cap);
+    off = align_up(off + sizeof(int32_t) * (size_t)p.pool);
     if (p.zsort) {
       p.off_keys = off;
-      off = align_up(off + sizeof(float) * (size_t)N * p.nbx * p.nby * (size_t)p.cap);
+      off = align_up(off + sizeof(float) * (size_t)p.pool);
     }
   }
   p.total = off;
@@ -220,6 +230,8 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   int4* ibbox = reinterpret_cast<int4*>(base + p.off_ibbox);
   int* counts = reinterpret_cast<int*>(base + p.off_counts);
   int32_t* lists = reinterpret_cast<int32_t*>(base + p.off_lists);
+  int* cursor = reinterpret_cast<int*>(base + p.off_cursor);
+  int64_t* bin_off = reinterpret_cast<int64_t*>(base + p.off_binoff);
   float* zkey = reinterpret_cast<float*>(base + p.off_zkey);
   float* bin_keys = p.zsort && p.binned ? reinterpret_cast<float*>(base + p.off_keys) : nullptr;
   const double inflate = std::sqrt(std::max(0.0, s->blur_radius));  // MR:103
@@ -233,15 +245,20 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   if (p.binned) {
     {
       ProfScope ps(st, KN_MEMSET);
-      cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)N * p.nbx * p.nby, st);
+      cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)p.nbins_total, st);
+      cudaMemsetAsync(cursor, 0, sizeof(int) * (size_t)p.nbins_total, st);
     }
     {
-      ProfScope ps(st, KN_BIN);
-      drb::launch_bin_faces(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, p.cap, counts, lists, st);
+      ProfScope ps(st, KN_BIN);  // count -> scan -> fill: exact-size lists
+      drb::launch_bin_faces(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, counts, st);
+      drb::launch_scan_bins(counts, p.nbins_total, bin_off, st);
+      drb::launch_fill_bins(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool,
+                            lists, st);
     }
     if (p.zsort) {
       ProfScope ps(st, KN_SORT);
-      drb::launch_sort_bins(counts, lists, bin_keys, zkey, N * (int64_t)p.nbx * p.nby, p.cap, st);
+      cudaError_t e = drb::launch_sort_bins(counts, bin_off, lists, bin_keys, zkey, p.nbins_total, p.pool, p.cap, st);
+      if (e != cudaSuccess) return cuda_fail(e, "sorting bins");
     }
   }
   drb::FineArgs<OutT> A;
@@ -251,6 +268,8 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   A.num = num;
   A.bin_counts = counts;
   A.bin_lists = lists;
+  A.bin_off = bin_off;
+  A.pool = p.pool;
   A.zkey = zkey;
   A.bin_keys = bin_keys;
   A.zsort = p.zsort ? 1 : 0;
@@ -516,18 +535,22 @@ int dr_rasterize_meshes_bin_stats(int64_t N, int64_t F, const dr_raster_settings
   if (rc) return rc;
   if (!p.binned) return fail(DR_ERR_USAGE, "bin_stats: bin_size == 0 (naive path has no bins)");
   if (!ws || !out) return fail(DR_ERR_USAGE, "null pointer");
-  size_t nb = (size_t)N * p.nbx * p.nby;
+  size_t nb = (size_t)p.nbins_total;
   std::vector<int> h(nb);
+  std::vector<int64_t> ho(nb);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemcpyAsync(h.data(), static_cast<const char*>(ws) + p.off_counts, sizeof(int) * nb,
                                   cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ho.data(), static_cast<const char*>(ws) + p.off_binoff, sizeof(int64_t) * nb,
+                        cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "bin_stats");
   int64_t over = 0, tot = 0, mx = 0;
-  for (int c : h) {
-    over += c > p.cap;
-    tot += c;
-    mx = std::max<int64_t>(mx, c);
+  for (size_t i = 0; i < nb; ++i) {
+    over += !drb::bin_fits(ho[i], h[i], p.pool, p.cap);
+    tot += h[i];
+    mx = std::max<int64_t>(mx, h[i]);
   }
   out[0] = (int64_t)nb;
   out[1] = over;

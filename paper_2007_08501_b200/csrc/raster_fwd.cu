@@ -123,23 +123,28 @@ __global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ f
 }
 
 // ------------------------------------------------------------------------------------------------
-// K1: coarse binning. Each warp walks 32 consecutive faces of one mesh; the bins a face touches form a
-// rectangle of the bin grid. Lanes that target the same bin in the same round are grouped with
-// __match_any_sync and reserve their slots with ONE atomicAdd (leader), so adjacent faces of a mesh
-// (which mostly share bins) cost one global atomic per (warp, bin). Order inside a bin is irrelevant:
-// the K smallest under the strict total order (z, id) do not depend on it (MR:138-140).
+// K1: coarse binning (pass 1, MR:237-264) into EXACT-size lists: count -> exclusive scan -> fill.
+// Each warp walks 32 consecutive faces of one mesh; the bins a face touches form a rectangle of the bin grid.
+// Lanes that target the same bin in the same round are grouped with __match_any_sync and reserve their slots
+// with ONE atomicAdd (leader), so adjacent faces of a mesh (which mostly share bins) cost one global atomic per
+// (warp, bin). Order inside a bin is irrelevant: the K smallest under the strict total order (z, id) do not
+// depend on it (MR:138-140). The lists live in one pool sized from F (workspace is planned before the counts
+// are known); a bin that does not fit the pool, or exceeds the caller's max_faces_per_bin, takes the spill
+// path in K2 (its micro-tiles scan the whole mesh), so results never depend on either capacity.
 
+template <bool kFill>
 __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbox, const int64_t* __restrict__ first,
-                                                   const int64_t* __restrict__ num, int bs, int nbx, int nby, int cap,
-                                                   int* __restrict__ counts, int32_t* __restrict__ lists) {
+                                                   const int64_t* __restrict__ num, int bs, int nbx, int nby,
+                                                   int* __restrict__ counts, const int64_t* __restrict__ off,
+                                                   int* __restrict__ cursor, int64_t pool,
+                                                   int32_t* __restrict__ lists) {
   const int b = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int64_t nf = num[b], f0 = first[b];
   const int nbins = nbx * nby;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int* cnt = counts + (int64_t)b * nbins;
-  int32_t* lst = lists + (int64_t)b * nbins * cap;
+  const int64_t bin0 = (int64_t)b * nbins;
   for (int64_t base = warp * 32; base < nf; base += nwarps * 32) {
     int64_t lf = base + lane;
     int4 ib = lf < nf ? ibbox[f0 + lf] : make_int4(1, 0, 1, 0);
@@ -156,11 +161,43 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
       unsigned peers = __match_any_sync(0xffffffffu, key);
       int leader = __ffs(peers) - 1;
       int rank = __popc(peers & ((1u << lane) - 1u));
-      int base_slot = 0;
-      if (active && lane == leader) base_slot = atomicAdd(cnt + key, __popc(peers));
-      base_slot = __shfl_sync(0xffffffffu, base_slot, leader);
-      if (active && base_slot + rank < cap) lst[(int64_t)key * cap + base_slot + rank] = (int32_t)(f0 + lf);
+      if constexpr (!kFill) {
+        if (active && lane == leader) atomicAdd(counts + bin0 + key, __popc(peers));
+      } else {
+        int64_t pos = -1;
+        if (active && lane == leader) {
+          const int64_t o = off[bin0 + key];
+          if (o + counts[bin0 + key] <= pool) pos = o + atomicAdd(cursor + bin0 + key, __popc(peers));
+        }
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (active && pos >= 0) lists[pos + rank] = (int32_t)(f0 + lf);
+      }
     }
+  }
+}
+
+// exclusive scan of the bin counts (one CTA; N * bins is at most a few million)
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) k_scan_bins(const int* __restrict__ counts, int64_t n,
+                                                            int64_t* __restrict__ off) {
+  __shared__ int64_t part[kScanThreads];
+  const int t = threadIdx.x;
+  const int64_t per = (n + kScanThreads - 1) / kScanThreads;
+  const int64_t lo = min(n, (int64_t)t * per), hi = min(n, lo + per);
+  int64_t sum = 0;
+  for (int64_t i = lo; i < hi; ++i) sum += counts[i];
+  part[t] = sum;
+  __syncthreads();
+  for (int d = 1; d < kScanThreads; d <<= 1) {  // Hillis-Steele inclusive scan of the partial sums
+    const int64_t v = t >= d ? part[t - d] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int64_t run = part[t] - sum;
+  for (int64_t i = lo; i < hi; ++i) {
+    off[i] = run;
+    run += counts[i];
   }
 }
 
@@ -180,15 +217,23 @@ __device__ __forceinline__ float float_from_order_bits(uint32_t u) {
 
 constexpr int kSortThreads = 256;
 
-__global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restrict__ counts, int32_t* __restrict__ lists,
-                                                            float* __restrict__ keys, const float* __restrict__ zkey,
-                                                            int64_t nbins_total, int cap) {
-  __shared__ unsigned long long s[kSortMax];
+// MAXN = shared-memory capacity in entries; bins with (MINN, MAXN] entries are sorted by this instantiation
+template <int MAXN, int MINN, bool kDyn>
+__global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restrict__ counts,
+                                                            const int64_t* __restrict__ off,
+                                                            int32_t* __restrict__ lists, float* __restrict__ keys,
+                                                            const float* __restrict__ zkey, int64_t nbins_total,
+                                                            int64_t pool, int cap) {
+  __shared__ unsigned long long s_static[kDyn ? 1 : MAXN];
+  extern __shared__ unsigned long long s_dyn[];
+  unsigned long long* s = kDyn ? s_dyn : s_static;
   for (int64_t bin = blockIdx.x; bin < nbins_total; bin += gridDim.x) {
     const int c = counts[bin];
-    if (c <= 0 || c > cap || c > kSortMax) continue;  // empty, overflowed (spill path) or too long: unsorted
-    int32_t* L = lists + bin * (int64_t)cap;
-    float* Kb = keys + bin * (int64_t)cap;
+    if (c <= MINN || c > MAXN) continue;
+    const int64_t o = off[bin];
+    if (!bin_fits(o, c, pool, cap)) continue;  // spill path: unsorted, never read as a list
+    int32_t* L = lists + o;
+    float* Kb = keys + o;
     int P = 1;
     while (P < c) P <<= 1;
     for (int i = threadIdx.x; i < P; i += kSortThreads) {
@@ -637,12 +682,17 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     // candidate faces: the bin list, or the whole mesh (naive mode / overflowed bin)
     const int64_t f0 = A.first[b], nf = A.num[b];
     const int32_t* list = nullptr;
+    const float* keys = nullptr;
     int64_t nsrc = nf;
     if (A.binned) {
-      const int c = A.bin_counts[(int64_t)b * nbins + bin];
-      if (c <= A.cap) {
-        list = A.bin_lists + ((int64_t)b * nbins + bin) * A.cap;
+      const int64_t gb = (int64_t)b * nbins + bin;
+      const int c = A.bin_counts[gb];
+      const int64_t o = A.bin_off[gb];
+      if (bin_fits(o, c, A.pool, A.cap)) {
+        list = A.bin_lists + o;
         nsrc = c;
+        // depth-ordered list (K1b) => once the next key exceeds every pixel's K-th depth, no later face can enter
+        if (A.zsort && c <= kSortMaxBig) keys = A.bin_keys + o;
       }
     }
     for (int s = 0; s < K; ++s) {
@@ -654,9 +704,6 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     else if (lane < 12) ws.pxy[lane] = pixel_y(A.H, mi0 + (lane - 8));   // micro-tile instead of per pair
     __syncwarp();
 
-    // depth-ordered list (K1b) => once the next key exceeds every pixel's K-th depth, no later face can enter
-    const float* keys = nullptr;
-    if (A.zsort && list && nsrc <= kSortMax) keys = A.bin_keys + ((int64_t)b * nbins + bin) * A.cap;
     const bool valid_px = (lane >> 3) < vh && (lane & 7) < vw;
     double T = pos_inf();  // max over the micro-tile's pixels of the K-th candidate depth (+inf: a list not full)
     int head = 0, pending = 0;
@@ -769,18 +816,40 @@ void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int 
 }
 
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
-                      int bs, int nbx, int nby, int cap, int* counts, int32_t* lists, cudaStream_t st) {
+                      int bs, int nbx, int nby, int* counts, cudaStream_t st) {
   if (max_faces <= 0) return;
   unsigned gx = (unsigned)std::min<int64_t>((max_faces + 255) / 256, 65535);
-  dim3 grid(gx, (unsigned)N);
-  k_bin_faces<<<grid, 256, 0, st>>>(ibbox, first, num, bs, nbx, nby, cap, counts, lists);
+  k_bin_faces<false><<<dim3(gx, (unsigned)N), 256, 0, st>>>(ibbox, first, num, bs, nbx, nby, counts, nullptr, nullptr,
+                                                           0, nullptr);
 }
 
-void launch_sort_bins(const int* counts, int32_t* lists, float* keys, const float* zkey, int64_t nbins_total, int cap,
-                      cudaStream_t st) {
+void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cudaStream_t st) {
   if (nbins_total <= 0) return;
+  k_scan_bins<<<1, kScanThreads, 0, st>>>(counts, nbins_total, off);
+}
+
+void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
+                      int bs, int nbx, int nby, const int* counts, const int64_t* off, int* cursor, int64_t pool,
+                      int32_t* lists, cudaStream_t st) {
+  if (max_faces <= 0) return;
+  unsigned gx = (unsigned)std::min<int64_t>((max_faces + 255) / 256, 65535);
+  k_bin_faces<true><<<dim3(gx, (unsigned)N), 256, 0, st>>>(ibbox, first, num, bs, nbx, nby,
+                                                          const_cast<int*>(counts), off, cursor, pool, lists);
+}
+
+cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int32_t* lists, float* keys, const float* zkey,
+                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st) {
+  if (nbins_total <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nbins_total, 148 * 16);
-  k_sort_bins<<<grid, kSortThreads, 0, st>>>(counts, lists, keys, zkey, nbins_total, cap);
+  k_sort_bins<kSortMax, 0, false><<<grid, kSortThreads, 0, st>>>(counts, off, lists, keys, zkey, nbins_total, pool,
+                                                                  cap);
+  auto big = k_sort_bins<kSortMaxBig, kSortMax, true>;
+  const int smem = kSortMaxBig * (int)sizeof(unsigned long long);
+  cudaError_t e = cudaFuncSetAttribute(big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  big<<<(unsigned)std::min<int64_t>(nbins_total, 148), kSortThreads, smem, st>>>(counts, off, lists, keys, zkey,
+                                                                                  nbins_total, pool, cap);
+  return cudaGetLastError();
 }
 
 template <typename OutT>

@@ -14,13 +14,15 @@ struct FineArgs {
   const int4* ibbox;        // [F] (i0, i1, j0, j1) exact pixel ranges; empty if i0 > i1
   const int64_t* first;     // [N] mesh_to_face_first_idx
   const int64_t* num;       // [N] num_faces_per_mesh
-  const int* bin_counts;    // [N, nby, nbx] entries per bin (may exceed cap: overflow => spill path)
-  const int32_t* bin_lists; // [N, nby, nbx, cap] packed face ids
+  const int* bin_counts;    // [N, nby, nbx] entries per bin
+  const int64_t* bin_off;   // [N, nby, nbx] start of each bin's list in the pool (exclusive scan of counts)
+  const int32_t* bin_lists; // [pool] packed face ids, bin after bin
   const float* zkey;        // [F] lower bound on any z the face can produce at any pixel (zsort only)
-  const float* bin_keys;    // [N, nby, nbx, cap] zkey of each bin entry, entries sorted ascending (zsort only)
+  const float* bin_keys;    // [pool] zkey of each bin entry, each bin's entries sorted ascending (zsort only)
+  int64_t pool;             // list pool capacity (entries); a bin that does not fit takes the spill path
   int zsort;                // 1 => depth-ordered bins + K-th-depth culling (needs clip_barycentric_coords)
   int binned;               // 0 => naive: every CTA scans its whole mesh
-  int cap;                  // max_faces_per_bin
+  int cap;                  // max_faces_per_bin: 0 = unlimited; longer bins take the spill path
   int bs, nbx, nby;         // bin (tile) side in pixels, bins per row / column
   int H, W, K;
   double blur, znear;
@@ -77,11 +79,20 @@ cudaError_t launch_item_to_element(const int64_t* first, const int64_t* num, int
 
 void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int W, double inflate, double znear,
                        int clip_z, int cull, int4* ibbox, float* zkey, cudaStream_t st);
-constexpr int kSortMax = 4096;  // bins longer than this stay unsorted (culling still applies, early exit does not)
-void launch_sort_bins(const int* counts, int32_t* lists, float* keys, const float* zkey, int64_t nbins_total, int cap,
-                      cudaStream_t st);
+constexpr int kSortMax = 4096;      // bins up to this length are sorted by k_sort_bins (32 KB shared memory)
+constexpr int kSortMaxBig = 16384;  // ... up to this one by its 128 KB variant; longer bins stay unsorted
+// bin usable as a list: fits the pool and the caller's max_faces_per_bin (0 = unlimited)
+__host__ __device__ __forceinline__ bool bin_fits(int64_t off, int cnt, int64_t pool, int cap) {
+  return off + cnt <= pool && (cap <= 0 || cnt <= cap);
+}
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
-                      int bs, int nbx, int nby, int cap, int* counts, int32_t* lists, cudaStream_t st);
+                      int bs, int nbx, int nby, int* counts, cudaStream_t st);  // count pass
+void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cudaStream_t st);
+void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
+                      int bs, int nbx, int nby, const int* counts, const int64_t* off, int* cursor, int64_t pool,
+                      int32_t* lists, cudaStream_t st);
+cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int32_t* lists, float* keys, const float* zkey,
+                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st);

@@ -74,7 +74,7 @@ class RasterSettings:
     faces_per_pixel: int = 1
     blur_radius: float = 1e-4
     bin_size: int = 16            # 0 => naive semantics (rasterize_meshes_naive); reference `tile_size`
-    max_faces_per_bin: int = 0    # 0 => automatic; overflow never changes results
+    max_faces_per_bin: int = 0    # 0 => unlimited (exact-size lists); overflow never changes results
     perspective_correct: bool = False
     clip_barycentric_coords: bool = True
     cull_backfaces: bool = False
