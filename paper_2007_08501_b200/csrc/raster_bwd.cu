@@ -35,25 +35,53 @@ __device__ __forceinline__ void clamp_bary_backward(const double wr[3], const do
   }
 }
 
-// per-slot cotangents -> g[9] = (dx, dy, dz) for vertices a, b, c
+// one occupied slot's per-slot inputs (bary + cotangents), loaded one batch ahead of their use
+#ifndef DR_BWD_PREFETCH_FV
+#define DR_BWD_PREFETCH_FV 1
+#endif
 template <typename InT>
-__device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slot, int32_t fid, double g[9]) {
+struct SlotIn {
+  InT w[3], dz, db[3], dd;
+#if DR_BWD_PREFETCH_FV
+  double v[9];  // the face's face_verts
+#endif
+};
+template <typename InT>
+__device__ __forceinline__ void load_slot(const BwdArgs<InT>& A, int64_t slot, int32_t fid, SlotIn<InT>& in) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    in.w[k] = __ldcs(A.bary + 3 * slot + k);  // every input is read exactly once: evict-first
+    in.db[k] = __ldcs(A.d_bary + 3 * slot + k);
+  }
+  in.dz = __ldcs(A.d_zbuf + slot);
+  in.dd = __ldcs(A.d_dists + slot);
+#if DR_BWD_PREFETCH_FV
+  const double* q = A.fv + 9 * (int64_t)fid;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) in.v[k] = __ldg(q + k);
+#endif
+}
+
+// per-slot cotangents -> g[9] = (dx, dy, dz) for vertices a, b, c; (i, j) = the slot's pixel
+template <typename InT>
+__device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int i, int j, int32_t fid, const SlotIn<InT>& in,
+                                              double g[9]) {
+#if DR_BWD_PREFETCH_FV
+  const FaceGeom fg = make_face_geom(in.v);
+#else
   const double* q = A.fv + 9 * (int64_t)fid;
   double v[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) v[k] = __ldg(q + k);
   const FaceGeom fg = make_face_geom(v);
+#endif
   const double z[3] = {fg.z0, fg.z1, fg.z2};
-  const int64_t pix = slot / A.K;
-  const int64_t rem = pix % ((int64_t)A.H * A.W);
-  const int i = (int)(rem / A.W), j = (int)(rem % A.W);
   const V2 p{pixel_x(A.W, j), pixel_y(A.H, i)};  // MR:357
 
-  const double w_hat[3] = {(double)A.bary[3 * slot], (double)A.bary[3 * slot + 1], (double)A.bary[3 * slot + 2]};
-  const double dz = (double)A.d_zbuf[slot];
+  const double w_hat[3] = {(double)in.w[0], (double)in.w[1], (double)in.w[2]};
+  const double dz = (double)in.dz;
   // MR:363-365: cotangent on the clamped bary = direct input + z-interpolation path
-  const double d_hat[3] = {(double)A.d_bary[3 * slot] + dz * z[0], (double)A.d_bary[3 * slot + 1] + dz * z[1],
-                           (double)A.d_bary[3 * slot + 2] + dz * z[2]};
+  const double d_hat[3] = {(double)in.db[0] + dz * z[0], (double)in.db[1] + dz * z[1], (double)in.db[2] + dz * z[2]};
   const V2 pa = p - fg.a, pb = p - fg.b, pc = p - fg.c;
   double w_raw[3];
   barycentric<false>(fg, pa, pb, pc, w_raw);  // MR:366
@@ -105,7 +133,7 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int64_t slo
   dxy[2] = ((gn0_c * d_w[0] + gn1_c * d_w[1]) - grad_d_c * wd) * inv;
 
   // MR:46-69 point_triangle_dist2_backward: nearest edge (first strict min), t and sign frozen
-  const double d_out = (double)A.d_dists[slot];
+  const double d_out = (double)in.dd;
   double t0, t1, t2;
   const double e0 = seg_dist2<false>(p, a, pa, fg.ab, fg.len_ab, t0);
   const double e1 = seg_dist2<false>(p, b, pb, fg.bc, fg.len_bc, t1);
@@ -164,62 +192,97 @@ constexpr int kBwdChunk = 32 * 16;
 #define DR_BWD_THREADS 128
 #endif
 #ifndef DR_BWD_MINBLOCKS
-#define DR_BWD_MINBLOCKS 6
+#define DR_BWD_MINBLOCKS 4
 #endif
-// 128-thread CTAs capped at 80 registers (6 CTAs = 24 warps per SM): the per-slot fp64 chain is latency-bound
-// and more resident warps beat the small (L1-resident) spill this cap causes — measured 6.8 ms (126 regs,
-// 16 warps) -> 5.7 ms on C4 (profiles/r01/README.md).
+// 128-thread CTAs, 4 per SM (128 registers, no spills): with the chunk-wide pix_to_face loads and the
+// one-batch-ahead input loads, latency is hidden by ILP rather than by more resident warps (C4: 80 registers x
+// 24 warps 3.47 ms, 96 x 20 3.33 ms, 128 x 16 3.10 ms; profiles/r01/README.md).
 constexpr int kBwdThreads = DR_BWD_THREADS;
 
 template <typename InT>
+__device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, int i, int j, int32_t my_fid,
+                                               const SlotIn<InT>& in, int lane) {
+  double g[9];
+  if (my_fid >= 0) {
+    slot_backward(A, i, j, my_fid, in, g);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) g[k] = 0.0;
+  }
+  if (reduce_by_face(my_fid, lane, g)) {
+    double* out = A.grad + 9 * (int64_t)my_fid;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) atomicAdd(out + k, g[k]);
+  }
+}
+
+// Phase A: the warp loads its whole 512-slot chunk of pix_to_face at once (16 independent coalesced loads per
+// lane in flight, instead of one exposed load latency per 32 slots) and compacts the occupied slots into a
+// warp-private queue in shared memory. Phase B: the queue is processed 32 slots per step, the next step's
+// bary / cotangents loaded before the current step computes.
+template <typename InT>
 __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdArgs<InT> A) {
-  __shared__ int64_t q_slot[kBwdThreads / 32][64];
-  __shared__ int32_t q_fid[kBwdThreads / 32][64];
+  __shared__ int32_t q_off[kBwdThreads / 32][kBwdChunk];
+  __shared__ int32_t q_fid[kBwdThreads / 32][kBwdChunk];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int64_t* qs = q_slot[wid];
+  int32_t* qo = q_off[wid];
   int32_t* qf = q_fid[wid];
+  constexpr int kSteps = kBwdChunk / 32;
+  const int HW = A.H * A.W;
   for (int64_t c0 = warp * kBwdChunk; c0 < A.S; c0 += nwarps * kBwdChunk) {
-    const int64_t c1 = c0 + kBwdChunk < A.S ? c0 + kBwdChunk : A.S;
-    int pending = 0;
-    for (int64_t s0 = c0; s0 < c1; s0 += 32) {
-      const int64_t slot = s0 + lane;
-      int32_t fid = -1;
-      if (slot < c1) {
-        const int64_t f = A.p2f[slot];
-        if (f >= 0 && f < A.F) fid = (int32_t)f;
-      }
-      const unsigned occ = __ballot_sync(0xffffffffu, fid >= 0);
-      if (fid >= 0) {
-        const int pos = pending + __popc(occ & ((1u << lane) - 1u));
-        qs[pos] = slot;
-        qf[pos] = fid;
-      }
-      pending += __popc(occ);
-      __syncwarp();
-      const bool last = s0 + 32 >= c1;
-      while (pending >= 32 || (last && pending > 0)) {
-        const int nb = pending < 32 ? pending : 32;
-        pending -= nb;
-        const bool act = lane < nb;
-        const int64_t my_slot = act ? qs[pending + lane] : 0;
-        const int32_t my_fid = act ? qf[pending + lane] : -1;
-        __syncwarp();
-        double g[9];
-        if (act) {
-          slot_backward(A, my_slot, my_fid, g);
-        } else {
+    int64_t f[kSteps];
 #pragma unroll
-          for (int k = 0; k < 9; ++k) g[k] = 0.0;
-        }
-        if (reduce_by_face(my_fid, lane, g)) {
-          double* out = A.grad + 9 * (int64_t)my_fid;
-#pragma unroll
-          for (int k = 0; k < 9; ++k) atomicAdd(out + k, g[k]);
-        }
-      }
+    for (int t = 0; t < kSteps; ++t) {
+      const int64_t slot = c0 + t * 32 + lane;
+      f[t] = slot < A.S ? __ldcs(A.p2f + slot) : -1;  // streamed once: evict-first
     }
+    int n = 0;
+#pragma unroll
+    for (int t = 0; t < kSteps; ++t) {
+      const bool occ = f[t] >= 0 && f[t] < A.F;
+      const unsigned m = __ballot_sync(0xffffffffu, occ);
+      if (occ) {
+        const int pos = n + __popc(m & ((1u << lane) - 1u));
+        qo[pos] = t * 32 + lane;
+        qf[pos] = (int32_t)f[t];
+      }
+      n += __popc(m);
+    }
+    __syncwarp();
+    // slot -> pixel with one 64-bit division per chunk; 32-bit arithmetic per slot
+    const int64_t pix0 = c0 / A.K;
+    const int r0 = (int)(c0 - pix0 * A.K);
+    const int pp0 = (int)(pix0 % HW);
+    SlotIn<InT> nxt;
+    int32_t nfid = -1;
+    int noff = 0;
+    if (lane < n) {
+      noff = qo[lane];
+      nfid = qf[lane];
+      load_slot(A, c0 + noff, nfid, nxt);
+    }
+    for (int q0 = 0; q0 < n; q0 += 32) {
+      const SlotIn<InT> cur = nxt;
+      const int32_t my_fid = nfid;
+      const int off = noff;
+      nfid = -1;
+      if (q0 + 32 + lane < n) {
+        noff = qo[q0 + 32 + lane];
+        nfid = qf[q0 + 32 + lane];
+        load_slot(A, c0 + noff, nfid, nxt);
+      }
+      int i = 0, j = 0;
+      if (my_fid >= 0) {
+        int pp = pp0 + (r0 + off) / A.K;
+        if (pp >= HW) pp %= HW;  // the chunk crossed into the next image
+        i = pp / A.W;
+        j = pp - i * A.W;
+      }
+      backward_batch(A, i, j, my_fid, cur, lane);
+    }
+    __syncwarp();
   }
 }
 
