@@ -87,7 +87,7 @@ struct Plan {
   bool zsort = false;  // depth-ordered bins + K-th-depth culling (clip_barycentric_coords only)
   int64_t nbins_total = 0, pool = 0;  // N * bins; list-pool capacity (entries)
   size_t off_ibbox = 0, off_zkey = 0, off_counter = 0, off_counts = 0, off_cursor = 0, off_binoff = 0, off_lists = 0,
-         off_keys = 0, total = 0;
+         total = 0;
 };
 
 // DR_ZSORT=0 disables the depth-ordered fine stage (A/B measurements; results are identical either way)
@@ -143,12 +143,8 @@ int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
     off = align_up(off + sizeof(int) * (size_t)p.nbins_total);
     p.off_binoff = off;
     off = align_up(off + sizeof(int64_t) * (size_t)p.nbins_total);
-    p.off_lists = off;
-    off = align_up(off + sizeof(int32_t) * (size_t)p.pool);
-    if (p.zsort) {
-      p.off_keys = off;
-      off = align_up(off + sizeof(float) * (size_t)p.pool);
-    }
+    p.off_lists = off;  // 16-byte entries: face id, zkey, packed pixel range
+    off = align_up(off + sizeof(int4) * (size_t)p.pool);
   }
   p.total = off;
   return DR_OK;
@@ -229,11 +225,10 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   char* base = static_cast<char*>(ws);
   int4* ibbox = reinterpret_cast<int4*>(base + p.off_ibbox);
   int* counts = reinterpret_cast<int*>(base + p.off_counts);
-  int32_t* lists = reinterpret_cast<int32_t*>(base + p.off_lists);
+  int4* entries = reinterpret_cast<int4*>(base + p.off_lists);
   int* cursor = reinterpret_cast<int*>(base + p.off_cursor);
   int64_t* bin_off = reinterpret_cast<int64_t*>(base + p.off_binoff);
   float* zkey = reinterpret_cast<float*>(base + p.off_zkey);
-  float* bin_keys = p.zsort && p.binned ? reinterpret_cast<float*>(base + p.off_keys) : nullptr;
   const double inflate = std::sqrt(std::max(0.0, s->blur_radius));  // MR:103
 
   {
@@ -253,11 +248,11 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
       drb::launch_bin_faces(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, counts, st);
       drb::launch_scan_bins(counts, p.nbins_total, bin_off, st);
       drb::launch_fill_bins(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool,
-                            lists, st);
+                            p.zsort ? zkey : nullptr, entries, st);
     }
     if (p.zsort) {
       ProfScope ps(st, KN_SORT);
-      cudaError_t e = drb::launch_sort_bins(counts, bin_off, lists, bin_keys, zkey, p.nbins_total, p.pool, p.cap, st);
+      cudaError_t e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, p.cap, st);
       if (e != cudaSuccess) return cuda_fail(e, "sorting bins");
     }
   }
@@ -267,11 +262,10 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   A.first = first;
   A.num = num;
   A.bin_counts = counts;
-  A.bin_lists = lists;
+  A.bin_entries = entries;
   A.bin_off = bin_off;
   A.pool = p.pool;
   A.zkey = zkey;
-  A.bin_keys = bin_keys;
   A.zsort = p.zsort ? 1 : 0;
   A.binned = p.binned ? 1 : 0;
   A.cap = p.cap;

@@ -132,12 +132,22 @@ __global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ f
 // are known); a bin that does not fit the pool, or exceeds the caller's max_faces_per_bin, takes the spill
 // path in K2 (its micro-tiles scan the whole mesh), so results never depend on either capacity.
 
+// A bin entry carries everything K2 needs to decide whether a face touches a micro-tile (one coalesced 16-byte
+// load per entry instead of a dependent ibbox gather): {face id, zkey bits, i0 | i1 << 16, j0 | j1 << 16}.
+// Pixel indices fit 16 bits (image side <= 32768, checked by make_plan).
+__device__ __forceinline__ int4 make_bin_entry(int32_t fid, float key, int4 ib) {
+  return make_int4(fid, __float_as_int(key), (ib.x & 0xffff) | (ib.y << 16), (ib.z & 0xffff) | (ib.w << 16));
+}
+__device__ __forceinline__ int4 entry_ibbox(int4 e) {
+  return make_int4(e.z & 0xffff, (int)((unsigned)e.z >> 16), e.w & 0xffff, (int)((unsigned)e.w >> 16));
+}
+
 template <bool kFill>
 __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbox, const int64_t* __restrict__ first,
                                                    const int64_t* __restrict__ num, int bs, int nbx, int nby,
                                                    int* __restrict__ counts, const int64_t* __restrict__ off,
                                                    int* __restrict__ cursor, int64_t pool,
-                                                   int32_t* __restrict__ lists) {
+                                                   const float* __restrict__ zkey, int4* __restrict__ entries) {
   const int b = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int64_t nf = num[b], f0 = first[b];
@@ -170,7 +180,7 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
           if (o + counts[bin0 + key] <= pool) pos = o + atomicAdd(cursor + bin0 + key, __popc(peers));
         }
         pos = __shfl_sync(0xffffffffu, pos, leader);
-        if (active && pos >= 0) lists[pos + rank] = (int32_t)(f0 + lf);
+        if (active && pos >= 0) entries[pos + rank] = make_bin_entry((int32_t)(f0 + lf), zkey ? zkey[f0 + lf] : 0.f, ib);
       }
     }
   }
@@ -221,8 +231,8 @@ constexpr int kSortThreads = 256;
 template <int MAXN, int MINN, bool kDyn>
 __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restrict__ counts,
                                                             const int64_t* __restrict__ off,
-                                                            int32_t* __restrict__ lists, float* __restrict__ keys,
-                                                            const float* __restrict__ zkey, int64_t nbins_total,
+                                                            int4* __restrict__ entries,
+                                                            const int4* __restrict__ ibbox, int64_t nbins_total,
                                                             int64_t pool, int cap) {
   __shared__ unsigned long long s_static[kDyn ? 1 : MAXN];
   extern __shared__ unsigned long long s_dyn[];
@@ -232,15 +242,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
     if (c <= MINN || c > MAXN) continue;
     const int64_t o = off[bin];
     if (!bin_fits(o, c, pool, cap)) continue;  // spill path: unsorted, never read as a list
-    int32_t* L = lists + o;
-    float* Kb = keys + o;
+    int4* L = entries + o;
     int P = 1;
     while (P < c) P <<= 1;
     for (int i = threadIdx.x; i < P; i += kSortThreads) {
       unsigned long long e = ~0ull;
       if (i < c) {
-        const int32_t f = L[i];
-        e = ((unsigned long long)float_order_bits(__ldg(zkey + f)) << 32) | (uint32_t)f;
+        const int2 fk = *reinterpret_cast<const int2*>(L + i);  // {face id, zkey bits}
+        e = ((unsigned long long)float_order_bits(__int_as_float(fk.y)) << 32) | (uint32_t)fk.x;
       }
       s[i] = e;
     }
@@ -262,8 +271,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
     }
     for (int i = threadIdx.x; i < c; i += kSortThreads) {
       const unsigned long long e = s[i];
-      L[i] = (int32_t)(uint32_t)e;
-      Kb[i] = float_from_order_bits((uint32_t)(e >> 32));
+      const int32_t f = (int32_t)(uint32_t)e;
+      L[i] = make_bin_entry(f, float_from_order_bits((uint32_t)(e >> 32)), __ldg(ibbox + f));
     }
     __syncthreads();
   }
@@ -681,18 +690,18 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 
     // candidate faces: the bin list, or the whole mesh (naive mode / overflowed bin)
     const int64_t f0 = A.first[b], nf = A.num[b];
-    const int32_t* list = nullptr;
-    const float* keys = nullptr;
+    const int4* list = nullptr;
+    bool sorted = false;
     int64_t nsrc = nf;
     if (A.binned) {
       const int64_t gb = (int64_t)b * nbins + bin;
       const int c = A.bin_counts[gb];
       const int64_t o = A.bin_off[gb];
       if (bin_fits(o, c, A.pool, A.cap)) {
-        list = A.bin_lists + o;
+        list = A.bin_entries + o;
         nsrc = c;
         // depth-ordered list (K1b) => once the next key exceeds every pixel's K-th depth, no later face can enter
-        if (A.zsort && c <= kSortMaxBig) keys = A.bin_keys + o;
+        sorted = A.zsort && c <= kSortMaxBig;
       }
     }
     for (int s = 0; s < K; ++s) {
@@ -712,15 +721,24 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       uint32_t r = 0u;
       int32_t fid = -1;
       float key = 0.f;
-      if (keys && (double)keys[c0] > T) {
+      if (sorted && (double)__int_as_float(list[c0].y) > T) {
         STAT_ADD(6, 1);
         break;
       }
       STAT_ADD(0, __popc(__ballot_sync(0xffffffffu, ci < nsrc)));
       if (ci < nsrc) {
-        fid = list ? list[ci] : (int32_t)(f0 + ci);
-        if (A.zsort) key = keys ? keys[ci] : A.zkey[fid];
-        if (!A.zsort || !((double)key > T)) r = cover_rect(A.ibbox[fid], mi0, mj0, vh, vw);
+        int4 ib;
+        if (list) {
+          const int4 e = list[ci];
+          fid = e.x;
+          key = __int_as_float(e.y);
+          ib = entry_ibbox(e);
+        } else {
+          fid = (int32_t)(f0 + ci);
+          key = A.zsort ? A.zkey[fid] : 0.f;
+          ib = A.ibbox[fid];
+        }
+        if (!A.zsort || !((double)key > T)) r = cover_rect(ib, mi0, mj0, vh, vw);
       }
       unsigned todo = __ballot_sync(0xffffffffu, r != 0u);
       const bool last = c0 + 32 >= nsrc;
@@ -820,7 +838,7 @@ void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* nu
   if (max_faces <= 0) return;
   unsigned gx = (unsigned)std::min<int64_t>((max_faces + 255) / 256, 65535);
   k_bin_faces<false><<<dim3(gx, (unsigned)N), 256, 0, st>>>(ibbox, first, num, bs, nbx, nby, counts, nullptr, nullptr,
-                                                           0, nullptr);
+                                                           0, nullptr, nullptr);
 }
 
 void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cudaStream_t st) {
@@ -830,24 +848,24 @@ void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cuda
 
 void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
                       int bs, int nbx, int nby, const int* counts, const int64_t* off, int* cursor, int64_t pool,
-                      int32_t* lists, cudaStream_t st) {
+                      const float* zkey, int4* entries, cudaStream_t st) {
   if (max_faces <= 0) return;
   unsigned gx = (unsigned)std::min<int64_t>((max_faces + 255) / 256, 65535);
   k_bin_faces<true><<<dim3(gx, (unsigned)N), 256, 0, st>>>(ibbox, first, num, bs, nbx, nby,
-                                                          const_cast<int*>(counts), off, cursor, pool, lists);
+                                                          const_cast<int*>(counts), off, cursor, pool, zkey, entries);
 }
 
-cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int32_t* lists, float* keys, const float* zkey,
+cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entries, const int4* ibbox,
                              int64_t nbins_total, int64_t pool, int cap, cudaStream_t st) {
   if (nbins_total <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nbins_total, 148 * 16);
-  k_sort_bins<kSortMax, 0, false><<<grid, kSortThreads, 0, st>>>(counts, off, lists, keys, zkey, nbins_total, pool,
+  k_sort_bins<kSortMax, 0, false><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total, pool,
                                                                   cap);
   auto big = k_sort_bins<kSortMaxBig, kSortMax, true>;
   const int smem = kSortMaxBig * (int)sizeof(unsigned long long);
   cudaError_t e = cudaFuncSetAttribute(big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  big<<<(unsigned)std::min<int64_t>(nbins_total, 148), kSortThreads, smem, st>>>(counts, off, lists, keys, zkey,
+  big<<<(unsigned)std::min<int64_t>(nbins_total, 148), kSortThreads, smem, st>>>(counts, off, entries, ibbox,
                                                                                   nbins_total, pool, cap);
   return cudaGetLastError();
 }

@@ -16,11 +16,10 @@ struct FineArgs {
   const int64_t* num;       // [N] num_faces_per_mesh
   const int* bin_counts;    // [N, nby, nbx] entries per bin
   const int64_t* bin_off;   // [N, nby, nbx] start of each bin's list in the pool (exclusive scan of counts)
-  const int32_t* bin_lists; // [pool] packed face ids, bin after bin
+  const int4* bin_entries;  // [pool] bin after bin: {face id, zkey bits, i0 | i1 << 16, j0 | j1 << 16}
   const float* zkey;        // [F] lower bound on any z the face can produce at any pixel (zsort only)
-  const float* bin_keys;    // [pool] zkey of each bin entry, each bin's entries sorted ascending (zsort only)
   int64_t pool;             // list pool capacity (entries); a bin that does not fit takes the spill path
-  int zsort;                // 1 => depth-ordered bins + K-th-depth culling (needs clip_barycentric_coords)
+  int zsort;                // 1 => depth-ordered bins (ascending zkey) + K-th-depth culling (clip_barycentric_coords)
   int binned;               // 0 => naive: every CTA scans its whole mesh
   int cap;                  // max_faces_per_bin: 0 = unlimited; longer bins take the spill path
   int bs, nbx, nby;         // bin (tile) side in pixels, bins per row / column
@@ -90,8 +89,8 @@ void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* nu
 void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cudaStream_t st);
 void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
                       int bs, int nbx, int nby, const int* counts, const int64_t* off, int* cursor, int64_t pool,
-                      int32_t* lists, cudaStream_t st);
-cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int32_t* lists, float* keys, const float* zkey,
+                      const float* zkey, int4* entries, cudaStream_t st);
+cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entries, const int4* ibbox,
                              int64_t nbins_total, int64_t pool, int cap, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st);
