@@ -168,6 +168,24 @@ int dr_padded_to_packed(const void* padded, const int64_t* first, const int64_t*
 int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
                               dr_stream_t stream);
 
+/* ---- fused fragment consumer: silhouette ----
+ * dr_rasterize_silhouette_fwd = silhouette_blend(rasterize_meshes(...), sigma)
+ *   (shading.cpp:75-91 over mesh_raster.cpp:234): alpha [N,H,W] fp32 = 1 - prod_k (1 - sigmoid(-dist_k / sigma))
+ *   over the occupied slots of each pixel; pix_to_face [N,H,W,K] (may be NULL) is bit-exact with
+ *   dr_rasterize_meshes_fwd. zbuf / bary / dists are never written to memory. Same workspace as the forward.
+ * dr_rasterize_silhouette_bwd = rasterize_backward(..., d_zbuf = 0, d_bary = 0,
+ *   silhouette_blend_backward(frag, sigma, d_alpha)) (shading.cpp:93-121, mesh_raster.cpp:329-403): the
+ *   reference fit loop's step (pipeline.cpp:153-162); grad_face_verts [F,3,3] is overwritten on the batch's
+ *   face ranges. sigma must be > 0 (DR_ERR_RANGE). */
+int dr_rasterize_silhouette_fwd(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                                const int64_t* num_faces_per_mesh, int64_t N, int64_t F, const dr_raster_settings* s,
+                                double sigma, int64_t* pix_to_face, float* alpha, void* workspace,
+                                size_t workspace_bytes, dr_stream_t stream);
+int dr_rasterize_silhouette_bwd(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                                const int64_t* num_faces_per_mesh, int64_t N, int64_t F, const dr_raster_settings* s,
+                                double sigma, const int64_t* pix_to_face, const float* grad_alpha,
+                                double* grad_face_verts, dr_stream_t stream);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* dr_last_error(void);
 

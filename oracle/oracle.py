@@ -65,6 +65,28 @@ class Oracle:
         L.orc_clamp_barycentric.argtypes = [_dp, _dp]
         L.orc_point_triangle_dist2_backward.argtypes = [_dp, _dp, _dp, _dp, C.c_double, _dp]
         L.orc_pixel_center_ndc.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        L.orc_silhouette_blend.argtypes = [_i64p, _dp, C.c_int64, C.c_int, C.c_double, _dp]
+        L.orc_silhouette_blend_backward.argtypes = [_i64p, _dp, C.c_int64, C.c_int, C.c_double, _dp, _dp]
+
+    def silhouette_blend(self, p2f, dists, sigma):
+        """shading.cpp:75-91 over fragments [N,H,W,K] -> alpha [N,H,W]."""
+        p2f = np.ascontiguousarray(p2f, np.int64)
+        di = np.ascontiguousarray(dists, np.float64)
+        k = p2f.shape[-1]
+        out = np.empty(p2f.shape[:-1], np.float64)
+        self.lib.orc_silhouette_blend(_p(p2f, _i64p), _p(di, _dp), p2f.size // k, k, sigma, _p(out, _dp))
+        return out
+
+    def silhouette_blend_backward(self, p2f, dists, sigma, d_alpha):
+        """shading.cpp:93-121 -> d_dists [N,H,W,K]."""
+        p2f = np.ascontiguousarray(p2f, np.int64)
+        di = np.ascontiguousarray(dists, np.float64)
+        da = np.ascontiguousarray(d_alpha, np.float64)
+        k = p2f.shape[-1]
+        out = np.empty(p2f.shape, np.float64)
+        self.lib.orc_silhouette_blend_backward(_p(p2f, _i64p), _p(di, _dp), p2f.size // k, k, sigma, _p(da, _dp),
+                                               _p(out, _dp))
+        return out
 
     def forward(self, face_verts, first, num, s: OrcSettings):
         fv = np.ascontiguousarray(face_verts, dtype=np.float64)
@@ -170,6 +192,9 @@ class RefLib:
         L.ref_rasterize.argtypes = [C.c_void_p, _dp, _i32p, C.c_double, C.c_int, _i64p, _dp, _dp, _dp]
         L.ref_rasterize_backward.argtypes = [C.c_void_p, _dp, _i32p, C.c_double, C.c_int32, _i64p, _dp, _dp,
                                              _dp, _dp, _dp, _dp, _dp]
+        L.ref_silhouette_blend.argtypes = [_i64p, _dp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _dp]
+        L.ref_silhouette_blend_backward.argtypes = [_i64p, _dp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                    C.c_double, _dp, _dp]
         L.ref_point_triangle_dist2.argtypes = [_dp] * 4
         L.ref_point_triangle_dist2.restype = C.c_double
         L.ref_barycentric.argtypes = [_dp] * 5
@@ -238,3 +263,25 @@ class RefLib:
     def point_triangle_dist2(self, p, a, b, c) -> float:
         arr = [np.asarray(x, np.float64) for x in (p, a, b, c)]
         return self.lib.ref_point_triangle_dist2(*[_p(x, _dp) for x in arr])
+
+    def silhouette_blend(self, p2f, dists, sigma):
+        """dr::silhouette_blend (shading.hpp:37) over fragments [N,H,W,K] -> alpha [N,H,W]."""
+        p2f = np.ascontiguousarray(p2f, np.int64)
+        di = np.ascontiguousarray(dists, np.float64)
+        n, h, w, k = p2f.shape
+        out = np.empty((n, h, w), np.float64)
+        if self.lib.ref_silhouette_blend(_p(p2f, _i64p), _p(di, _dp), n, h, w, k, sigma, _p(out, _dp)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return out
+
+    def silhouette_blend_backward(self, p2f, dists, sigma, d_alpha):
+        """dr::silhouette_blend_backward (shading.hpp:39-41) -> d_dists [N,H,W,K]."""
+        p2f = np.ascontiguousarray(p2f, np.int64)
+        di = np.ascontiguousarray(dists, np.float64)
+        da = np.ascontiguousarray(d_alpha, np.float64)
+        n, h, w, k = p2f.shape
+        out = np.empty((n, h, w, k), np.float64)
+        if self.lib.ref_silhouette_blend_backward(_p(p2f, _i64p), _p(di, _dp), n, h, w, k, sigma, _p(da, _dp),
+                                                  _p(out, _dp)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return out

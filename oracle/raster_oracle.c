@@ -482,3 +482,46 @@ int orc_rasterize_bwd(const double* face_verts, const int64_t* first, const int6
   }
   return 0;
 }
+
+/* ---- silhouette blend (/root/reference/proj/src/shading.cpp, "SH") on fragments ----
+ * orc_silhouette_blend:          SH:75-91  alpha[px] = 1 - prod over occupied slots (in slot order) of
+ *                                          (1 - sigmoid(-dists / sigma)), sigmoid(x) = 1 / (1 + exp(-x)) (SH:9)
+ * orc_silhouette_blend_backward: SH:93-121 d_dists[slot] = d_alpha * prod_{other occupied} (1 - p) *
+ *                                          (-p (1 - p) / sigma); pixels with d_alpha == 0 and empty slots get 0 */
+static inline double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+void orc_silhouette_blend(const int64_t* p2f, const double* dists, int64_t npix, int k, double sigma,
+                          double* alpha) {
+  for (int64_t px = 0; px < npix; ++px) {
+    double keep = 1.0;
+    for (int s = 0; s < k; ++s) {
+      int64_t slot = px * k + s;
+      if (p2f[slot] < 0) continue;
+      double prob = sigmoid(-dists[slot] / sigma);
+      keep *= 1.0 - prob;
+    }
+    alpha[px] = 1.0 - keep;
+  }
+}
+
+void orc_silhouette_blend_backward(const int64_t* p2f, const double* dists, int64_t npix, int k, double sigma,
+                                   const double* d_alpha, double* d_dists) {
+  for (int64_t i = 0; i < npix * k; ++i) d_dists[i] = 0.0;
+  for (int64_t px = 0; px < npix; ++px) {
+    double da = d_alpha[px];
+    if (da == 0) continue;
+    for (int s = 0; s < k; ++s) {
+      int64_t slot = px * k + s;
+      if (p2f[slot] < 0) continue;
+      double prob_s = sigmoid(-dists[slot] / sigma);
+      double rest = 1.0;
+      for (int s2 = 0; s2 < k; ++s2) {
+        if (s2 == s) continue;
+        int64_t slot2 = px * k + s2;
+        if (p2f[slot2] < 0) continue;
+        rest *= 1.0 - sigmoid(-dists[slot2] / sigma);
+      }
+      d_dists[slot] = da * rest * (-prob_s * (1.0 - prob_s) / sigma);
+    }
+  }
+}

@@ -8,6 +8,7 @@
 //   dr::rasterize_backward                          (mesh_raster.hpp:66-69)
 //   dr::world_to_ndc                                (camera.hpp:50)
 //   dr::ico_sphere / cube / synthetic_batch         (templates.hpp:12-24)
+//   dr::silhouette_blend / silhouette_blend_backward (shading.hpp:37-41)
 // Errors are caught and reported through ref_last_error() (the reference throws).
 #include <cstdint>
 #include <cstring>
@@ -19,6 +20,7 @@
 #include "dr/camera.hpp"
 #include "dr/core.hpp"
 #include "dr/mesh_raster.hpp"
+#include "dr/shading.hpp"
 #include "dr/templates.hpp"
 
 namespace {
@@ -167,6 +169,44 @@ int ref_rasterize(void* h, const double* cam, const int32_t* si, double blur, in
     std::memcpy(zbuf, f.zbuf.data(), f.zbuf.size() * sizeof(double));
     std::memcpy(bary, f.bary.data(), f.bary.size() * sizeof(double));
     std::memcpy(dists, f.dists.data(), f.dists.size() * sizeof(double));
+  });
+}
+
+// silhouette blend over fragments (dr::silhouette_blend / _backward, shading.hpp:37-41); only pix_to_face and
+// dists are read by the reference
+int ref_silhouette_blend(const int64_t* p2f, const double* dists, int32_t nbatch, int32_t h, int32_t w, int32_t k,
+                         double sigma, double* alpha) {
+  return guarded([&] {
+    dr::MeshFragments f;
+    f.batch = nbatch;
+    f.h = h;
+    f.w = w;
+    f.k = k;
+    size_t ns = size_t(f.slots());
+    f.pix_to_face.assign(p2f, p2f + ns);
+    f.dists.assign(dists, dists + ns);
+    f.zbuf.assign(ns, 0.0);
+    f.bary.assign(3 * ns, 0.0);
+    std::vector<double> a = dr::silhouette_blend(f, sigma);
+    std::memcpy(alpha, a.data(), a.size() * sizeof(double));
+  });
+}
+int ref_silhouette_blend_backward(const int64_t* p2f, const double* dists, int32_t nbatch, int32_t h, int32_t w,
+                                  int32_t k, double sigma, const double* d_alpha, double* d_dists) {
+  return guarded([&] {
+    dr::MeshFragments f;
+    f.batch = nbatch;
+    f.h = h;
+    f.w = w;
+    f.k = k;
+    size_t ns = size_t(f.slots());
+    f.pix_to_face.assign(p2f, p2f + ns);
+    f.dists.assign(dists, dists + ns);
+    f.zbuf.assign(ns, 0.0);
+    f.bary.assign(3 * ns, 0.0);
+    std::vector<double> da(d_alpha, d_alpha + ns / size_t(k));
+    std::vector<double> dd = dr::silhouette_blend_backward(f, sigma, da);
+    std::memcpy(d_dists, dd.data(), dd.size() * sizeof(double));
   });
 }
 

@@ -2,6 +2,7 @@
 
 Public surface (mirrors /root/reference/proj/include/dr/mesh_raster.hpp on the north-star boundary):
     RasterSettings, rasterize_meshes, rasterize_meshes_naive, rasterize_meshes_backward, RasterizeMeshes
+    rasterize_silhouette, rasterize_silhouette_backward, RasterizeSilhouette (fused silhouette_blend, shading.cpp)
 Input generators and the host camera transform live in ``scenes``; mesh sharding across GPUs in ``shard``.
 """
 from .raster import (  # noqa: F401
@@ -11,6 +12,7 @@ from .raster import (  # noqa: F401
     RangeError,
     RasterError,
     RasterizeMeshes,
+    RasterizeSilhouette,
     RasterSettings,
     ShapeError,
     UsageError,
@@ -20,6 +22,8 @@ from .raster import (  # noqa: F401
     rasterize_meshes,
     rasterize_meshes_backward,
     rasterize_meshes_naive,
+    rasterize_silhouette,
+    rasterize_silhouette_backward,
     face_verts_backward,
     workspace_bytes,
     world_to_face_verts,

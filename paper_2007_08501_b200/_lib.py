@@ -24,6 +24,8 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_meshes_bwd_f64",
     "dr_rasterize_meshes_fwd_hr",
     "dr_rasterize_meshes_bwd_hr",
+    "dr_rasterize_silhouette_fwd",
+    "dr_rasterize_silhouette_bwd",
     "dr_world_to_face_verts",
     "dr_face_verts_backward",
     "dr_packed_to_padded",
@@ -104,7 +106,12 @@ def load() -> C.CDLL:
     L.dr_profile_read.argtypes = [C.POINTER(C.c_int), C.POINTER(C.c_float), C.c_int]
     L.dr_profile_kernel_name.argtypes = [C.c_int]
     L.dr_profile_kernel_name.restype = C.c_char_p
-    for fn in ("dr_rasterize_meshes_fwd", "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
+    L.dr_rasterize_silhouette_fwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp,
+                                              C.c_size_t, _vp]
+    L.dr_rasterize_silhouette_bwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp,
+                                              _vp]
+    for fn in ("dr_rasterize_silhouette_fwd", "dr_rasterize_silhouette_bwd", "dr_rasterize_meshes_fwd",
+               "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
                "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_fwd_hr", "dr_rasterize_meshes_bwd_hr",
                "dr_rasterize_meshes_bin_stats"):
         getattr(L, fn).restype = C.c_int

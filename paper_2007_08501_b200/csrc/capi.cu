@@ -43,9 +43,12 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 // ---- optional per-kernel timing ring ----
-const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine",     "k_backward",
-                              "memset",       "k_camera",    "k_batching", "k_sort_bins"};
-enum { KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5, KN_BATCH = 6, KN_SORT = 7 };
+const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine",      "k_backward",          "memset",
+                              "k_camera",     "k_batching",  "k_sort_bins", "k_silhouette_backward"};
+enum {
+  KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5, KN_BATCH = 6, KN_SORT = 7,
+  KN_SIL_BWD = 8
+};
 struct ProfEntry {
   int kernel;
   cudaEvent_t a, b;
@@ -199,15 +202,18 @@ cudaError_t zero_face_ranges(double* grad, const std::vector<int64_t>& h, int64_
   return cudaSuccess;
 }
 
+// alpha != nullptr selects the fused silhouette emit (p2f optional, zbuf/bary/dists unused)
 template <typename OutT>
 int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
              const dr_raster_settings* s, int64_t* p2f, OutT* zbuf, OutT* bary, OutT* dists, void* ws, size_t ws_bytes,
-             cudaStream_t st, const int64_t* host_first = nullptr, const int64_t* host_num = nullptr) {
+             cudaStream_t st, const int64_t* host_first = nullptr, const int64_t* host_num = nullptr,
+             OutT* alpha = nullptr, double sigma = 0.0) {
   Plan p;
   int rc = make_plan(N, F, s, p);
   if (rc) return rc;
-  if (!first || !num || !p2f || !zbuf || !bary || !dists || (F > 0 && !fv))
-    return fail(DR_ERR_USAGE, "null input/output pointer");
+  if (!first || !num || (F > 0 && !fv)) return fail(DR_ERR_USAGE, "null input pointer");
+  if (alpha ? false : (!p2f || !zbuf || !bary || !dists)) return fail(DR_ERR_USAGE, "null output pointer");
+  if (alpha && !(sigma > 0.0)) return fail(DR_ERR_RANGE, "silhouette sigma must be > 0 (got %g)", sigma);
   if (!ws || ws_bytes < p.total)
     return fail(DR_ERR_OOM, "workspace too small: %zu bytes given, %zu needed", ws_bytes, p.total);
   int64_t max_faces = 0;
@@ -299,6 +305,8 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   A.zbuf = zbuf;
   A.bary = bary;
   A.dists = dists;
+  A.alpha = alpha;
+  A.sigma = sigma;
   cudaError_t e = cudaMemsetAsync(A.work_counter, 0, sizeof(unsigned long long), st);
   if (e == cudaSuccess) {
     ProfScope ps(st, KN_FINE);
@@ -353,9 +361,64 @@ int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   return DR_OK;
 }
 
+int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                 const dr_raster_settings* s, double sigma, const int64_t* p2f, const float* d_alpha, double* grad,
+                 cudaStream_t st) {
+  Plan p;
+  int rc = make_plan(N, F, s, p);
+  if (rc) return rc;
+  if (!first || !num || !p2f || !d_alpha || (F > 0 && (!fv || !grad)))
+    return fail(DR_ERR_USAGE, "null input/output pointer");
+  if (!(sigma > 0.0)) return fail(DR_ERR_RANGE, "silhouette sigma must be > 0 (got %g)", sigma);
+  int64_t mx;
+  std::vector<int64_t> ranges;
+  rc = read_ranges(first, num, N, F, st, &mx, &ranges);
+  if (rc) return rc;
+  if (F == 0) return DR_OK;
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_MEMSET);
+    e = zero_face_ranges(grad, ranges, N, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "zeroing grad_face_verts");
+  drb::SilBwdArgs A;
+  A.fv = fv;
+  A.p2f = p2f;
+  A.d_alpha = d_alpha;
+  A.grad = grad;
+  A.npix = N * (int64_t)p.H * p.W;
+  A.F = F;
+  A.H = p.H;
+  A.W = p.W;
+  A.K = p.K;
+  A.sigma = sigma;
+  {
+    ProfScope ps(st, KN_SIL_BWD);
+    e = drb::launch_silhouette_backward(A, st);
+  }
+  if (e == cudaErrorInvalidConfiguration)
+    return fail(DR_ERR_RANGE, "faces_per_pixel=%d too large for the fused silhouette backward", p.K);
+  if (e != cudaSuccess) return cuda_fail(e, "rasterize_silhouette backward");
+  return DR_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int dr_rasterize_silhouette_fwd(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                                const dr_raster_settings* s, double sigma, int64_t* p2f, float* alpha, void* ws,
+                                size_t ws_bytes, dr_stream_t stream) {
+  if (!alpha) return fail(DR_ERR_USAGE, "alpha is null");
+  return fwd_impl<float>(fv, first, num, N, F, s, p2f, nullptr, nullptr, nullptr, ws, ws_bytes,
+                         reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, alpha, sigma);
+}
+
+int dr_rasterize_silhouette_bwd(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                                const dr_raster_settings* s, double sigma, const int64_t* p2f, const float* d_alpha,
+                                double* grad, dr_stream_t stream) {
+  return sil_bwd_impl(fv, first, num, N, F, s, sigma, p2f, d_alpha, grad, reinterpret_cast<cudaStream_t>(stream));
+}
 
 void dr_raster_settings_default(dr_raster_settings* s) {
   if (!s) return;

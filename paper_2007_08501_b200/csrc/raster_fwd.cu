@@ -303,9 +303,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
 #ifndef DR_FINE_MINBLOCKS
 #define DR_FINE_MINBLOCKS 0
 #endif
-#ifndef DR_EMIT_PREFETCH
-#define DR_EMIT_PREFETCH 1
-#endif
 #ifndef DR_COMPACT
 #define DR_COMPACT 1  // compact the pairs the K-th-depth cull leaves before evaluating them
 #endif
@@ -439,6 +436,16 @@ __device__ DR_EMIT_ATTR void emit_slot(const FineArgs<OutT>& A, int64_t slot, bo
     A.bary[3 * slot + 2] = (OutT)0.0;
     A.dists[slot] = (OutT)0.0;
   }
+}
+
+// silhouette_blend's per-slot opacity (shading.cpp:82-83): sigmoid(-dist / sigma) of the slot's signed squared
+// distance, recomputed from the face (fast divisions: the value is consumed within tolerance, not selected on)
+__device__ __forceinline__ double silhouette_prob(const double* v, double px, double py, double sigma) {
+  const FaceGeom g = make_face_geom(v);
+  const V2 p{px, py};
+  const DistResult dr = point_triangle_dist2<false>(p, g, p - g.a, p - g.b, p - g.c);
+  const double x = -dr.dist / sigma;
+  return 1.0 / (1.0 + exp(-x));
 }
 
 // Insert (zc, f) into pixel p's sorted list (column p of [K][32]) in shared memory: shifting loop.
@@ -788,13 +795,13 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       const int pi = mi0 + row, pj = mj0 + col;
       const double px = pixel_x(A.W, pj), py = pixel_y(A.H, pi);
       const int64_t slot0 = (((int64_t)b * A.H + pi) * A.W + pj) * K;
-#if DR_EMIT_PREFETCH
       double vnext[9];
       int32_t fnext = ws.tid[lane];
       if (fnext != INT_MAX) {
 #pragma unroll
         for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
       }
+      double keep = 1.0;  // silhouette mode: prod over occupied slots of (1 - prob)
       for (int s = 0; s < K; ++s) {
         const int32_t f = fnext;
         double v[9];
@@ -805,19 +812,14 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 #pragma unroll
           for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
         }
-        emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, v, px, py);
-      }
-#else
-      for (int s = 0; s < K; ++s) {
-        const int32_t f = ws.tid[s * 32 + lane];
-        double v[9];
-        if (f != INT_MAX) {
-#pragma unroll
-          for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)f + t);
+        if (A.alpha) {
+          if (A.p2f) A.p2f[slot0 + s] = f != INT_MAX ? (int64_t)f : -1;
+          if (f != INT_MAX) keep *= 1.0 - silhouette_prob(v, px, py, A.sigma);
+        } else {
+          emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, v, px, py);
         }
-        emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, v, px, py);
       }
-#endif
+      if (A.alpha) A.alpha[((int64_t)b * A.H + pi) * A.W + pj] = (OutT)(1.0 - keep);  // shading.cpp:86
     }
     __syncwarp();
   }

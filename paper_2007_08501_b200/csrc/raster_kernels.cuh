@@ -32,6 +32,8 @@ struct FineArgs {
   OutT* zbuf;
   OutT* bary;
   OutT* dists;
+  OutT* alpha;   // non-null => fused silhouette_blend (shading.cpp:75-91): alpha [N,H,W] (+ p2f if non-null)
+  double sigma;  // silhouette opacity falloff (BlendParams.sigma)
 };
 
 template <typename InT>
@@ -47,6 +49,18 @@ struct BwdArgs {
   int64_t F;
   int H, W, K;
   bool persp, clip;
+};
+
+// fused silhouette_blend_backward + rasterize_backward (shading.cpp:93-121, MR:329-403 with d_zbuf = d_bary = 0)
+struct SilBwdArgs {
+  const double* fv;
+  const int64_t* p2f;     // [N,H,W,K]
+  const float* d_alpha;   // [N,H,W]
+  double* grad;           // [F,3,3]
+  int64_t npix;           // N*H*W
+  int64_t F;
+  int H, W, K;
+  double sigma;
 };
 
 // Camera (dr_camera / dr::Camera, camera.hpp:19-35) as kernel arguments.
@@ -96,6 +110,7 @@ cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st);
 cudaError_t launch_backward(const BwdArgs<double>& A, cudaStream_t st);
+cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st);
 size_t fine_warp_smem_bytes(int K);  // shared memory one warp of K2 needs
 
 }  // namespace drb

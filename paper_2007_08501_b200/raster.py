@@ -231,6 +231,74 @@ def rasterize_meshes_backward(face_verts, mesh_to_face_first_idx, num_faces_per_
     return grad
 
 
+def rasterize_silhouette(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
+                         sigma: float = 1e-4, want_pix_to_face: bool = True, workspace=None):
+    """Fused ``silhouette_blend(rasterize_meshes(...), sigma)`` (shading.cpp:75-91 over mesh_raster.cpp:234):
+    returns (pix_to_face int64 [N,H,W,K] or None, alpha float32 [N,H,W]). zbuf / bary / dists are never
+    materialised; pix_to_face is what the fused backward needs."""
+    L = _lib.load()
+    fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
+    N, F = int(first.numel()), int(fv.shape[0])
+    H, W = settings.hw
+    K = int(settings.faces_per_pixel)
+    s = settings.to_c()
+    dev = fv.device
+    ws_n = L.dr_rasterize_meshes_workspace_bytes(N, F, C.byref(s))
+    if ws_n == 0:
+        _check(_lib.DR_ERR_RANGE if N >= 1 else _lib.DR_ERR_SHAPE, "rasterize_silhouette")
+    if workspace is None or workspace.numel() < ws_n:
+        workspace = torch.empty(ws_n, dtype=torch.uint8, device=dev)
+    p2f = torch.empty((N, H, W, K), dtype=torch.int64, device=dev) if want_pix_to_face else None
+    alpha = torch.empty((N, H, W), dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        rc = L.dr_rasterize_silhouette_fwd(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma),
+                                           _ptr(p2f), _ptr(alpha), _ptr(workspace), workspace.numel(), _stream(dev))
+    _check(rc, "rasterize_silhouette")
+    return p2f, alpha
+
+
+def rasterize_silhouette_backward(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
+                                  sigma: float, pix_to_face, grad_alpha):
+    """Fused ``rasterize_backward(..., 0, 0, silhouette_blend_backward(frag, sigma, grad_alpha))``
+    (shading.cpp:93-121 + mesh_raster.cpp:329-403, the reference fit loop pipeline.cpp:153-162): returns
+    grad_face_verts [F,3,3] f64 (z components are zero: only the distance envelope carries gradient)."""
+    L = _lib.load()
+    fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
+    N, F = int(first.numel()), int(fv.shape[0])
+    H, W = settings.hw
+    K = int(settings.faces_per_pixel)
+    if tuple(pix_to_face.shape) != (N, H, W, K) or tuple(grad_alpha.shape) != (N, H, W):
+        raise ShapeError(f"rasterize_silhouette_backward: pix_to_face {tuple(pix_to_face.shape)} / grad_alpha "
+                         f"{tuple(grad_alpha.shape)} do not match [N,H,W,K] / [N,H,W] = {(N, H, W, K)}")
+    p2f = pix_to_face.to(torch.int64).contiguous()
+    ga = grad_alpha.to(torch.float32).contiguous()
+    grad = torch.zeros((F, 3, 3), dtype=torch.float64, device=fv.device)
+    s = settings.to_c()
+    with torch.cuda.device(fv.device):
+        rc = L.dr_rasterize_silhouette_bwd(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma),
+                                           _ptr(p2f), _ptr(ga), _ptr(grad), _stream(fv.device))
+    _check(rc, "rasterize_silhouette_backward")
+    return grad
+
+
+class RasterizeSilhouette(torch.autograd.Function):
+    """Autograd wrapper of the fused silhouette path: face_verts -> alpha [N,H,W]."""
+
+    @staticmethod
+    def forward(ctx, face_verts, first, num, settings: RasterSettings, sigma: float):
+        p2f, alpha = rasterize_silhouette(face_verts, first, num, settings, sigma)
+        ctx.settings, ctx.sigma = settings, sigma
+        ctx.save_for_backward(face_verts, torch.as_tensor(first, device=face_verts.device),
+                              torch.as_tensor(num, device=face_verts.device), p2f)
+        return alpha
+
+    @staticmethod
+    def backward(ctx, g_alpha):
+        fv, first, num, p2f = ctx.saved_tensors
+        g = rasterize_silhouette_backward(fv, first, num, ctx.settings, ctx.sigma, p2f, g_alpha)
+        return g.to(fv.dtype), None, None, None, None
+
+
 def bin_stats(num_meshes, num_faces, settings: RasterSettings, workspace: torch.Tensor) -> dict:
     """Coarse-stage counters left in the workspace by the last forward (synchronises)."""
     L = _lib.load()
