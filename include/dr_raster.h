@@ -186,6 +186,50 @@ int dr_rasterize_silhouette_bwd(const double* face_verts, const int64_t* mesh_to
                                 double sigma, const int64_t* pix_to_face, const float* grad_alpha,
                                 double* grad_face_verts, dr_stream_t stream);
 
+/* ---- point rasterizer ----
+ * Replaces dr::rasterize_points / rasterize_points_naive (point_render.hpp:33-36, point_render.cpp:82-155) on the
+ * same boundary as the meshes: points_ndc [P,3] fp64 = world_to_ndc (x_ndc, y_ndc, z_view) of the packed points
+ * (PointCloudBatch::points_packed, batching.hpp:138), cloud_to_packed_first_idx / num_points_per_cloud [N] int64.
+ * Outputs PointFragments (point_render.hpp:21-30): idx int64 [N,H,W,K] (packed point id, -1 empty), zbuf
+ * [N,H,W,K] (z_view, -1 empty), dists2 [N,H,W,K] (squared NDC distance, 0 empty); occupied slots ascending in
+ * (z, id). fp32 payload, or fp64 (_f64, bit-identical to the reference). */
+typedef struct dr_point_raster_settings {
+  int32_t image_h, image_w;   /* PointRasterSettings.image_h / image_w */
+  int32_t points_per_pixel;   /* K in [1, 128] */
+  int32_t bin_size;           /* 0 => rasterize_points_naive; > 0 => tiled (PointRasterSettings.tile_size) */
+  double radius;              /* splat radius in NDC (PointRasterSettings.radius); r2 = radius * radius */
+  double znear;               /* Camera.znear: points with z_view < znear are dropped (point_render.cpp:26) */
+  uint8_t clip_nonpositive_z; /* 1 for perspective cameras: drop points with z_view <= 0 (NdcPoint.clipped) */
+  uint8_t _reserved[7];       /* must be 0 */
+} dr_point_raster_settings;
+
+void dr_point_raster_settings_default(dr_point_raster_settings* s);
+size_t dr_rasterize_points_workspace_bytes(int64_t N, int64_t P, const dr_point_raster_settings* s);
+int dr_rasterize_points_fwd(const double* points_ndc, const int64_t* cloud_to_packed_first_idx,
+                            const int64_t* num_points_per_cloud, int64_t N, int64_t P,
+                            const dr_point_raster_settings* s, int64_t* idx, float* zbuf, float* dists2,
+                            void* workspace, size_t workspace_bytes, dr_stream_t stream);
+int dr_rasterize_points_fwd_f64(const double* points_ndc, const int64_t* cloud_to_packed_first_idx,
+                                const int64_t* num_points_per_cloud, int64_t N, int64_t P,
+                                const dr_point_raster_settings* s, int64_t* idx, double* zbuf, double* dists2,
+                                void* workspace, size_t workspace_bytes, dr_stream_t stream);
+/* grad_points_ndc [P,3] (overwritten on the batch's point ranges) = sum over occupied slots of
+ * (-2 (px - x) g_dists2, -2 (py - y) g_dists2, g_zbuf). The reference's splat_position_backward
+ * (point_render.cpp:302-338) is this with g_dists2 = -d_alpha / radius^2, g_zbuf = 0, then dr_points_ndc_backward. */
+int dr_rasterize_points_bwd(const double* points_ndc, const int64_t* cloud_to_packed_first_idx,
+                            const int64_t* num_points_per_cloud, int64_t N, int64_t P,
+                            const dr_point_raster_settings* s, const int64_t* idx, const float* grad_zbuf,
+                            const float* grad_dists2, double* grad_points_ndc, dr_stream_t stream);
+int dr_rasterize_points_bwd_f64(const double* points_ndc, const int64_t* cloud_to_packed_first_idx,
+                                const int64_t* num_points_per_cloud, int64_t N, int64_t P,
+                                const dr_point_raster_settings* s, const int64_t* idx, const double* grad_zbuf,
+                                const double* grad_dists2, double* grad_points_ndc, dr_stream_t stream);
+/* world_to_ndc (camera.cpp:36-70) of P packed points -> points_ndc [P,3], and its backward (camera.cpp:72-85). */
+int dr_world_to_points_ndc(const double* points, int64_t P, const dr_camera* cam, double* points_ndc,
+                           dr_stream_t stream);
+int dr_points_ndc_backward(const double* points, int64_t P, const dr_camera* cam, const double* grad_points_ndc,
+                           double* grad_points, dr_stream_t stream);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* dr_last_error(void);
 

@@ -65,8 +65,38 @@ class Oracle:
         L.orc_clamp_barycentric.argtypes = [_dp, _dp]
         L.orc_point_triangle_dist2_backward.argtypes = [_dp, _dp, _dp, _dp, C.c_double, _dp]
         L.orc_pixel_center_ndc.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        L.orc_rasterize_points.argtypes = [_dp, _i64p, _i64p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, C.c_double, C.c_double, C.c_int, _i64p, _dp, _dp]
+        L.orc_rasterize_points_bwd.argtypes = [_dp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, _i64p, _dp, _dp,
+                                               _dp]
         L.orc_silhouette_blend.argtypes = [_i64p, _dp, C.c_int64, C.c_int, C.c_double, _dp]
         L.orc_silhouette_blend_backward.argtypes = [_i64p, _dp, C.c_int64, C.c_int, C.c_double, _dp, _dp]
+
+    def rasterize_points(self, points_ndc, first, num, H, W, K, radius, tile=16, znear=0.1, clip_nonpositive_z=1):
+        """point_render.cpp:82-155 on points_ndc [P,3]; tile=0 = rasterize_points_naive."""
+        pts = np.ascontiguousarray(points_ndc, np.float64)
+        first = np.ascontiguousarray(first, np.int64)
+        num = np.ascontiguousarray(num, np.int64)
+        N = len(first)
+        S = N * H * W * K
+        idx, zb, d2 = np.empty(S, np.int64), np.empty(S), np.empty(S)
+        rc = self.lib.orc_rasterize_points(_p(pts, _dp), _p(first, _i64p), _p(num, _i64p), N, len(pts), H, W, K, tile,
+                                           radius, znear, clip_nonpositive_z, _p(idx, _i64p), _p(zb, _dp), _p(d2, _dp))
+        if rc:
+            raise RuntimeError(f"orc_rasterize_points rc={rc}")
+        shp = (N, H, W, K)
+        return idx.reshape(shp), zb.reshape(shp), d2.reshape(shp)
+
+    def rasterize_points_backward(self, points_ndc, idx, g_zbuf, g_dists2):
+        pts = np.ascontiguousarray(points_ndc, np.float64)
+        idx = np.ascontiguousarray(idx, np.int64)
+        gz = np.ascontiguousarray(g_zbuf, np.float64)
+        gd = np.ascontiguousarray(g_dists2, np.float64)
+        N, H, W, K = idx.shape
+        g = np.empty((len(pts), 3))
+        self.lib.orc_rasterize_points_bwd(_p(pts, _dp), len(pts), N, H, W, K, _p(idx, _i64p), _p(gz, _dp), _p(gd, _dp),
+                                          _p(g, _dp))
+        return g
 
     def silhouette_blend(self, p2f, dists, sigma):
         """shading.cpp:75-91 over fragments [N,H,W,K] -> alpha [N,H,W]."""
@@ -192,6 +222,9 @@ class RefLib:
         L.ref_rasterize.argtypes = [C.c_void_p, _dp, _i32p, C.c_double, C.c_int, _i64p, _dp, _dp, _dp]
         L.ref_rasterize_backward.argtypes = [C.c_void_p, _dp, _i32p, C.c_double, C.c_int32, _i64p, _dp, _dp,
                                              _dp, _dp, _dp, _dp, _dp]
+        L.ref_rasterize_points.argtypes = [_dp, _i64p, C.c_int32, _dp, _i32p, C.c_double, C.c_int, _i64p, _dp, _dp]
+        L.ref_splat_position_backward.argtypes = [_dp, _i64p, C.c_int32, _dp, _i32p, C.c_double, _i64p, _dp, _dp,
+                                                  _dp, _dp]
         L.ref_silhouette_blend.argtypes = [_i64p, _dp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _dp]
         L.ref_silhouette_blend_backward.argtypes = [_i64p, _dp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                                     C.c_double, _dp, _dp]
@@ -263,6 +296,36 @@ class RefLib:
     def point_triangle_dist2(self, p, a, b, c) -> float:
         arr = [np.asarray(x, np.float64) for x in (p, a, b, c)]
         return self.lib.ref_point_triangle_dist2(*[_p(x, _dp) for x in arr])
+
+    def rasterize_points(self, points, counts, cam_packed, H, W, K, radius, tile=16, naive=False):
+        """dr::rasterize_points / _naive (point_render.hpp:33-36) on world points [P,3] split by counts."""
+        pts = np.ascontiguousarray(points, np.float64)
+        counts = np.ascontiguousarray(counts, np.int64)
+        cam = np.ascontiguousarray(cam_packed, np.float64)
+        si = np.array([H, W, K, tile], np.int32)
+        n = len(counts)
+        S = n * H * W * K
+        idx, zb, d2 = np.empty(S, np.int64), np.empty(S), np.empty(S)
+        if self.lib.ref_rasterize_points(_p(pts, _dp), _p(counts, _i64p), n, _p(cam, _dp), _p(si, _i32p), radius,
+                                         int(naive), _p(idx, _i64p), _p(zb, _dp), _p(d2, _dp)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        shp = (n, H, W, K)
+        return idx.reshape(shp), zb.reshape(shp), d2.reshape(shp)
+
+    def splat_position_backward(self, points, counts, cam_packed, H, W, K, radius, frags, d_alphas, tile=16):
+        """dr::splat_position_backward (point_render.hpp:66-68): world-space d_points [P,3]."""
+        pts = np.ascontiguousarray(points, np.float64)
+        counts = np.ascontiguousarray(counts, np.int64)
+        cam = np.ascontiguousarray(cam_packed, np.float64)
+        si = np.array([H, W, K, tile], np.int32)
+        idx, zb, d2 = (np.ascontiguousarray(x) for x in frags)
+        da = np.ascontiguousarray(d_alphas, np.float64)
+        out = np.empty((len(pts), 3))
+        if self.lib.ref_splat_position_backward(_p(pts, _dp), _p(counts, _i64p), len(counts), _p(cam, _dp),
+                                                _p(si, _i32p), radius, _p(idx, _i64p), _p(zb, _dp), _p(d2, _dp),
+                                                _p(da, _dp), _p(out, _dp)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return out
 
     def silhouette_blend(self, p2f, dists, sigma):
         """dr::silhouette_blend (shading.hpp:37) over fragments [N,H,W,K] -> alpha [N,H,W]."""

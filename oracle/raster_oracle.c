@@ -525,3 +525,120 @@ void orc_silhouette_blend_backward(const int64_t* p2f, const double* dists, int6
     }
   }
 }
+
+/* ---- point rasterizer (/root/reference/proj/src/point_render.cpp, "PR") on the points_ndc boundary ----
+ * points_ndc [P,3] = (x_ndc, y_ndc, z_view) per packed point; tile = 0 selects rasterize_points_naive (PR:82-103),
+ * tile > 0 rasterize_points (PR:105-155). Outputs [N,H,W,K]: idx (-1 empty), zbuf (-1 empty), dists2 (0 empty). */
+typedef struct {
+  double z;
+  int64_t point;
+  double dist2;
+} pcand;
+
+static inline int pcand_less(const pcand* x, const pcand* y) { /* PR:37 */
+  return x->z != y->z ? x->z < y->z : x->point < y->point;
+}
+
+static inline void poffer(pcand* arr, int* n, int k, const pcand* c) {
+  int m = *n;
+  if (m == k) {
+    if (!pcand_less(c, &arr[k - 1])) return;
+    m = k - 1;
+  }
+  int pos = m;
+  while (pos > 0 && pcand_less(c, &arr[pos - 1])) {
+    arr[pos] = arr[pos - 1];
+    --pos;
+  }
+  arr[pos] = *c;
+  *n = m + 1;
+}
+
+static void pemit(int64_t* idx, double* zbuf, double* d2, int64_t slot0, int k, const pcand* arr, int n) {
+  for (int s = 0; s < k; ++s) { /* PR:60-80 */
+    if (s < n) {
+      idx[slot0 + s] = arr[s].point;
+      zbuf[slot0 + s] = arr[s].z;
+      d2[slot0 + s] = arr[s].dist2;
+    } else {
+      idx[slot0 + s] = -1;
+      zbuf[slot0 + s] = -1.0;
+      d2[slot0 + s] = 0.0;
+    }
+  }
+}
+
+int orc_rasterize_points(const double* pts, const int64_t* first, const int64_t* num, int64_t n_clouds, int64_t P,
+                         int h, int w, int k, int tile, double radius, double znear, int clip_nonpositive_z,
+                         int64_t* idx, double* zbuf, double* dists2) {
+  double r2 = radius * radius; /* PR:112 */
+  pcand* arr = (pcand*)malloc(sizeof(pcand) * (size_t)k);
+  int64_t* keep = (int64_t*)malloc(sizeof(int64_t) * (size_t)(P > 0 ? P : 1));
+  if (!arr || !keep) {
+    free(arr);
+    free(keep);
+    return 5;
+  }
+  for (int64_t b = 0; b < n_clouds; ++b) {
+    /* prepare_points (PR:17-31): clipped (perspective z_view <= 0) or z_view < znear are dropped */
+    int64_t nk = 0;
+    for (int64_t p = first[b]; p < first[b] + num[b]; ++p) {
+      double z = pts[3 * p + 2];
+      if (clip_nonpositive_z && z <= 0) continue;
+      if (z < znear) continue;
+      keep[nk++] = p;
+    }
+    int tiles_x = tile > 0 ? (w + tile - 1) / tile : 1, tiles_y = tile > 0 ? (h + tile - 1) / tile : 1;
+    for (int ty = 0; ty < tiles_y; ++ty) {
+      for (int tx = 0; tx < tiles_x; ++tx) {
+        int i0 = tile > 0 ? ty * tile : 0, i1 = tile > 0 ? (h < i0 + tile ? h : i0 + tile) : h;
+        int j0 = tile > 0 ? tx * tile : 0, j1 = tile > 0 ? (w < j0 + tile ? w : j0 + tile) : w;
+        double min_x = 0, max_x = 0, min_y = 0, max_y = 0;
+        if (tile > 0) { /* PR:125-132 */
+          v2 tl = pixel_center_ndc(h, w, i0, j0), br = pixel_center_ndc(h, w, i1 - 1, j1 - 1);
+          min_x = (tl.x < br.x ? tl.x : br.x) - radius;
+          max_x = (tl.x < br.x ? br.x : tl.x) + radius;
+          min_y = (tl.y < br.y ? tl.y : br.y) - radius;
+          max_y = (tl.y < br.y ? br.y : tl.y) + radius;
+        }
+        for (int i = i0; i < i1; ++i) {
+          for (int j = j0; j < j1; ++j) {
+            v2 pix = pixel_center_ndc(h, w, i, j);
+            int n = 0;
+            for (int64_t q = 0; q < nk; ++q) {
+              int64_t p = keep[q];
+              double x = pts[3 * p], y = pts[3 * p + 1];
+              if (tile > 0 && (x < min_x || x > max_x || y < min_y || y > max_y)) continue; /* PR:133-134 */
+              v2 xy = {x, y};
+              double d2 = norm2(sub(pix, xy)); /* PR:145 */
+              if (d2 <= r2) {
+                pcand c = {pts[3 * p + 2], p, d2};
+                poffer(arr, &n, k, &c);
+              }
+            }
+            pemit(idx, zbuf, dists2, (((int64_t)b * h + i) * w + j) * k, k, arr, n);
+          }
+        }
+      }
+    }
+  }
+  free(arr);
+  free(keep);
+  return 0;
+}
+
+/* d points_ndc [P,3] from per-slot cotangents on zbuf and dists2 (dists2 = |pix - xy|^2, zbuf = z_view) */
+void orc_rasterize_points_bwd(const double* pts, int64_t P, int64_t n_clouds, int h, int w, int k, const int64_t* idx,
+                              const double* g_zbuf, const double* g_d2, double* grad) {
+  for (int64_t i = 0; i < 3 * P; ++i) grad[i] = 0.0;
+  int64_t S = n_clouds * h * w * k;
+  for (int64_t slot = 0; slot < S; ++slot) {
+    int64_t p = idx[slot];
+    if (p < 0) continue;
+    int64_t px = slot / k, rem = px % ((int64_t)h * w);
+    v2 pix = pixel_center_ndc(h, w, (int)(rem / w), (int)(rem % w));
+    grad[3 * p] += -2.0 * (pix.x - pts[3 * p]) * g_d2[slot];
+    grad[3 * p + 1] += -2.0 * (pix.y - pts[3 * p + 1]) * g_d2[slot];
+    grad[3 * p + 2] += g_zbuf[slot];
+  }
+}

@@ -9,6 +9,7 @@
 //   dr::world_to_ndc                                (camera.hpp:50)
 //   dr::ico_sphere / cube / synthetic_batch         (templates.hpp:12-24)
 //   dr::silhouette_blend / silhouette_blend_backward (shading.hpp:37-41)
+//   dr::rasterize_points / _naive, splat_position_backward (point_render.hpp:33-36, 66-68)
 // Errors are caught and reported through ref_last_error() (the reference throws).
 #include <cstdint>
 #include <cstring>
@@ -20,6 +21,7 @@
 #include "dr/camera.hpp"
 #include "dr/core.hpp"
 #include "dr/mesh_raster.hpp"
+#include "dr/point_render.hpp"
 #include "dr/shading.hpp"
 #include "dr/templates.hpp"
 
@@ -207,6 +209,65 @@ int ref_silhouette_blend_backward(const int64_t* p2f, const double* dists, int32
     std::vector<double> da(d_alpha, d_alpha + ns / size_t(k));
     std::vector<double> dd = dr::silhouette_blend_backward(f, sigma, da);
     std::memcpy(d_dists, dd.data(), dd.size() * sizeof(double));
+  });
+}
+
+// ---- point clouds ----
+// points [P,3] world, counts [n]; si: [H, W, K, tile]; outputs [n,H,W,K]
+int ref_rasterize_points(const double* pts, const int64_t* counts, int32_t n, const double* cam, const int32_t* si,
+                         double radius, int naive, int64_t* idx, double* zbuf, double* dists2) {
+  return guarded([&] {
+    std::vector<std::vector<dr::Vec3>> pl(size_t(n > 0 ? n : 0));
+    int64_t o = 0;
+    for (int32_t b = 0; b < n; ++b)
+      for (int64_t i = 0; i < counts[b]; ++i, ++o) pl[size_t(b)].push_back({pts[3 * o], pts[3 * o + 1], pts[3 * o + 2]});
+    dr::PointCloudBatch pc(std::move(pl));
+    dr::Camera c = make_camera(cam);
+    dr::PointRasterSettings s;
+    s.image_h = si[0];
+    s.image_w = si[1];
+    s.points_per_pixel = si[2];
+    s.tile_size = si[3];
+    s.radius = radius;
+    dr::PointFragments f = naive ? dr::rasterize_points_naive(pc, c, s) : dr::rasterize_points(pc, c, s);
+    std::memcpy(idx, f.idx.data(), f.idx.size() * sizeof(int64_t));
+    std::memcpy(zbuf, f.zbuf.data(), f.zbuf.size() * sizeof(double));
+    std::memcpy(dists2, f.dists2.data(), f.dists2.size() * sizeof(double));
+  });
+}
+// splat_opacity -> d_alphas -> splat_position_backward (world-space d_points [P,3])
+int ref_splat_position_backward(const double* pts, const int64_t* counts, int32_t n, const double* cam,
+                                const int32_t* si, double radius, const int64_t* idx, const double* zbuf,
+                                const double* dists2, const double* d_alphas, double* d_points) {
+  return guarded([&] {
+    std::vector<std::vector<dr::Vec3>> pl(size_t(n > 0 ? n : 0));
+    int64_t o = 0;
+    for (int32_t b = 0; b < n; ++b)
+      for (int64_t i = 0; i < counts[b]; ++i, ++o) pl[size_t(b)].push_back({pts[3 * o], pts[3 * o + 1], pts[3 * o + 2]});
+    dr::PointCloudBatch pc(std::move(pl));
+    dr::Camera c = make_camera(cam);
+    dr::PointRasterSettings s;
+    s.image_h = si[0];
+    s.image_w = si[1];
+    s.points_per_pixel = si[2];
+    s.tile_size = si[3];
+    s.radius = radius;
+    dr::PointFragments f;
+    f.batch = n;
+    f.h = s.image_h;
+    f.w = s.image_w;
+    f.k = s.points_per_pixel;
+    size_t ns = size_t(f.slots());
+    f.idx.assign(idx, idx + ns);
+    f.zbuf.assign(zbuf, zbuf + ns);
+    f.dists2.assign(dists2, dists2 + ns);
+    std::vector<double> da(d_alphas, d_alphas + ns);
+    std::vector<dr::Vec3> g = dr::splat_position_backward(pc, c, s, f, da);
+    for (size_t i = 0; i < g.size(); ++i) {
+      d_points[3 * i] = g[i].x;
+      d_points[3 * i + 1] = g[i].y;
+      d_points[3 * i + 2] = g[i].z;
+    }
   });
 }
 

@@ -3,6 +3,7 @@
 Public surface (mirrors /root/reference/proj/include/dr/mesh_raster.hpp on the north-star boundary):
     RasterSettings, rasterize_meshes, rasterize_meshes_naive, rasterize_meshes_backward, RasterizeMeshes
     rasterize_silhouette, rasterize_silhouette_backward, RasterizeSilhouette (fused silhouette_blend, shading.cpp)
+    rasterize_points, rasterize_points_naive, rasterize_points_backward, PointRasterSettings (point_render.cpp)
 Input generators and the host camera transform live in ``scenes``; mesh sharding across GPUs in ``shard``.
 """
 from .raster import (  # noqa: F401
@@ -27,4 +28,14 @@ from .raster import (  # noqa: F401
     face_verts_backward,
     workspace_bytes,
     world_to_face_verts,
+)
+from .points import (  # noqa: F401
+    PointRasterSettings,
+    points_ndc_backward,
+    rasterize_points,
+    rasterize_points_backward,
+    rasterize_points_naive,
+    splat_opacity,
+    splat_position_backward,
+    world_to_points_ndc,
 )

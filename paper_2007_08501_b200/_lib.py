@@ -26,6 +26,14 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_meshes_bwd_hr",
     "dr_rasterize_silhouette_fwd",
     "dr_rasterize_silhouette_bwd",
+    "dr_point_raster_settings_default",
+    "dr_rasterize_points_workspace_bytes",
+    "dr_rasterize_points_fwd",
+    "dr_rasterize_points_fwd_f64",
+    "dr_rasterize_points_bwd",
+    "dr_rasterize_points_bwd_f64",
+    "dr_world_to_points_ndc",
+    "dr_points_ndc_backward",
     "dr_world_to_face_verts",
     "dr_face_verts_backward",
     "dr_packed_to_padded",
@@ -49,6 +57,15 @@ class DrRasterSettings(C.Structure):
         ("blur_radius", C.c_double), ("znear", C.c_double),
         ("clip_nonpositive_z", C.c_uint8), ("perspective_correct", C.c_uint8),
         ("clip_barycentric_coords", C.c_uint8), ("cull_backfaces", C.c_uint8), ("_reserved1", C.c_uint8 * 4),
+    ]
+
+
+class DrPointRasterSettings(C.Structure):
+    """dr_point_raster_settings (include/dr_raster.h) = PointRasterSettings (point_render.hpp:14-19)."""
+
+    _fields_ = [
+        ("image_h", C.c_int32), ("image_w", C.c_int32), ("points_per_pixel", C.c_int32), ("bin_size", C.c_int32),
+        ("radius", C.c_double), ("znear", C.c_double), ("clip_nonpositive_z", C.c_uint8), ("_reserved", C.c_uint8 * 7),
     ]
 
 
@@ -110,6 +127,19 @@ def load() -> C.CDLL:
                                               C.c_size_t, _vp]
     L.dr_rasterize_silhouette_bwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp,
                                               _vp]
+    pp = C.POINTER(DrPointRasterSettings)
+    L.dr_point_raster_settings_default.argtypes = [pp]
+    L.dr_rasterize_points_workspace_bytes.argtypes = [C.c_int64, C.c_int64, pp]
+    L.dr_rasterize_points_workspace_bytes.restype = C.c_size_t
+    for fn in ("dr_rasterize_points_fwd", "dr_rasterize_points_fwd_f64"):
+        getattr(L, fn).argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, pp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]
+    for fn in ("dr_rasterize_points_bwd", "dr_rasterize_points_bwd_f64"):
+        getattr(L, fn).argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, pp, _vp, _vp, _vp, _vp, _vp]
+    L.dr_world_to_points_ndc.argtypes = [_vp, C.c_int64, C.POINTER(DrCamera), _vp, _vp]
+    L.dr_points_ndc_backward.argtypes = [_vp, C.c_int64, C.POINTER(DrCamera), _vp, _vp, _vp]
+    for fn in ("dr_rasterize_points_fwd", "dr_rasterize_points_fwd_f64", "dr_rasterize_points_bwd",
+               "dr_rasterize_points_bwd_f64", "dr_world_to_points_ndc", "dr_points_ndc_backward"):
+        getattr(L, fn).restype = C.c_int
     for fn in ("dr_rasterize_silhouette_fwd", "dr_rasterize_silhouette_bwd", "dr_rasterize_meshes_fwd",
                "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
                "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_fwd_hr", "dr_rasterize_meshes_bwd_hr",

@@ -43,11 +43,12 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 // ---- optional per-kernel timing ring ----
-const char* kKernelNames[] = {"k_face_setup", "k_bin_faces", "k_fine",      "k_backward",          "memset",
-                              "k_camera",     "k_batching",  "k_sort_bins", "k_silhouette_backward"};
+const char* kKernelNames[] = {"k_face_setup",  "k_bin_faces",   "k_fine",        "k_backward",
+                              "memset",        "k_camera",      "k_batching",    "k_sort_bins",
+                              "k_silhouette_backward", "k_point_setup", "k_points_fine", "k_points_backward"};
 enum {
   KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5, KN_BATCH = 6, KN_SORT = 7,
-  KN_SIL_BWD = 8
+  KN_SIL_BWD = 8, KN_PT_SETUP = 9, KN_PT_FINE = 10, KN_PT_BWD = 11
 };
 struct ProfEntry {
   int kernel;
@@ -183,9 +184,9 @@ int read_ranges(const int64_t* first, const int64_t* num, int64_t N, int64_t F, 
   return DR_OK;
 }
 
-// Zero grad_face_verts on the union of the batch's face ranges only (merged intervals), so a caller may run the
-// backward on disjoint groups of meshes of one packed buffer (e.g. a copy/compute pipeline) concurrently.
-cudaError_t zero_face_ranges(double* grad, const std::vector<int64_t>& h, int64_t N, cudaStream_t st) {
+// Zero grad rows (`row` doubles per packed item) on the union of the batch's item ranges only (merged
+// intervals), so a caller may run the backward on disjoint groups of one packed buffer concurrently.
+cudaError_t zero_rows(double* grad, int row, const std::vector<int64_t>& h, int64_t N, cudaStream_t st) {
   std::vector<std::pair<int64_t, int64_t>> iv;
   for (int64_t b = 0; b < N; ++b)
     if (h[N + b] > 0) iv.push_back({h[b], h[b] + h[N + b]});
@@ -195,7 +196,7 @@ cudaError_t zero_face_ranges(double* grad, const std::vector<int64_t>& h, int64_
     int64_t lo = iv[i].first, hi = iv[i].second;
     size_t j = i + 1;
     while (j < iv.size() && iv[j].first <= hi) hi = std::max(hi, iv[j++].second);
-    cudaError_t e = cudaMemsetAsync(grad + 9 * lo, 0, sizeof(double) * 9 * (size_t)(hi - lo), st);
+    cudaError_t e = cudaMemsetAsync(grad + (int64_t)row * lo, 0, sizeof(double) * row * (size_t)(hi - lo), st);
     if (e != cudaSuccess) return e;
     i = j;
   }
@@ -335,7 +336,7 @@ int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   cudaError_t e;
   {
     ProfScope ps(st, KN_MEMSET);
-    e = zero_face_ranges(grad, ranges, N, st);
+    e = zero_rows(grad, 9, ranges, N, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "zeroing grad_face_verts");
   drb::BwdArgs<InT> A;
@@ -378,7 +379,7 @@ int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int
   cudaError_t e;
   {
     ProfScope ps(st, KN_MEMSET);
-    e = zero_face_ranges(grad, ranges, N, st);
+    e = zero_rows(grad, 9, ranges, N, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "zeroing grad_face_verts");
   drb::SilBwdArgs A;
@@ -402,9 +403,209 @@ int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int
   return DR_OK;
 }
 
+// ---- point rasterizer (point_render.cpp:105-155) ----
+struct PointPlan {
+  int64_t N = 0, P = 0;
+  int H = 0, W = 0, K = 0, bs = 16, nbx = 0, nby = 0;
+  bool binned = false;
+  int64_t nbins_total = 0, pool = 0;
+  size_t off_ibbox = 0, off_bounds = 0, off_counts = 0, off_cursor = 0, off_binoff = 0, off_lists = 0, total = 0;
+};
+
+int make_point_plan(int64_t N, int64_t P, const dr_point_raster_settings* s, PointPlan& p) {
+  if (!s) return fail(DR_ERR_USAGE, "settings pointer is null");
+  if (N < 1) return fail(DR_ERR_SHAPE, "empty point cloud batch (N=%lld)", (long long)N);
+  if (N > 65535) return fail(DR_ERR_RANGE, "N=%lld clouds exceeds 65535", (long long)N);
+  if (P < 0) return fail(DR_ERR_SHAPE, "negative point count P=%lld", (long long)P);
+  if (P > INT32_MAX - 1) return fail(DR_ERR_RANGE, "P=%lld exceeds the int32 point-id range", (long long)P);
+  if (s->image_h < 1 || s->image_w < 1 || s->image_h > 32768 || s->image_w > 32768)
+    return fail(DR_ERR_RANGE, "image size %dx%d outside [1, 32768]", s->image_h, s->image_w);
+  if (s->points_per_pixel < 1 || s->points_per_pixel > 128)
+    return fail(DR_ERR_RANGE, "points_per_pixel=%d outside [1, 128]", s->points_per_pixel);
+  if (s->bin_size < 0) return fail(DR_ERR_RANGE, "bin_size=%d < 0", s->bin_size);
+  if (std::isnan(s->radius) || std::isnan(s->znear)) return fail(DR_ERR_RANGE, "radius/znear is NaN");
+  p.N = N;
+  p.P = P;
+  p.H = s->image_h;
+  p.W = s->image_w;
+  p.K = s->points_per_pixel;
+  p.binned = s->bin_size > 0;
+  p.bs = p.binned ? s->bin_size : 16;
+  p.nbx = (p.W + p.bs - 1) / p.bs;
+  p.nby = (p.H + p.bs - 1) / p.bs;
+  size_t off = 0;
+  p.off_ibbox = off;
+  off = align_up(off + sizeof(int4) * (size_t)std::max<int64_t>(P, 1));
+  p.off_bounds = off;
+  off = align_up(off + sizeof(double) * 2 * (size_t)(p.nbx + p.nby));
+  p.off_counts = off;
+  if (p.binned) {
+    p.nbins_total = N * (int64_t)p.nbx * p.nby;
+    p.pool = 8 * P + 65536;
+    off = align_up(off + sizeof(int) * (size_t)p.nbins_total);
+    p.off_cursor = off;
+    off = align_up(off + sizeof(int) * (size_t)p.nbins_total);
+    p.off_binoff = off;
+    off = align_up(off + sizeof(int64_t) * (size_t)p.nbins_total);
+    p.off_lists = off;
+    off = align_up(off + sizeof(int4) * (size_t)p.pool);
+  }
+  p.total = off;
+  return DR_OK;
+}
+
+template <typename OutT>
+int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num, int64_t N, int64_t P,
+                    const dr_point_raster_settings* s, int64_t* idx, OutT* zbuf, OutT* dists2, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+  PointPlan p;
+  int rc = make_point_plan(N, P, s, p);
+  if (rc) return rc;
+  if (!first || !num || !idx || !zbuf || !dists2 || (P > 0 && !pts)) return fail(DR_ERR_USAGE, "null pointer");
+  if (!ws || ws_bytes < p.total)
+    return fail(DR_ERR_OOM, "workspace too small: %zu bytes given, %zu needed", ws_bytes, p.total);
+  int64_t max_pts = 0;
+  std::vector<int64_t> ranges;
+  rc = read_ranges(first, num, N, P, st, &max_pts, &ranges);
+  if (rc) return rc;
+  int64_t p_lo = P, p_hi = 0;
+  for (int64_t b = 0; b < N; ++b)
+    if (ranges[N + b] > 0) {
+      p_lo = std::min(p_lo, ranges[b]);
+      p_hi = std::max(p_hi, ranges[b] + ranges[N + b]);
+    }
+  char* base = static_cast<char*>(ws);
+  int4* ibbox = reinterpret_cast<int4*>(base + p.off_ibbox);
+  double* bounds = reinterpret_cast<double*>(base + p.off_bounds);
+  int* counts = reinterpret_cast<int*>(base + p.off_counts);
+  int* cursor = reinterpret_cast<int*>(base + p.off_cursor);
+  int64_t* bin_off = reinterpret_cast<int64_t*>(base + p.off_binoff);
+  int4* entries = reinterpret_cast<int4*>(base + p.off_lists);
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_PT_SETUP);
+    e = drb::launch_point_setup(pts, p_lo, p_hi, p.H, p.W, p.bs, p.nbx, p.nby, s->radius, s->znear,
+                                s->clip_nonpositive_z, bounds, ibbox, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "rasterize_points setup");
+  if (p.binned) {
+    {
+      ProfScope ps(st, KN_MEMSET);
+      cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)p.nbins_total, st);
+      cudaMemsetAsync(cursor, 0, sizeof(int) * (size_t)p.nbins_total, st);
+    }
+    ProfScope ps(st, KN_BIN);
+    drb::launch_bin_faces(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, st);
+    drb::launch_scan_bins(counts, p.nbins_total, bin_off, st);
+    drb::launch_fill_bins(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool, nullptr,
+                          entries, st);
+  }
+  drb::PointFineArgs<OutT> A;
+  A.pts = pts;
+  A.ibbox = ibbox;
+  A.first = first;
+  A.num = num;
+  A.bin_counts = counts;
+  A.bin_off = bin_off;
+  A.bin_entries = entries;
+  A.pool = p.pool;
+  A.binned = p.binned ? 1 : 0;
+  A.bs = p.bs;
+  A.nbx = p.nbx;
+  A.nby = p.nby;
+  A.sub_x = (p.bs + 15) / 16;
+  A.sub_y = (p.bs + 15) / 16;
+  A.H = p.H;
+  A.W = p.W;
+  A.K = p.K;
+  A.r2 = s->radius * s->radius;  // point_render.cpp:112
+  A.N = (int)N;
+  A.idx = idx;
+  A.zbuf = zbuf;
+  A.dists2 = dists2;
+  {
+    ProfScope ps(st, KN_PT_FINE);
+    e = drb::launch_points_fine(A, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "rasterize_points");
+  return DR_OK;
+}
+
+template <typename InT>
+int points_bwd_impl(const double* pts, const int64_t* first, const int64_t* num, int64_t N, int64_t P,
+                    const dr_point_raster_settings* s, const int64_t* idx, const InT* gz, const InT* gd, double* grad,
+                    cudaStream_t st) {
+  PointPlan p;
+  int rc = make_point_plan(N, P, s, p);
+  if (rc) return rc;
+  if (!first || !num || !idx || !gz || !gd || (P > 0 && (!pts || !grad))) return fail(DR_ERR_USAGE, "null pointer");
+  int64_t mx;
+  std::vector<int64_t> ranges;
+  rc = read_ranges(first, num, N, P, st, &mx, &ranges);
+  if (rc) return rc;
+  if (P == 0) return DR_OK;
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_MEMSET);
+    e = zero_rows(grad, 3, ranges, N, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "zeroing grad_points");
+  {
+    ProfScope ps(st, KN_PT_BWD);
+    e = drb::launch_points_backward(pts, idx, gz, gd, N * (int64_t)p.H * p.W * p.K, P, p.H, p.W, p.K, grad, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "rasterize_points backward");
+  return DR_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+void dr_point_raster_settings_default(dr_point_raster_settings* s) {
+  if (!s) return;
+  std::memset(s, 0, sizeof(*s));
+  s->image_h = s->image_w = 64;  // PointRasterSettings{} (point_render.hpp:14-19)
+  s->points_per_pixel = 8;
+  s->bin_size = 16;
+  s->radius = 0.05;
+  s->znear = 0.1;
+  s->clip_nonpositive_z = 1;
+}
+
+size_t dr_rasterize_points_workspace_bytes(int64_t N, int64_t P, const dr_point_raster_settings* s) {
+  PointPlan p;
+  if (make_point_plan(N, P, s, p)) return 0;
+  return p.total;
+}
+
+int dr_rasterize_points_fwd(const double* pts, const int64_t* first, const int64_t* num, int64_t N, int64_t P,
+                            const dr_point_raster_settings* s, int64_t* idx, float* zbuf, float* dists2, void* ws,
+                            size_t ws_bytes, dr_stream_t stream) {
+  return points_fwd_impl<float>(pts, first, num, N, P, s, idx, zbuf, dists2, ws, ws_bytes,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dr_rasterize_points_fwd_f64(const double* pts, const int64_t* first, const int64_t* num, int64_t N, int64_t P,
+                                const dr_point_raster_settings* s, int64_t* idx, double* zbuf, double* dists2,
+                                void* ws, size_t ws_bytes, dr_stream_t stream) {
+  return points_fwd_impl<double>(pts, first, num, N, P, s, idx, zbuf, dists2, ws, ws_bytes,
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dr_rasterize_points_bwd(const double* pts, const int64_t* first, const int64_t* num, int64_t N, int64_t P,
+                            const dr_point_raster_settings* s, const int64_t* idx, const float* grad_zbuf,
+                            const float* grad_dists2, double* grad_points, dr_stream_t stream) {
+  return points_bwd_impl<float>(pts, first, num, N, P, s, idx, grad_zbuf, grad_dists2, grad_points,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dr_rasterize_points_bwd_f64(const double* pts, const int64_t* first, const int64_t* num, int64_t N, int64_t P,
+                                const dr_point_raster_settings* s, const int64_t* idx, const double* grad_zbuf,
+                                const double* grad_dists2, double* grad_points, dr_stream_t stream) {
+  return points_bwd_impl<double>(pts, first, num, N, P, s, idx, grad_zbuf, grad_dists2, grad_points,
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
 
 int dr_rasterize_silhouette_fwd(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
                                 const dr_raster_settings* s, double sigma, int64_t* p2f, float* alpha, void* ws,
@@ -534,6 +735,36 @@ int dr_face_verts_backward(const double* verts, int64_t V, const int64_t* faces,
   }
   if (e != cudaSuccess) return cuda_fail(e, "face_verts_backward");
   return DR_OK;
+}
+
+int dr_world_to_points_ndc(const double* points, int64_t P, const dr_camera* cam, double* points_ndc,
+                           dr_stream_t stream) {
+  if (!cam) return fail(DR_ERR_USAGE, "camera pointer is null");
+  if (P < 0) return fail(DR_ERR_SHAPE, "negative point count");
+  if (P == 0) return DR_OK;
+  if (!points || !points_ndc) return fail(DR_ERR_USAGE, "null input/output pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_CAMERA);
+    e = drb::launch_world_to_points_ndc(points, P, camera_args(cam), points_ndc, st);
+  }
+  return e == cudaSuccess ? DR_OK : cuda_fail(e, "world_to_points_ndc");
+}
+
+int dr_points_ndc_backward(const double* points, int64_t P, const dr_camera* cam, const double* grad_points_ndc,
+                           double* grad_points, dr_stream_t stream) {
+  if (!cam) return fail(DR_ERR_USAGE, "camera pointer is null");
+  if (P < 0) return fail(DR_ERR_SHAPE, "negative point count");
+  if (P == 0) return DR_OK;
+  if (!points || !grad_points_ndc || !grad_points) return fail(DR_ERR_USAGE, "null input/output pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_CAMERA);
+    e = drb::launch_points_ndc_backward(points, P, camera_args(cam), grad_points_ndc, grad_points, st);
+  }
+  return e == cudaSuccess ? DR_OK : cuda_fail(e, "points_ndc_backward");
 }
 
 int dr_packed_to_padded(const void* packed, const int64_t* first, const int64_t* num, int64_t N, int64_t max_count,

@@ -30,14 +30,15 @@ __device__ __forceinline__ View world_to_view(const CameraArgs& c, double px, do
   return v;
 }
 
+// one output point per thread: face vertex t = faces[t] (n = 3F), or point t itself when faces == nullptr (n = P)
 __global__ void k_world_to_face_verts(const double* __restrict__ verts, int64_t V, const int64_t* __restrict__ faces,
-                                      int64_t F, CameraArgs c, double* __restrict__ fv, int* __restrict__ bad_index) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one face vertex
-  if (t >= 3 * F) return;
-  const int64_t vi = faces[t];
+                                      int64_t n, CameraArgs c, double* __restrict__ fv, int* __restrict__ bad_index) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t vi = faces ? faces[t] : t;
   double x = 0.0, y = 0.0, z = 0.0;
   if (vi < 0 || vi >= V) {
-    atomicExch(bad_index, 1);
+    if (bad_index) atomicExch(bad_index, 1);
     x = y = z = __longlong_as_double(0x7ff8000000000000LL);  // NaN: the face is culled downstream
   } else {
     const View v = world_to_view(c, verts[3 * vi], verts[3 * vi + 1], verts[3 * vi + 2]);
@@ -100,7 +101,25 @@ cudaError_t launch_world_to_face_verts(const double* verts, int64_t V, const int
                                        const CameraArgs& c, double* fv, int* bad_index, cudaStream_t st) {
   if (F <= 0) return cudaSuccess;
   const int64_t n = 3 * F;
-  k_world_to_face_verts<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(verts, V, faces, F, c, fv, bad_index);
+  k_world_to_face_verts<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(verts, V, faces, n, c, fv, bad_index);
+  return cudaGetLastError();
+}
+
+// point clouds: world_to_ndc of every packed point (prepare_points, point_render.cpp:17-31)
+cudaError_t launch_world_to_points_ndc(const double* points, int64_t P, const CameraArgs& c, double* out,
+                                       cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  k_world_to_face_verts<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(points, P, nullptr, P, c, out, nullptr);
+  return cudaGetLastError();
+}
+
+// world_to_ndc_backward per point (point_render.cpp:333-337)
+cudaError_t launch_points_ndc_backward(const double* points, int64_t P, const CameraArgs& c, const double* g_ndc,
+                                       double* g_world, cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemcpyAsync(g_world, g_ndc, sizeof(double) * 3 * (size_t)P, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  k_world_to_ndc_backward<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(points, P, c, g_world);
   return cudaGetLastError();
 }
 

@@ -63,6 +63,36 @@ struct SilBwdArgs {
   double sigma;
 };
 
+// point rasterizer (raster_points.cu)
+template <typename OutT>
+struct PointFineArgs {  // rasterize_points (point_render.cpp:105-155)
+  const double* pts;
+  const int4* ibbox;
+  const int64_t* first;
+  const int64_t* num;
+  const int* bin_counts;
+  const int64_t* bin_off;
+  const int4* bin_entries;
+  int64_t pool;
+  int binned, bs, nbx, nby, sub_x, sub_y;  // sub_x/sub_y: 16x16 blocks per bin row / column
+  int H, W, K;
+  double r2;
+  int N;
+  int64_t* idx;
+  OutT* zbuf;
+  OutT* dists2;
+};
+
+cudaError_t launch_point_setup(const double* pts, int64_t p_lo, int64_t p_hi, int H, int W, int ts, int nbx, int nby,
+                               double radius, double znear, int clip_z, double* bounds /*[2*nbx + 2*nby]*/,
+                               int4* ibbox, cudaStream_t st);
+cudaError_t launch_points_fine(const PointFineArgs<float>& A, cudaStream_t st);
+cudaError_t launch_points_fine(const PointFineArgs<double>& A, cudaStream_t st);
+cudaError_t launch_points_backward(const double* pts, const int64_t* idx, const float* gz, const float* gd, int64_t S,
+                                   int64_t P, int H, int W, int K, double* grad, cudaStream_t st);
+cudaError_t launch_points_backward(const double* pts, const int64_t* idx, const double* gz, const double* gd,
+                                   int64_t S, int64_t P, int H, int W, int K, double* grad, cudaStream_t st);
+
 // Camera (dr_camera / dr::Camera, camera.hpp:19-35) as kernel arguments.
 struct CameraArgs {
   double r[9];      // world -> view rotation, row-major
@@ -75,6 +105,10 @@ struct CameraArgs {
 
 cudaError_t launch_world_to_face_verts(const double* verts, int64_t V, const int64_t* faces, int64_t F,
                                        const CameraArgs& c, double* fv, int* bad_index, cudaStream_t st);
+cudaError_t launch_world_to_points_ndc(const double* points, int64_t P, const CameraArgs& c, double* out,
+                                       cudaStream_t st);
+cudaError_t launch_points_ndc_backward(const double* points, int64_t P, const CameraArgs& c, const double* g_ndc,
+                                       double* g_world, cudaStream_t st);
 cudaError_t launch_face_verts_backward(const double* verts, int64_t V, const int64_t* faces, int64_t F,
                                        const CameraArgs& c, const double* gfv, double* gverts, cudaStream_t st);
 // pad row of packed_to_padded (passed by value in the kernel parameters)

@@ -403,6 +403,21 @@ CONFIGS = {
 }
 
 
+def random_clouds(rng: Rng, batch: int, max_n: int, scale: float = 1.0) -> list:
+    """tests/helpers.hpp:23-33 (random_cloud_list): per cloud 1 + uniform_int(max_n) points ~ normal_vec3 * scale."""
+    out = []
+    for _ in range(batch):
+        n = 1 + rng.uniform_int(max_n)
+        out.append(np.array([np.array(rng.normal_vec3()) * scale for _ in range(n)], np.float64).reshape(n, 3))
+    return out
+
+
+def points_ndc(points: np.ndarray, cam: Camera) -> np.ndarray:
+    """world_to_ndc of packed points -> [P,3] (x_ndc, y_ndc, z_view), the point rasterizer's boundary input."""
+    xy, z, _ = world_to_ndc(cam, points)
+    return np.concatenate([xy, z[:, None]], axis=1)
+
+
 def config_meshes(name: str) -> Meshes:
     if name == "C1":
         return ico_sphere(3)
