@@ -384,7 +384,7 @@ struct WarpSmem {
 
 constexpr int kBuf = 8;  // buffered candidates per pixel before the owner lane merges them into its list
 
-// per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt
+// per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt | pairq
 __host__ __device__ constexpr size_t warp_smem_bytes(int K) {
   return (size_t)kNF * kRing * sizeof(double) + (size_t)K * 32 * sizeof(double) + (size_t)kBuf * 32 * sizeof(double) +
          12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) + (size_t)K * 32 * sizeof(int32_t) +
@@ -653,7 +653,9 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
 
 // 128 registers per thread (16 resident warps per SM) is the measured sweet spot: capping lower spills, and
 // fewer resident warps cannot hide the fp64 dependency latency (profiles/r01/README.md).
-template <typename OutT, int NW, int KMAX>
+// kSil: fused silhouette emit (alpha, optional pix_to_face) instead of the fragment payload — a separate
+// instantiation so the fragment path's code (and register allocation) does not carry it
+template <typename OutT, int NW, int KMAX, bool kSil>
 __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS : 16 / NW) k_fine(FineArgs<OutT> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -812,14 +814,14 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 #pragma unroll
           for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
         }
-        if (A.alpha) {
+        if constexpr (kSil) {
           if (A.p2f) A.p2f[slot0 + s] = f != INT_MAX ? (int64_t)f : -1;
           if (f != INT_MAX) keep *= 1.0 - silhouette_prob(v, px, py, A.sigma);
         } else {
           emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, v, px, py);
         }
       }
-      if (A.alpha) A.alpha[((int64_t)b * A.H + pi) * A.W + pj] = (OutT)(1.0 - keep);  // shading.cpp:86
+      if constexpr (kSil) A.alpha[((int64_t)b * A.H + pi) * A.W + pj] = (OutT)(1.0 - keep);  // shading.cpp:86
     }
     __syncwarp();
   }
@@ -890,10 +892,20 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
   auto by_k = [&](auto nw_c) -> cudaError_t {
     constexpr int NW = decltype(nw_c)::value;
     // register-resident merge for small K, shared-memory shifting loop otherwise
-    if (A.K == 1) return go(k_fine<OutT, NW, 1>);
-    if (A.K <= 4) return go(k_fine<OutT, NW, 4>);
-    if (A.K <= 8) return go(k_fine<OutT, NW, 8>);
-    return go(k_fine<OutT, NW, 0>);
+    if (A.alpha) {
+      if constexpr (std::is_same<OutT, float>::value) {
+        if (A.K == 1) return go(k_fine<OutT, NW, 1, true>);
+        if (A.K <= 4) return go(k_fine<OutT, NW, 4, true>);
+        if (A.K <= 8) return go(k_fine<OutT, NW, 8, true>);
+        return go(k_fine<OutT, NW, 0, true>);
+      } else {
+        return cudaErrorInvalidValue;  // the fused silhouette writes fp32 alpha only
+      }
+    }
+    if (A.K == 1) return go(k_fine<OutT, NW, 1, false>);
+    if (A.K <= 4) return go(k_fine<OutT, NW, 4, false>);
+    if (A.K <= 8) return go(k_fine<OutT, NW, 8, false>);
+    return go(k_fine<OutT, NW, 0, false>);
   };
   if (nw == 8) return by_k(std::integral_constant<int, 8>{});
   return by_k(std::integral_constant<int, 2>{});
