@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-groups", type=int, default=8, help="mesh groups the host pipeline streams")
+    ap.add_argument("--e2e-groups", type=int, default=16, help="mesh groups the host pipeline streams")
     ap.add_argument("--cpu-sample-faces", type=float, default=0.25,
                     help="fraction of the batch's faces the CPU sample covers")
     return ap.parse_args()
