@@ -354,6 +354,8 @@ int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   A.K = p.K;
   A.persp = s->perspective_correct != 0;
   A.clip = s->clip_barycentric_coords != 0;
+  A.divK = drb::FastDivU32((uint32_t)p.K);
+  A.divW = drb::FastDivU32((uint32_t)p.W);
   {
     ProfScope ps(st, KN_BWD);
     e = drb::launch_backward(A, st);

@@ -63,9 +63,9 @@ __device__ __forceinline__ void load_slot(const BwdArgs<InT>& A, int64_t slot, i
 #endif
 }
 
-// per-slot cotangents -> g[9] = (dx, dy, dz) for vertices a, b, c; (i, j) = the slot's pixel
+// per-slot cotangents -> g[9] = (dx, dy, dz) for vertices a, b, c; p = the slot's pixel centre (MR:357)
 template <typename InT>
-__device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int i, int j, int32_t fid, const SlotIn<InT>& in,
+__device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32_t fid, const SlotIn<InT>& in,
                                               double g[9]) {
 #if DR_BWD_PREFETCH_FV
   const FaceGeom fg = make_face_geom(in.v);
@@ -77,7 +77,6 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, int i, int 
   const FaceGeom fg = make_face_geom(v);
 #endif
   const double z[3] = {fg.z0, fg.z1, fg.z2};
-  const V2 p{pixel_x(A.W, j), pixel_y(A.H, i)};  // MR:357
 
   const double w_hat[3] = {(double)in.w[0], (double)in.w[1], (double)in.w[2]};
   const double dz = (double)in.dz;
@@ -205,11 +204,11 @@ constexpr int kBwdChunk = 32 * 16;
 constexpr int kBwdThreads = DR_BWD_THREADS;
 
 template <typename InT>
-__device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, int i, int j, int32_t my_fid,
-                                               const SlotIn<InT>& in, int lane) {
+__device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, V2 p, int32_t my_fid, const SlotIn<InT>& in,
+                                               int lane) {
   double g[9];
   if (my_fid >= 0) {
-    slot_backward(A, i, j, my_fid, in, g);
+    slot_backward(A, p, my_fid, in, g);
   } else {
 #pragma unroll
     for (int k = 0; k < 9; ++k) g[k] = 0.0;
@@ -225,10 +224,19 @@ __device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, int i, int
 // lane in flight, instead of one exposed load latency per 32 slots) and compacts the occupied slots into a
 // warp-private queue in shared memory. Phase B: the queue is processed 32 slots per step, the next step's
 // bary / cotangents loaded before the current step computes.
+constexpr int kPixTab = 2048;  // pixel-centre tables in shared memory when H + W fits
+
 template <typename InT>
 __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdArgs<InT> A) {
   __shared__ int32_t q_off[kBwdThreads / 32][kBwdChunk];
   __shared__ int32_t q_fid[kBwdThreads / 32][kBwdChunk];
+  __shared__ double pix_tab[kPixTab];  // pixel_x(W, j) for j < W, then pixel_y(H, i) (camera.cpp:100-102)
+  const bool tab = A.W + A.H <= kPixTab;
+  if (tab) {
+    for (int t = threadIdx.x; t < A.W + A.H; t += kBwdThreads)
+      pix_tab[t] = t < A.W ? pixel_x(A.W, t) : pixel_y(A.H, t - A.W);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -278,14 +286,14 @@ __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdA
         nfid = qf[q0 + 32 + lane];
         load_slot(A, c0 + noff, nfid, nxt);
       }
-      int i = 0, j = 0;
+      V2 p{0.0, 0.0};
       if (my_fid >= 0) {
-        int pp = pp0 + (r0 + off) / A.K;
-        if (pp >= HW) pp %= HW;  // the chunk crossed into the next image
-        i = pp / A.W;
-        j = pp - i * A.W;
+        uint32_t pp = (uint32_t)pp0 + A.divK.div((uint32_t)(r0 + off));
+        if (pp >= (uint32_t)HW) pp %= (uint32_t)HW;  // the chunk crossed into the next image
+        const uint32_t i = A.divW.div(pp), j = pp - i * (uint32_t)A.W;
+        p = tab ? V2{pix_tab[j], pix_tab[A.W + i]} : V2{pixel_x(A.W, (int)j), pixel_y(A.H, (int)i)};  // MR:357
       }
-      backward_batch(A, i, j, my_fid, cur, lane);
+      backward_batch(A, p, my_fid, cur, lane);
     }
     __syncwarp();
   }

@@ -382,7 +382,10 @@ struct WarpSmem {
   }
 };
 
-constexpr int kBuf = 8;  // buffered candidates per pixel before the owner lane merges them into its list
+#ifndef DR_KBUF
+#define DR_KBUF 8
+#endif
+constexpr int kBuf = DR_KBUF;  // buffered candidates per pixel before the owner lane merges them into its list
 
 // per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt | pairq
 __host__ __device__ constexpr size_t warp_smem_bytes(int K) {

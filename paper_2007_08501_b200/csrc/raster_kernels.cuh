@@ -36,6 +36,25 @@ struct FineArgs {
   double sigma;  // silhouette opacity falloff (BlendParams.sigma)
 };
 
+// Unsigned 32-bit division by a run-time invariant divisor with one multiply-high (Granlund & Montgomery,
+// "Division by invariant integers using multiplication", Fig. 4.1): exact for every 32-bit dividend.
+struct FastDivU32 {
+  uint32_t d = 1, m = 1;
+  int sh1 = 0, sh2 = 0;
+  FastDivU32() = default;
+  explicit FastDivU32(uint32_t div) : d(div) {
+    int l = 0;
+    while (l < 32 && (1ull << l) < div) ++l;  // l = ceil(log2 d)
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+    sh1 = l < 1 ? l : 1;
+    sh2 = l - 1 > 0 ? l - 1 : 0;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    const uint32_t t1 = __umulhi(m, n);
+    return (t1 + ((n - t1) >> sh1)) >> sh2;
+  }
+};
+
 template <typename InT>
 struct BwdArgs {
   const double* fv;
@@ -49,6 +68,7 @@ struct BwdArgs {
   int64_t F;
   int H, W, K;
   bool persp, clip;
+  FastDivU32 divK, divW;  // slot -> pixel -> (i, j) without integer division instructions
 };
 
 // fused silhouette_blend_backward + rasterize_backward (shading.cpp:93-121, MR:329-403 with d_zbuf = d_bary = 0)
