@@ -1,7 +1,9 @@
-// dr_b200:: host adaptor (include/dr_b200/mesh_raster.hpp): the reference's C++ surface on top of the C-ABI.
+// dr_b200:: host adaptor (include/dr_b200/*.hpp): the reference's C++ surface on top of the C-ABI.
 //
 // rasterize_meshes:  verts/faces -> HBM -> dr_world_to_face_verts -> dr_rasterize_meshes_fwd_f64 -> host
 // rasterize_backward: fragments + cotangents -> HBM -> dr_rasterize_meshes_bwd_f64 -> dr_face_verts_backward -> host
+// rasterize_silhouette(_backward): the same with the fused silhouette entry points
+// rasterize_points / splat_position_backward: points -> HBM -> dr_world_to_points_ndc -> dr_rasterize_points_*
 // Error codes from the C-ABI are rethrown as the reference's exception types.
 #include <cuda_runtime.h>
 
@@ -10,6 +12,8 @@
 #include <utility>
 
 #include "../../include/dr_b200/mesh_raster.hpp"
+#include "../../include/dr_b200/point_render.hpp"
+#include "../../include/dr_b200/shading.hpp"
 #include "../../include/dr_raster.h"
 
 namespace dr_b200 {
@@ -262,6 +266,188 @@ std::vector<Vec3> rasterize_backward(const MeshBatch& m, const Camera& c, const 
         "world_to_ndc_backward");
   std::vector<Vec3> out(size_t(d.V));
   download(reinterpret_cast<double*>(out.data()), gv, 3 * (size_t)d.V);
+  return out;
+}
+
+// ---- fused silhouette (pipeline.cpp:153-162) ----
+
+SilhouetteFragments rasterize_silhouette(const MeshBatch& m, const Camera& c, const RasterSettings& s, double sigma) {
+  DeviceMesh d(m, c);
+  dr_raster_settings rs = to_c(s, c, s.tile_size <= 0);
+  size_t ws_bytes = dr_rasterize_meshes_workspace_bytes(d.N, d.F, &rs);
+  if (ws_bytes == 0) throw_status(DR_ERR_RANGE, "rasterize_silhouette");
+  SilhouetteFragments out;
+  out.batch = m.size();
+  out.h = s.image_h;
+  out.w = s.image_w;
+  out.k = s.faces_per_pixel;
+  const size_t npix = (size_t)out.batch * out.h * out.w, S = npix * (size_t)out.k;
+  DevBuf ws(ws_bytes), p2f(sizeof(int64_t) * S), alpha(sizeof(float) * npix);
+  check(dr_rasterize_silhouette_fwd(d.fv.as<double>(), d.first.as<int64_t>(), d.num.as<int64_t>(), d.N, d.F, &rs,
+                                    sigma, p2f.as<int64_t>(), alpha.as<float>(), ws.p, ws_bytes, nullptr),
+        "rasterize_silhouette");
+  out.pix_to_face.resize(S);
+  download(out.pix_to_face.data(), p2f, S);
+  std::vector<float> a(npix);
+  download(a.data(), alpha, npix);
+  out.alpha.assign(a.begin(), a.end());
+  return out;
+}
+
+std::vector<Vec3> rasterize_silhouette_backward(const MeshBatch& m, const Camera& c, const RasterSettings& s,
+                                                double sigma, const SilhouetteFragments& frag,
+                                                const std::vector<double>& d_alpha) {
+  const size_t npix = (size_t)frag.batch * frag.h * frag.w;
+  if (d_alpha.size() != npix) throw ShapeError("silhouette_blend_backward: cotangent shape mismatch");  // SH:98
+  if (frag.batch != m.size() || frag.h != s.image_h || frag.w != s.image_w || frag.k != s.faces_per_pixel ||
+      frag.pix_to_face.size() != npix * (size_t)frag.k)
+    throw ShapeError("rasterize_silhouette_backward: fragments were not produced with these settings");
+  DeviceMesh d(m, c);
+  dr_raster_settings rs = to_c(s, c, false);
+  DevBuf p2f(sizeof(int64_t) * npix * frag.k), da(sizeof(float) * npix), gfv(sizeof(double) * 9 * d.F),
+      gv(sizeof(double) * 3 * d.V);
+  upload(p2f, frag.pix_to_face.data(), npix * (size_t)frag.k);
+  std::vector<float> da32(d_alpha.begin(), d_alpha.end());
+  upload(da, da32.data(), npix);
+  check(dr_rasterize_silhouette_bwd(d.fv.as<double>(), d.first.as<int64_t>(), d.num.as<int64_t>(), d.N, d.F, &rs,
+                                    sigma, p2f.as<int64_t>(), da.as<float>(), gfv.as<double>(), nullptr),
+        "rasterize_silhouette_backward");
+  dr_camera cam = to_c(c);
+  check(dr_face_verts_backward(d.verts.as<double>(), d.V, d.faces.as<int64_t>(), d.F, &cam, gfv.as<double>(),
+                               gv.as<double>(), nullptr),
+        "world_to_ndc_backward");
+  std::vector<Vec3> out(size_t(d.V));
+  download(reinterpret_cast<double*>(out.data()), gv, 3 * (size_t)d.V);
+  return out;
+}
+
+// ---- point clouds (point_render.cpp) ----
+
+PointCloudBatch::PointCloudBatch(std::vector<std::vector<Vec3>> points_list) : points_list_(std::move(points_list)) {
+  if (points_list_.empty()) throw ShapeError("empty point cloud batch");
+  const size_t n = points_list_.size();
+  num_points_.resize(n);
+  points_packed_.offsets.assign(n + 1, 0);
+  for (size_t i = 0; i < n; ++i) {
+    num_points_[i] = int64_t(points_list_[i].size());
+    points_packed_.offsets[i + 1] = points_packed_.offsets[i] + num_points_[i];
+  }
+  points_packed_.data.reserve(size_t(points_packed_.offsets.back()));
+  for (const auto& l : points_list_) points_packed_.data.insert(points_packed_.data.end(), l.begin(), l.end());
+}
+
+PointCloudBatch PointCloudBatch::with_points(const std::vector<Vec3>& new_points_packed) const {
+  if (int64_t(new_points_packed.size()) != total_points())
+    throw ShapeError("with_points: expected " + std::to_string(total_points()) + " packed points, got " +
+                     std::to_string(new_points_packed.size()));
+  std::vector<std::vector<Vec3>> lists(points_list_.size());
+  for (size_t i = 0; i < points_list_.size(); ++i) {
+    auto b = new_points_packed.begin() + points_packed_.offsets[i];
+    lists[i].assign(b, b + num_points_[i]);
+  }
+  return PointCloudBatch(std::move(lists));
+}
+
+namespace {
+
+struct DevicePoints {
+  int64_t P, N;
+  DevBuf pts, ndc, first, num;
+  DevicePoints(const PointCloudBatch& pc, const Camera& c)
+      : P(pc.total_points()),
+        N(pc.size()),
+        pts(sizeof(double) * 3 * P),
+        ndc(sizeof(double) * 3 * P),
+        first(sizeof(int64_t) * N),
+        num(sizeof(int64_t) * N) {
+    upload(pts, reinterpret_cast<const double*>(pc.points_packed().data.data()), 3 * (size_t)P);
+    upload(first, pc.points_packed().offsets.data(), (size_t)N);
+    upload(num, pc.num_points_per_cloud().data(), (size_t)N);
+    dr_camera cam = to_c(c);
+    check(dr_world_to_points_ndc(pts.as<double>(), P, &cam, ndc.as<double>(), nullptr), "world_to_ndc");
+  }
+};
+
+dr_point_raster_settings to_c(const PointRasterSettings& s, const Camera& c, bool naive) {
+  dr_point_raster_settings o;
+  std::memset(&o, 0, sizeof(o));
+  o.image_h = s.image_h;
+  o.image_w = s.image_w;
+  o.points_per_pixel = s.points_per_pixel;
+  o.bin_size = naive ? 0 : s.tile_size;
+  o.radius = s.radius;
+  o.znear = c.znear;
+  o.clip_nonpositive_z = c.kind == ProjectionKind::Perspective ? 1 : 0;
+  return o;
+}
+
+PointFragments run_points(const PointCloudBatch& pc, const Camera& c, const PointRasterSettings& s, bool naive) {
+  DevicePoints d(pc, c);
+  dr_point_raster_settings rs = to_c(s, c, naive);
+  size_t ws_bytes = dr_rasterize_points_workspace_bytes(d.N, d.P, &rs);
+  if (ws_bytes == 0) throw_status(DR_ERR_RANGE, "rasterize_points");
+  PointFragments f;
+  f.batch = pc.size();
+  f.h = s.image_h;
+  f.w = s.image_w;
+  f.k = s.points_per_pixel;
+  const size_t S = (size_t)f.slots();
+  DevBuf ws(ws_bytes), idx(sizeof(int64_t) * S), zb(sizeof(double) * S), d2(sizeof(double) * S);
+  check(dr_rasterize_points_fwd_f64(d.ndc.as<double>(), d.first.as<int64_t>(), d.num.as<int64_t>(), d.N, d.P, &rs,
+                                    idx.as<int64_t>(), zb.as<double>(), d2.as<double>(), ws.p, ws_bytes, nullptr),
+        "rasterize_points");
+  f.idx.resize(S);
+  f.zbuf.resize(S);
+  f.dists2.resize(S);
+  download(f.idx.data(), idx, S);
+  download(f.zbuf.data(), zb, S);
+  download(f.dists2.data(), d2, S);
+  return f;
+}
+
+}  // namespace
+
+PointFragments rasterize_points(const PointCloudBatch& pc, const Camera& c, const PointRasterSettings& s) {
+  return run_points(pc, c, s, /*naive=*/s.tile_size <= 0);
+}
+
+PointFragments rasterize_points_naive(const PointCloudBatch& pc, const Camera& c, const PointRasterSettings& s) {
+  return run_points(pc, c, s, /*naive=*/true);
+}
+
+std::vector<double> splat_opacity(const PointFragments& frag, double radius) {
+  std::vector<double> alpha(size_t(frag.slots()), 0.0);  // point_render.cpp:157-168
+  const double inv_r2 = 1.0 / (radius * radius);
+  for (size_t slot = 0; slot < alpha.size(); ++slot)
+    if (frag.idx[slot] >= 0) alpha[slot] = 1.0 - frag.dists2[slot] * inv_r2;
+  return alpha;
+}
+
+std::vector<Vec3> splat_position_backward(const PointCloudBatch& pc, const Camera& c, const PointRasterSettings& s,
+                                          const PointFragments& frag, const std::vector<double>& d_alphas) {
+  if (int64_t(d_alphas.size()) != frag.slots())
+    throw ShapeError("splat_position_backward: cotangent shape mismatch");  // point_render.cpp:305-306
+  DevicePoints d(pc, c);
+  dr_point_raster_settings rs = to_c(s, c, false);
+  const size_t S = (size_t)frag.slots();
+  // alpha = 1 - dists2 / r^2  =>  d dists2 = -d_alpha / r^2; zbuf carries no gradient here
+  const double inv_r2 = 1.0 / (s.radius * s.radius);
+  std::vector<double> gd(S, 0.0), gz(S, 0.0);
+  for (size_t slot = 0; slot < S; ++slot)
+    if (frag.idx[slot] >= 0) gd[slot] = -d_alphas[slot] * inv_r2;
+  DevBuf idx(sizeof(int64_t) * S), dgz(sizeof(double) * S), dgd(sizeof(double) * S), gndc(sizeof(double) * 3 * d.P),
+      gw(sizeof(double) * 3 * d.P);
+  upload(idx, frag.idx.data(), S);
+  upload(dgz, gz.data(), S);
+  upload(dgd, gd.data(), S);
+  check(dr_rasterize_points_bwd_f64(d.ndc.as<double>(), d.first.as<int64_t>(), d.num.as<int64_t>(), d.N, d.P, &rs,
+                                    idx.as<int64_t>(), dgz.as<double>(), dgd.as<double>(), gndc.as<double>(), nullptr),
+        "rasterize_points_backward");
+  dr_camera cam = to_c(c);
+  check(dr_points_ndc_backward(d.pts.as<double>(), d.P, &cam, gndc.as<double>(), gw.as<double>(), nullptr),
+        "world_to_ndc_backward");
+  std::vector<Vec3> out(size_t(d.P));
+  download(reinterpret_cast<double*>(out.data()), gw, 3 * (size_t)d.P);
   return out;
 }
 

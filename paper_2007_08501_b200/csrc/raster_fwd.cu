@@ -306,6 +306,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
 #ifndef DR_COMPACT
 #define DR_COMPACT 1  // compact the pairs the K-th-depth cull leaves before evaluating them
 #endif
+#ifndef DR_T_REFRESH
+#define DR_T_REFRESH 1
+#endif
 #ifndef DR_LEAN_STAGE
 #define DR_LEAN_STAGE 1
 #endif
@@ -727,7 +730,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 
     const bool valid_px = (lane >> 3) < vh && (lane & 7) < vw;
     double T = pos_inf();  // max over the micro-tile's pixels of the K-th candidate depth (+inf: a list not full)
-    int head = 0, pending = 0;
+    int head = 0, pending = 0, groups = 0;
     for (int64_t c0 = 0; c0 < nsrc; c0 += 32) {
       const int64_t ci = c0 + lane;
       uint32_t r = 0u;
@@ -774,9 +777,12 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
           ran = true;
         }
         if (A.zsort && ran) {  // refresh T: merge the buffered candidates, then max of the K-th depths
-          __syncwarp();
-          merge_buffers<KMAX>(ws, K, lane);
-          __syncwarp();
+          // (every DR_T_REFRESH groups; the list tails alone are a valid, looser threshold in between)
+          if (++groups % DR_T_REFRESH == 0) {
+            __syncwarp();
+            merge_buffers<KMAX>(ws, K, lane);
+            __syncwarp();
+          }
           double t = valid_px ? ws.tz[(K - 1) * 32 + lane] : -pos_inf();
 #pragma unroll
           for (int d = 16; d >= 1; d >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, d));

@@ -11,8 +11,12 @@
 #include "dr/batching.hpp"
 #include "dr/camera.hpp"
 #include "dr/mesh_raster.hpp"
+#include "dr/point_render.hpp"
+#include "dr/shading.hpp"
 #include "dr/templates.hpp"
 #include "dr_b200/mesh_raster.hpp"
+#include "dr_b200/point_render.hpp"
+#include "dr_b200/shading.hpp"
 
 namespace ref = dr;
 namespace gpu = dr_b200;
@@ -234,6 +238,92 @@ static void errors_mirror_reference() {
   CHECK(threw);
 }
 
+static double max_rel(const std::vector<double>& a, const std::vector<double>& b) {
+  double num = 0, den = 1e-300;
+  for (size_t i = 0; i < a.size() && i < b.size(); ++i) {
+    num = std::fmax(num, std::fabs(a[i] - b[i]));
+    den = std::fmax(den, std::fabs(b[i]));
+  }
+  return a.size() == b.size() ? num / den : 1e300;
+}
+
+static std::vector<double> flat(const std::vector<gpu::Vec3>& v) {
+  std::vector<double> o;
+  for (const auto& p : v) o.insert(o.end(), {p.x, p.y, p.z});
+  return o;
+}
+static std::vector<double> flat(const std::vector<ref::Vec3>& v) {
+  std::vector<double> o;
+  for (const auto& p : v) o.insert(o.end(), {p.x, p.y, p.z});
+  return o;
+}
+
+// test_point_render.cpp:24-43 against the GPU mirror: tiled == naive == reference, bit for bit
+static void points_tiled_naive_reference() {
+  ref::Rng rng(83);
+  for (int trial = 0; trial < 15; ++trial) {
+    int b = 1 + int(rng.uniform_int(3));
+    std::vector<std::vector<ref::Vec3>> clouds(static_cast<size_t>(b));
+    for (auto& cl : clouds) {  // tests/helpers.hpp:23-33
+      int64_t n = 1 + rng.uniform_int(200);
+      for (int64_t i = 0; i < n; ++i) cl.push_back(rng.normal_vec3());
+    }
+    ref::PointRasterSettings s;
+    s.image_h = s.image_w = rng.uniform_int(2) == 0 ? 32 : 64;
+    s.points_per_pixel = rng.uniform_int(2) == 0 ? 1 : 8;
+    s.radius = rng.uniform(0.02, 0.15);
+    s.tile_size = rng.uniform_int(2) == 0 ? 16 : 8;
+    ref::Camera cam = rng.uniform_int(2) == 0 ? ref::Camera::look_from_distance(3.0, ref::ProjectionKind::Perspective, 1.5)
+                                              : ref::Camera::look_from_distance(3.0, ref::ProjectionKind::Orthographic);
+    ref::PointFragments want = ref::rasterize_points(ref::PointCloudBatch(clouds), cam, s);
+    std::vector<std::vector<gpu::Vec3>> gc(clouds.size());
+    for (size_t i = 0; i < clouds.size(); ++i)
+      for (const auto& p : clouds[i]) gc[i].push_back({p.x, p.y, p.z});
+    gpu::PointCloudBatch pc(gc);
+    gpu::PointRasterSettings gs;
+    gs.image_h = s.image_h;
+    gs.image_w = s.image_w;
+    gs.points_per_pixel = s.points_per_pixel;
+    gs.radius = s.radius;
+    gs.tile_size = s.tile_size;
+    gpu::PointFragments t = gpu::rasterize_points(pc, to_gpu(cam), gs);
+    gpu::PointFragments n = gpu::rasterize_points_naive(pc, to_gpu(cam), gs);
+    CHECK(t.idx == want.idx && t.zbuf == want.zbuf && t.dists2 == want.dists2);
+    CHECK(n.idx == want.idx && n.zbuf == want.zbuf && n.dists2 == want.dists2);
+    if (trial == 0) {  // splat_opacity -> splat_position_backward vs the reference
+      std::vector<double> da(size_t(want.slots()));
+      for (auto& x : da) x = rng.normal();
+      std::vector<ref::Vec3> gr = ref::splat_position_backward(ref::PointCloudBatch(clouds), cam, s, want, da);
+      std::vector<gpu::Vec3> gg = gpu::splat_position_backward(pc, to_gpu(cam), gs, t, da);
+      CHECK(max_rel(flat(gg), flat(gr)) < 1e-10);
+      CHECK(gpu::splat_opacity(t, s.radius) == ref::splat_opacity(want, s.radius));
+    }
+  }
+}
+
+// the reference fit step (pipeline.cpp:153-162) vs the fused GPU silhouette calls
+static void fused_silhouette_matches_reference_fit_step() {
+  ref::MeshBatch m = ref::ico_sphere(2);
+  ref::Camera cam = ref::Camera::look_from_distance(3.0, ref::ProjectionKind::Perspective, 2.0);
+  ref::RasterSettings s;
+  s.image_h = s.image_w = 64;
+  s.faces_per_pixel = 4;
+  s.blur_radius = 2e-4;
+  const double sigma = 1e-4;
+  ref::MeshFragments frag = ref::rasterize_meshes(m, cam, s);
+  std::vector<double> alpha = ref::silhouette_blend(frag, sigma);
+  gpu::SilhouetteFragments g = gpu::rasterize_silhouette(to_gpu(m), to_gpu(cam), to_gpu(s), sigma);
+  CHECK(g.pix_to_face == frag.pix_to_face);
+  CHECK(max_rel(g.alpha, alpha) < 1e-6);
+  std::vector<double> da(alpha.size());
+  for (size_t i = 0; i < da.size(); ++i) da[i] = alpha[i] - 0.5;
+  std::vector<double> dd = ref::silhouette_blend_backward(frag, sigma, da);
+  std::vector<ref::Vec3> want = ref::rasterize_backward(m, cam, s, frag, std::vector<double>(frag.zbuf.size(), 0.0),
+                                                        std::vector<double>(frag.bary.size(), 0.0), dd);
+  std::vector<gpu::Vec3> got = gpu::rasterize_silhouette_backward(to_gpu(m), to_gpu(cam), to_gpu(s), sigma, g, da);
+  CHECK(max_rel(flat(got), flat(want)) < 1e-4);
+}
+
 int main() {
   struct Case {
     const char* name;
@@ -242,7 +332,9 @@ int main() {
                {"slot_invariants", slot_invariants},
                {"blur_grows_coverage", blur_grows_coverage},
                {"backward_matches_fd_and_reference", backward_matches_fd_and_reference},
-               {"errors_mirror_reference", errors_mirror_reference}};
+               {"errors_mirror_reference", errors_mirror_reference},
+               {"points_tiled_naive_reference", points_tiled_naive_reference},
+               {"fused_silhouette_matches_reference_fit_step", fused_silhouette_matches_reference_fit_step}};
   for (auto& c : cases) {
     int before = g_fail;
     try {
