@@ -306,6 +306,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
 #ifndef DR_COMPACT
 #define DR_COMPACT 1  // compact the pairs the K-th-depth cull leaves before evaluating them
 #endif
+#ifndef DR_LIST_PREFETCH
+#define DR_LIST_PREFETCH 1
+#endif
 #ifndef DR_T_REFRESH
 #define DR_T_REFRESH 1
 #endif
@@ -731,12 +734,23 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     const bool valid_px = (lane >> 3) < vh && (lane & 7) < vw;
     double T = pos_inf();  // max over the micro-tile's pixels of the K-th candidate depth (+inf: a list not full)
     int head = 0, pending = 0, groups = 0;
+#if DR_LIST_PREFETCH
+    // the next 32 list entries are loaded while the current ones are staged and evaluated
+    int4 e_next = make_int4(-1, 0, 0, 0);
+    if (list && lane < nsrc) e_next = list[lane];
+#endif
     for (int64_t c0 = 0; c0 < nsrc; c0 += 32) {
       const int64_t ci = c0 + lane;
       uint32_t r = 0u;
       int32_t fid = -1;
       float key = 0.f;
+#if DR_LIST_PREFETCH
+      const int4 e_cur = e_next;
+      if (list && ci + 32 < nsrc) e_next = list[ci + 32];
+      if (sorted && (double)__int_as_float(__shfl_sync(0xffffffffu, e_cur.y, 0)) > T) {
+#else
       if (sorted && (double)__int_as_float(list[c0].y) > T) {
+#endif
         STAT_ADD(6, 1);
         break;
       }
@@ -744,7 +758,11 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       if (ci < nsrc) {
         int4 ib;
         if (list) {
+#if DR_LIST_PREFETCH
+          const int4 e = e_cur;
+#else
           const int4 e = list[ci];
+#endif
           fid = e.x;
           key = __int_as_float(e.y);
           ib = entry_ibbox(e);
