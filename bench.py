@@ -134,6 +134,24 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
+def ncu_issue(cfg, kernel):
+    """Issue-side utilisation of `kernel` from the newest committed ncu capture (the kernel is fp64-issue/latency
+    bound, not HBM bound): fp64 pipe active and issue-slot active fractions, or None."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_*_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                k = json.load(f)[cfg][kernel]
+            pct = lambda key: float(k[key].split()[0]) / 100.0  # noqa: E731
+            return {"fp64_pipe_active_frac": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "issue_active_frac": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "source": os.path.relpath(path, ROOT)}
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
+
+
 def ncu_traffic(cfg, kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed ncu --set full capture of this
     bench command (profiles/*/ncu_*_summary.json, newest round first); None if there is none."""
@@ -334,6 +352,7 @@ def main():
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "kernel": dom,
                 "kernel_ms": dom_ms, "kernel_share_of_step": shares[dom][0] / args.steps / max(step_ms_sum, 1e-9),
                 "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
+                "issue": ncu_issue(cfg, dom),
                 "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in shares.items()}}
 
     # end to end through the public API with host buffers (pinned), copies inside the timed region: the
