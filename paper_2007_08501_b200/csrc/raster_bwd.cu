@@ -332,13 +332,24 @@ __device__ __forceinline__ void silhouette_envelope(const double* v, V2 p, doubl
 }
 
 constexpr int kSilThreads = 128;
+constexpr int kSilStoreMaxK = 16;  // up to this K the pass-1 envelope is kept in shared memory for pass 3
 
+// kStore: pass 1 keeps each slot's distance envelope ((qq - p) * 2 sign, t, nearest edge) in shared memory, so
+// pass 3 needs no second geometry evaluation (K <= kSilStoreMaxK); otherwise pass 3 recomputes it.
+template <bool kStore>
 __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs A) {
   extern __shared__ double sil_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
-  double* P = sil_smem + (size_t)wid * 2 * K * 32;  // [K][32] prob of slot s (-1: unoccupied)
-  double* Sf = P + K * 32;                          // [K][32] prod_{s2 > s} (1 - prob)
+  const size_t per_warp = (size_t)K * 32 * (kStore ? 5 : 2) + (size_t)K * 16 * (kStore ? 2 : 1);  // doubles
+  double* P = sil_smem + (size_t)wid * per_warp;  // [K][32] prob (-1: empty)
+  double* Sf = P + K * 32;     // [K][32] prod_{s2 > s} (1 - prob)
+  double* EX = Sf + K * 32;    // [K][32] (qq - p).x * 2 sign      (kStore)
+  double* EY = EX + K * 32;    // [K][32] (qq - p).y * 2 sign      (kStore)
+  double* BT = EY + K * 32;    // [K][32] t on the nearest edge    (kStore)
+  int* BE = reinterpret_cast<int*>(BT + K * 32);  // [K][32] nearest edge (kStore)
+  // [32][K] the warp's pix_to_face block (32 consecutive pixels x K slots: one contiguous, coalesced load)
+  int32_t* FID = kStore ? BE + K * 32 : reinterpret_cast<int32_t*>(Sf + K * 32);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t HW = (int64_t)A.H * A.W;
@@ -350,22 +361,49 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
     const int rem = act ? (int)(pix % HW) : 0;
     const int i = rem / A.W, j = rem - (rem / A.W) * A.W;
     const V2 p{pixel_x(A.W, j), pixel_y(A.H, i)};
-    const int64_t* row = A.p2f + pix * K;
-    // pass 1: per-slot probabilities
+    {
+      const int64_t n = (A.npix - base < 32 ? A.npix - base : 32) * K;
+      const int64_t* src = A.p2f + base * K;
+      for (int t = lane; t < 32 * K; t += 32) {
+        const int64_t f = t < n ? __ldcs(src + t) : -1;
+        FID[t] = (f >= 0 && f < A.F) ? (int32_t)f : -1;
+      }
+      __syncwarp();
+    }
+    const int32_t* row = FID + lane * K;
+    // pass 1: per-slot probabilities (and the envelope); the next occupied slot's face_verts are loaded while
+    // the current slot is evaluated
+    double vn[9];
+    int32_t fn = act ? row[0] : -1;
+    if (fn >= 0) {
+#pragma unroll
+      for (int t = 0; t < 9; ++t) vn[t] = __ldg(A.fv + 9 * (int64_t)fn + t);
+    }
     for (int s = 0; s < K; ++s) {
       double prob = -1.0;
-      if (act) {
-        const int64_t f = row[s];
-        if (f >= 0 && f < A.F) {
-          double v[9];
+      const int32_t f = fn;
+      double v[9];
 #pragma unroll
-          for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * f + t);
+      for (int t = 0; t < 9; ++t) v[t] = vn[t];
+      fn = (act && s + 1 < K) ? row[s + 1] : -1;
+      if (fn >= 0) {
+#pragma unroll
+        for (int t = 0; t < 9; ++t) vn[t] = __ldg(A.fv + 9 * (int64_t)fn + t);
+      }
+      if (act) {
+        if (f >= 0) {
           double dist, bt, sign;
           int be;
           V2 qq;
           silhouette_envelope(v, p, dist, be, bt, qq, sign);
           const double x = -dist / A.sigma;
           prob = 1.0 / (1.0 + exp(-x));  // sigmoid, shading.cpp:9
+          if constexpr (kStore) {
+            EX[s * 32 + lane] = (qq.x - p.x) * (2.0 * sign);
+            EY[s * 32 + lane] = (qq.y - p.y) * (2.0 * sign);
+            BT[s * 32 + lane] = bt;
+            BE[s * 32 + lane] = be;
+          }
         }
       }
       P[s * 32 + lane] = prob;
@@ -384,18 +422,27 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
       int32_t fid = -1;
       double g[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       if (pr >= 0.0) {
-        const int64_t f = row[s];
-        fid = (int32_t)f;
-        double v[9];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * f + t);
-        double dist, bt, sign;
+        fid = row[s];
+        double ex, ey, bt;
         int be;
-        V2 qq;
-        silhouette_envelope(v, p, dist, be, bt, qq, sign);
+        if constexpr (kStore) {
+          ex = EX[s * 32 + lane];
+          ey = EY[s * 32 + lane];
+          bt = BT[s * 32 + lane];
+          be = BE[s * 32 + lane];
+        } else {
+          double v[9];
+#pragma unroll
+          for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)fid + t);
+          double dist, sign;
+          V2 qq;
+          silhouette_envelope(v, p, dist, be, bt, qq, sign);
+          ex = (qq.x - p.x) * (2.0 * sign);
+          ey = (qq.y - p.y) * (2.0 * sign);
+        }
         const double rest = pre * Sf[s * 32 + lane];
         const double d_out = da * rest * (-pr * (1.0 - pr) / A.sigma);
-        const V2 gg = (qq - p) * (2.0 * sign * d_out);
+        const V2 gg{ex * d_out, ey * d_out};  // (qq - p) * (2 sign d_out): the same single rounding
         const V2 g_first = gg * (1.0 - bt), g_second = gg * bt;
         const int v0 = be, v1 = be == 2 ? 0 : be + 1;
         g[2 * v0] += g_first.x;
@@ -418,25 +465,30 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
 
 cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
-  const size_t per_warp = (size_t)2 * A.K * 32 * sizeof(double);
+  const bool store = A.K <= kSilStoreMaxK;
+  const size_t per_warp = (size_t)A.K * 32 * (store ? 5 * sizeof(double) : 2 * sizeof(double)) +
+                          (size_t)A.K * 16 * sizeof(double) * (store ? 2 : 1);  // + edge ids + the p2f block
   const int max_smem = 227 * 1024;
   if (per_warp > (size_t)max_smem) return cudaErrorInvalidConfiguration;
   const int warps = (int)std::min<size_t>(kSilThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));
   const size_t smem = per_warp * warps;
-  cudaError_t e = cudaFuncSetAttribute(k_silhouette_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::max<size_t>(smem, 48 * 1024));
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_silhouette_backward, warps * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int64_t blocks = (int64_t)sms * per_sm;
-  const int64_t need = (A.npix + warps * 32 - 1) / (warps * 32);
-  if (blocks > need) blocks = need;
-  k_silhouette_backward<<<(unsigned)blocks, warps * 32, smem, st>>>(A);
-  return cudaGetLastError();
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 48 * 1024));
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int64_t need = (A.npix + warps * 32 - 1) / (warps * 32);
+    if (blocks > need) blocks = need;
+    kern<<<(unsigned)blocks, warps * 32, smem, st>>>(A);
+    return cudaGetLastError();
+  };
+  return store ? go(k_silhouette_backward<true>) : go(k_silhouette_backward<false>);
 }
 
 template <typename InT>

@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_bins(const int* __restric
   const int64_t per = (n + kScanThreads - 1) / kScanThreads;
   const int64_t lo = min(n, (int64_t)t * per), hi = min(n, lo + per);
   int64_t sum = 0;
+#pragma unroll 8
   for (int64_t i = lo; i < hi; ++i) sum += counts[i];
   part[t] = sum;
   __syncthreads();
@@ -235,13 +236,32 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
                                                             const int4* __restrict__ ibbox, int64_t nbins_total,
                                                             int64_t pool, int cap) {
   __shared__ unsigned long long s_static[kDyn ? 1 : MAXN];
+  __shared__ unsigned sel_mask;
   extern __shared__ unsigned long long s_dyn[];
   unsigned long long* s = kDyn ? s_dyn : s_static;
-  for (int64_t bin = blockIdx.x; bin < nbins_total; bin += gridDim.x) {
+  // CTA b owns bins b, b + grid, b + 2 grid, ... (round robin: adjacent large bins land on different CTAs);
+  // warp 0 reads 32 of its counts at once and keeps the ones in this instantiation's size range, so a CTA does
+  // not walk the (mostly out-of-range) bins one by one
+  const int64_t stride = gridDim.x;
+  for (int64_t k0 = 0; (int64_t)blockIdx.x + k0 * stride < nbins_total; k0 += 32) {
+    if (threadIdx.x < 32) {
+      const int64_t bin = (int64_t)blockIdx.x + (k0 + threadIdx.x) * stride;
+      bool in = false;
+      if (bin < nbins_total) {
+        const int c = counts[bin];
+        in = c > MINN && c <= MAXN && bin_fits(off[bin], c, pool, cap);  // spill bins are never read as lists
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (threadIdx.x == 0) sel_mask = m;
+    }
+    __syncthreads();
+    unsigned todo = sel_mask;
+    __syncthreads();
+  while (todo) {
+    const int64_t bin = (int64_t)blockIdx.x + (k0 + __ffs(todo) - 1) * stride;
+    todo &= todo - 1;
     const int c = counts[bin];
-    if (c <= MINN || c > MAXN) continue;
     const int64_t o = off[bin];
-    if (!bin_fits(o, c, pool, cap)) continue;  // spill path: unsorted, never read as a list
     int4* L = entries + o;
     int P = 1;
     while (P < c) P <<= 1;
@@ -275,6 +295,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
       L[i] = make_bin_entry(f, float_from_order_bits((uint32_t)(e >> 32)), __ldg(ibbox + f));
     }
     __syncthreads();
+  }
   }
 }
 
