@@ -360,6 +360,7 @@ struct WarpSmem {
   int32_t* bcnt;    // [32]
   double* pxy;      // [12] pixel-centre NDC coordinates of the micro-tile: x of its 8 columns, y of its 4 rows
   uint32_t* pairq;  // [64] queued (ring slot << 5 | pixel) pairs awaiting evaluation
+  int32_t* tcnt;    // [32] entries held by each pixel's list (shared-memory list path, KMAX == 0)
 
   __device__ __forceinline__ double get(int f, int k) const { return d[f * kRing + k]; }
   __device__ __forceinline__ void put(int f, int k, double v) const { d[f * kRing + k] = v; }
@@ -414,12 +415,14 @@ struct WarpSmem {
 #endif
 constexpr int kBuf = DR_KBUF;  // buffered candidates per pixel before the owner lane merges them into its list
 
-// per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt | pairq
+// per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt | pairq |
+// tcnt
 __host__ __device__ constexpr size_t warp_smem_bytes(int K) {
   return (size_t)kNF * kRing * sizeof(double) + (size_t)K * 32 * sizeof(double) + (size_t)kBuf * 32 * sizeof(double) +
          12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) + (size_t)K * 32 * sizeof(int32_t) +
          (size_t)kBuf * 32 * sizeof(int32_t) + (size_t)kRing * (sizeof(uint32_t) + sizeof(float)) +
-         32 * sizeof(int32_t) + 64 * sizeof(uint32_t) + 8;  // + pad keeps the next warp's base 8-byte aligned
+         32 * sizeof(int32_t) + 64 * sizeof(uint32_t) + 32 * sizeof(int32_t) +
+         8;  // + pad keeps the next warp's base 8-byte aligned
 }
 
 // Rectangle of the micro-tile (rows i0..i0+3, cols j0..j0+7, limited to vh x vw existing pixels) covered by
@@ -479,9 +482,15 @@ __device__ __forceinline__ double silhouette_prob(const double* v, double px, do
 }
 
 // Insert (zc, f) into pixel p's sorted list (column p of [K][32]) in shared memory: shifting loop.
+// kCounted (the shared-memory list path, KMAX == 0): ws.tcnt[p] = entries held, so a list that is not full grows
+// at its end instead of shifting +inf padding down from slot K-1 (for K = 50 that padding walk was most of the
+// fine stage's time). The register path (KMAX > 0, K <= 8) does not maintain tcnt and walks from K-1.
+template <bool kCounted>
 __device__ __forceinline__ void list_insert(const WarpSmem& ws, int K, int p, double zc, int32_t f) {
-  if (cand_less(zc, f, ws.tz[(K - 1) * 32 + p], ws.tid[(K - 1) * 32 + p])) {
-    int s = K - 1;
+  const int n = kCounted ? ws.tcnt[p] : K;
+  if (n < K || cand_less(zc, f, ws.tz[(K - 1) * 32 + p], ws.tid[(K - 1) * 32 + p])) {
+    int s = n < K ? n : K - 1;
+    if (kCounted && n < K) ws.tcnt[p] = n + 1;
     while (s > 0) {
       const double zp = ws.tz[(s - 1) * 32 + p];
       const int32_t ip = ws.tid[(s - 1) * 32 + p];
@@ -512,7 +521,7 @@ __device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane)
   const int n = ws.bcnt[lane];
   if (n > 0) {
     if constexpr (KMAX == 0) {
-      for (int c = 0; c < n; ++c) list_insert(ws, K, lane, ws.bz[c * 32 + lane], ws.bid[c * 32 + lane]);
+      for (int c = 0; c < n; ++c) list_insert<true>(ws, K, lane, ws.bz[c * 32 + lane], ws.bid[c * 32 + lane]);
     } else {
       double z[KMAX];
       int32_t id[KMAX];
@@ -595,7 +604,7 @@ __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSm
     // more than kBuf candidates for one pixel in one step (rare): insert the excess directly, one at a time
     const int extra = __reduce_max_sync(0xffffffffu, pass ? n_same - kBuf : 0);
     for (int rr = 0; rr < extra; ++rr) {
-      if (pass && rank == kBuf + rr) list_insert(ws, K, p, res.z, f);
+      if (pass && rank == kBuf + rr) list_insert<KMAX == 0>(ws, K, p, res.z, f);
       __syncwarp();
     }
   }
@@ -704,6 +713,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     ws.fkey = reinterpret_cast<float*>(ws.rect + kRing);
     ws.bcnt = reinterpret_cast<int32_t*>(ws.fkey + kRing);
     ws.pairq = reinterpret_cast<uint32_t*>(ws.bcnt + 32);
+    ws.tcnt = reinterpret_cast<int32_t*>(ws.pairq + 64);
   }
   const int nbins = A.nbx * A.nby;
   const int mtx = (A.bs + 7) >> 3, mty = (A.bs + 3) >> 2;  // micro-tiles per bin row / column
@@ -748,6 +758,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       ws.tid[s * 32 + lane] = INT_MAX;
     }
     ws.bcnt[lane] = 0;
+    ws.tcnt[lane] = 0;
     if (lane < 8) ws.pxy[lane] = pixel_x(A.W, mj0 + lane);               // camera.cpp:100-102, once per
     else if (lane < 12) ws.pxy[lane] = pixel_y(A.H, mi0 + (lane - 8));   // micro-tile instead of per pair
     __syncwarp();
