@@ -186,6 +186,32 @@ int dr_rasterize_silhouette_bwd(const double* face_verts, const int64_t* mesh_to
                                 double sigma, const int64_t* pix_to_face, const float* grad_alpha,
                                 double* grad_face_verts, dr_stream_t stream);
 
+/* ---- fused fragment consumer: softmax render ----
+ * The reference's differentiable softmax render (grad.cpp:177-209): rasterize_meshes -> interpolate_face_attributes
+ * of per-vertex colours with the clamped barycentrics (shading.cpp:11-32) -> softmax_blend (shading.cpp:123-160).
+ * dr_rasterize_softmax_fwd writes image [N,H,W,3] fp32 (and pix_to_face, may be NULL); no fragment payload is
+ * materialised. dr_rasterize_softmax_bwd chains softmax_blend_backward (shading.cpp:162-230) ->
+ * interpolate_face_attributes_backward (shading.cpp:35-73) -> rasterize_backward (mesh_raster.cpp:329-378):
+ * grad_face_verts [F,3,3] (overwritten on the batch's face ranges) and grad_vert_colors [V,3] (overwritten).
+ * faces [F,3] = MeshBatch::faces_packed() global vertex ids (must be valid: they are not re-checked here);
+ * vert_colors [V,3] fp64. faces_per_pixel <= 64 for the backward. */
+typedef struct dr_blend_params {
+  double sigma;          /* BlendParams.sigma (shading.hpp:14), > 0 */
+  double gamma;          /* BlendParams.gamma (shading.hpp:15), > 0 */
+  double background[3];  /* BlendParams.background_color */
+  double znear, zfar;    /* Camera.znear / zfar (softmax_blend's depth normalisation) */
+} dr_blend_params;
+int dr_rasterize_softmax_fwd(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                             const int64_t* num_faces_per_mesh, int64_t N, int64_t F, const dr_raster_settings* s,
+                             const dr_blend_params* blend, const double* vert_colors, const int64_t* faces, int64_t V,
+                             int64_t* pix_to_face, float* image, void* workspace, size_t workspace_bytes,
+                             dr_stream_t stream);
+int dr_rasterize_softmax_bwd(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                             const int64_t* num_faces_per_mesh, int64_t N, int64_t F, const dr_raster_settings* s,
+                             const dr_blend_params* blend, const double* vert_colors, const int64_t* faces, int64_t V,
+                             const int64_t* pix_to_face, const float* grad_image, double* grad_face_verts,
+                             double* grad_vert_colors, dr_stream_t stream);
+
 /* ---- point rasterizer ----
  * Replaces dr::rasterize_points / rasterize_points_naive (point_render.hpp:33-36, point_render.cpp:82-155) on the
  * same boundary as the meshes: points_ndc [P,3] fp64 = world_to_ndc (x_ndc, y_ndc, z_view) of the packed points

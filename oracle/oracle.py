@@ -225,6 +225,8 @@ class RefLib:
         L.ref_rasterize_points.argtypes = [_dp, _i64p, C.c_int32, _dp, _i32p, C.c_double, C.c_int, _i64p, _dp, _dp]
         L.ref_splat_position_backward.argtypes = [_dp, _i64p, C.c_int32, _dp, _i32p, C.c_double, _i64p, _dp, _dp,
                                                   _dp, _dp]
+        L.ref_softmax_render.argtypes = [C.c_void_p, _dp, _i32p, C.c_double, _dp, _dp, _dp, _i64p]
+        L.ref_softmax_render_backward.argtypes = [C.c_void_p, _dp, _i32p, C.c_double, _dp, _dp, _dp, _dp, _dp]
         L.ref_silhouette_blend.argtypes = [_i64p, _dp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _dp]
         L.ref_silhouette_blend_backward.argtypes = [_i64p, _dp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                                     C.c_double, _dp, _dp]
@@ -296,6 +298,34 @@ class RefLib:
     def point_triangle_dist2(self, p, a, b, c) -> float:
         arr = [np.asarray(x, np.float64) for x in (p, a, b, c)]
         return self.lib.ref_point_triangle_dist2(*[_p(x, _dp) for x in arr])
+
+    def softmax_render(self, batch: RefBatch, cam_packed, H, W, K, blur, vert_colors, sigma, gamma, bg=(0, 0, 0),
+                       tile=16):
+        """grad.cpp:181-193: rasterize_meshes -> interpolate_face_attributes -> softmax_blend -> image [n,H,W,3]."""
+        cam = np.ascontiguousarray(cam_packed, np.float64)
+        si = np.array([H, W, K, tile], np.int32)
+        vc = np.ascontiguousarray(vert_colors, np.float64)
+        bl = np.array([sigma, gamma, *bg], np.float64)
+        img = np.empty((batch.n, H, W, 3))
+        p2f = np.empty((batch.n, H, W, K), np.int64)
+        if self.lib.ref_softmax_render(batch.h, _p(cam, _dp), _p(si, _i32p), blur, _p(vc, _dp), _p(bl, _dp),
+                                       _p(img, _dp), _p(p2f, _i64p)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return img, p2f
+
+    def softmax_render_backward(self, batch: RefBatch, cam_packed, H, W, K, blur, vert_colors, sigma, gamma, d_image,
+                                bg=(0, 0, 0), tile=16):
+        """grad.cpp:195-206 vjp: (world d_verts [V,3], d_vert_colors [V,3])."""
+        cam = np.ascontiguousarray(cam_packed, np.float64)
+        si = np.array([H, W, K, tile], np.int32)
+        vc = np.ascontiguousarray(vert_colors, np.float64)
+        bl = np.array([sigma, gamma, *bg], np.float64)
+        di = np.ascontiguousarray(d_image, np.float64)
+        dv, dc = np.empty((batch.V, 3)), np.empty((batch.V, 3))
+        if self.lib.ref_softmax_render_backward(batch.h, _p(cam, _dp), _p(si, _i32p), blur, _p(vc, _dp), _p(bl, _dp),
+                                                _p(di, _dp), _p(dv, _dp), _p(dc, _dp)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return dv, dc
 
     def rasterize_points(self, points, counts, cam_packed, H, W, K, radius, tile=16, naive=False):
         """dr::rasterize_points / _naive (point_render.hpp:33-36) on world points [P,3] split by counts."""

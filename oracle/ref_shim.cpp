@@ -9,6 +9,7 @@
 //   dr::world_to_ndc                                (camera.hpp:50)
 //   dr::ico_sphere / cube / synthetic_batch         (templates.hpp:12-24)
 //   dr::silhouette_blend / silhouette_blend_backward (shading.hpp:37-41)
+//   the softmax render op of grad.cpp:177-209 (interpolate_face_attributes + softmax_blend and their backwards)
 //   dr::rasterize_points / _naive, splat_position_backward (point_render.hpp:33-36, 66-68)
 // Errors are caught and reported through ref_last_error() (the reference throws).
 #include <cstdint>
@@ -209,6 +210,69 @@ int ref_silhouette_blend_backward(const int64_t* p2f, const double* dists, int32
     std::vector<double> da(d_alpha, d_alpha + ns / size_t(k));
     std::vector<double> dd = dr::silhouette_blend_backward(f, sigma, da);
     std::memcpy(d_dists, dd.data(), dd.size() * sizeof(double));
+  });
+}
+
+// ---- softmax render (grad.cpp:177-209 composed from the reference's own functions) ----
+// vert_colors [V,3]; blend = [sigma, gamma, bg_r, bg_g, bg_b]; image [n*H*W*3]; p2f [S]
+int ref_softmax_render(void* h, const double* cam, const int32_t* si, double blur, const double* vert_colors,
+                       const double* blend, double* image, int64_t* p2f) {
+  return guarded([&] {
+    auto* m = static_cast<dr::MeshBatch*>(h);
+    dr::Camera c = make_camera(cam);
+    dr::RasterSettings s = make_settings(si, blur);
+    dr::BlendParams p;
+    p.sigma = blend[0];
+    p.gamma = blend[1];
+    p.background_color = {blend[2], blend[3], blend[4]};
+    dr::MeshFragments frag = dr::rasterize_meshes(*m, c, s);
+    std::vector<double> attr(vert_colors, vert_colors + 3 * m->total_verts());
+    std::vector<double> interp = dr::interpolate_face_attributes(*m, frag, attr, 3);
+    std::vector<dr::Vec3> colors(size_t(frag.slots()));
+    for (size_t i = 0; i < colors.size(); ++i) colors[i] = {interp[3 * i], interp[3 * i + 1], interp[3 * i + 2]};
+    std::vector<dr::Vec3> img = dr::softmax_blend(frag, colors, p, c.znear, c.zfar);
+    for (size_t i = 0; i < img.size(); ++i) {
+      image[3 * i] = img[i].x;
+      image[3 * i + 1] = img[i].y;
+      image[3 * i + 2] = img[i].z;
+    }
+    std::memcpy(p2f, frag.pix_to_face.data(), frag.pix_to_face.size() * sizeof(int64_t));
+  });
+}
+// vjp: d_image [n*H*W*3] -> world d_verts [V,3] and d_vert_colors [V,3]
+int ref_softmax_render_backward(void* h, const double* cam, const int32_t* si, double blur, const double* vert_colors,
+                                const double* blend, const double* d_image, double* d_verts, double* d_colors) {
+  return guarded([&] {
+    auto* m = static_cast<dr::MeshBatch*>(h);
+    dr::Camera c = make_camera(cam);
+    dr::RasterSettings s = make_settings(si, blur);
+    dr::BlendParams p;
+    p.sigma = blend[0];
+    p.gamma = blend[1];
+    p.background_color = {blend[2], blend[3], blend[4]};
+    dr::MeshFragments frag = dr::rasterize_meshes(*m, c, s);
+    std::vector<double> attr(vert_colors, vert_colors + 3 * m->total_verts());
+    std::vector<double> interp = dr::interpolate_face_attributes(*m, frag, attr, 3);
+    std::vector<dr::Vec3> colors(size_t(frag.slots()));
+    for (size_t i = 0; i < colors.size(); ++i) colors[i] = {interp[3 * i], interp[3 * i + 1], interp[3 * i + 2]};
+    const size_t npix = size_t(frag.slots() / frag.k);
+    std::vector<dr::Vec3> dimg(npix);
+    for (size_t i = 0; i < npix; ++i) dimg[i] = {d_image[3 * i], d_image[3 * i + 1], d_image[3 * i + 2]};
+    dr::SoftmaxBlendGrads bg = dr::softmax_blend_backward(frag, colors, p, c.znear, c.zfar, dimg);
+    std::vector<double> flat_dc(3 * bg.d_colors.size());
+    for (size_t i = 0; i < bg.d_colors.size(); ++i) {
+      flat_dc[3 * i] = bg.d_colors[i].x;
+      flat_dc[3 * i + 1] = bg.d_colors[i].y;
+      flat_dc[3 * i + 2] = bg.d_colors[i].z;
+    }
+    dr::InterpolateGrads ig = dr::interpolate_face_attributes_backward(*m, frag, attr, 3, flat_dc);
+    std::vector<dr::Vec3> g = dr::rasterize_backward(*m, c, s, frag, bg.d_zbuf, ig.d_bary, bg.d_dists);
+    for (size_t i = 0; i < g.size(); ++i) {
+      d_verts[3 * i] = g[i].x;
+      d_verts[3 * i + 1] = g[i].y;
+      d_verts[3 * i + 2] = g[i].z;
+    }
+    std::memcpy(d_colors, ig.d_attrs.data(), ig.d_attrs.size() * sizeof(double));
   });
 }
 

@@ -3,10 +3,12 @@
 Public surface (mirrors /root/reference/proj/include/dr/mesh_raster.hpp on the north-star boundary):
     RasterSettings, rasterize_meshes, rasterize_meshes_naive, rasterize_meshes_backward, RasterizeMeshes
     rasterize_silhouette, rasterize_silhouette_backward, RasterizeSilhouette (fused silhouette_blend, shading.cpp)
+    rasterize_softmax, rasterize_softmax_backward, RasterizeSoftmax, BlendParams (fused softmax render, grad.cpp)
     rasterize_points, rasterize_points_naive, rasterize_points_backward, PointRasterSettings (point_render.cpp)
 Input generators and the host camera transform live in ``scenes``; mesh sharding across GPUs in ``shard``.
 """
 from .raster import (  # noqa: F401
+    BlendParams,
     CudaError,
     KernelTimer,
     MeshIndexError,
@@ -14,6 +16,7 @@ from .raster import (  # noqa: F401
     RasterError,
     RasterizeMeshes,
     RasterizeSilhouette,
+    RasterizeSoftmax,
     RasterSettings,
     ShapeError,
     UsageError,
@@ -25,6 +28,8 @@ from .raster import (  # noqa: F401
     rasterize_meshes_naive,
     rasterize_silhouette,
     rasterize_silhouette_backward,
+    rasterize_softmax,
+    rasterize_softmax_backward,
     face_verts_backward,
     workspace_bytes,
     world_to_face_verts,

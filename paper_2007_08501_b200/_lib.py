@@ -26,6 +26,8 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_meshes_bwd_hr",
     "dr_rasterize_silhouette_fwd",
     "dr_rasterize_silhouette_bwd",
+    "dr_rasterize_softmax_fwd",
+    "dr_rasterize_softmax_bwd",
     "dr_point_raster_settings_default",
     "dr_rasterize_points_workspace_bytes",
     "dr_rasterize_points_fwd",
@@ -67,6 +69,13 @@ class DrPointRasterSettings(C.Structure):
         ("image_h", C.c_int32), ("image_w", C.c_int32), ("points_per_pixel", C.c_int32), ("bin_size", C.c_int32),
         ("radius", C.c_double), ("znear", C.c_double), ("clip_nonpositive_z", C.c_uint8), ("_reserved", C.c_uint8 * 7),
     ]
+
+
+class DrBlendParams(C.Structure):
+    """dr_blend_params (include/dr_raster.h) = BlendParams (shading.hpp:13-17) + Camera znear/zfar."""
+
+    _fields_ = [("sigma", C.c_double), ("gamma", C.c_double), ("background", C.c_double * 3),
+                ("znear", C.c_double), ("zfar", C.c_double)]
 
 
 class DrCamera(C.Structure):
@@ -127,6 +136,13 @@ def load() -> C.CDLL:
                                               C.c_size_t, _vp]
     L.dr_rasterize_silhouette_bwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp,
                                               _vp]
+    bpp = C.POINTER(DrBlendParams)
+    L.dr_rasterize_softmax_fwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, bpp, _vp, _vp, C.c_int64, _vp, _vp,
+                                           _vp, C.c_size_t, _vp]
+    L.dr_rasterize_softmax_bwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, bpp, _vp, _vp, C.c_int64, _vp, _vp,
+                                           _vp, _vp, _vp]
+    L.dr_rasterize_softmax_fwd.restype = C.c_int
+    L.dr_rasterize_softmax_bwd.restype = C.c_int
     pp = C.POINTER(DrPointRasterSettings)
     L.dr_point_raster_settings_default.argtypes = [pp]
     L.dr_rasterize_points_workspace_bytes.argtypes = [C.c_int64, C.c_int64, pp]

@@ -45,10 +45,11 @@ int cuda_fail(cudaError_t e, const char* where) {
 // ---- optional per-kernel timing ring ----
 const char* kKernelNames[] = {"k_face_setup",  "k_bin_faces",   "k_fine",        "k_backward",
                               "memset",        "k_camera",      "k_batching",    "k_sort_bins",
-                              "k_silhouette_backward", "k_point_setup", "k_points_fine", "k_points_backward"};
+                              "k_silhouette_backward", "k_point_setup", "k_points_fine", "k_points_backward",
+                              "k_softmax_backward"};
 enum {
   KN_SETUP = 0, KN_BIN = 1, KN_FINE = 2, KN_BWD = 3, KN_MEMSET = 4, KN_CAMERA = 5, KN_BATCH = 6, KN_SORT = 7,
-  KN_SIL_BWD = 8, KN_PT_SETUP = 9, KN_PT_FINE = 10, KN_PT_BWD = 11
+  KN_SIL_BWD = 8, KN_PT_SETUP = 9, KN_PT_FINE = 10, KN_PT_BWD = 11, KN_SOFT_BWD = 12
 };
 struct ProfEntry {
   int kernel;
@@ -208,12 +209,12 @@ template <typename OutT>
 int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
              const dr_raster_settings* s, int64_t* p2f, OutT* zbuf, OutT* bary, OutT* dists, void* ws, size_t ws_bytes,
              cudaStream_t st, const int64_t* host_first = nullptr, const int64_t* host_num = nullptr,
-             OutT* alpha = nullptr, double sigma = 0.0) {
+             OutT* alpha = nullptr, double sigma = 0.0, OutT* image = nullptr, const drb::BlendArgs* blend = nullptr) {
   Plan p;
   int rc = make_plan(N, F, s, p);
   if (rc) return rc;
   if (!first || !num || (F > 0 && !fv)) return fail(DR_ERR_USAGE, "null input pointer");
-  if (alpha ? false : (!p2f || !zbuf || !bary || !dists)) return fail(DR_ERR_USAGE, "null output pointer");
+  if ((alpha || image) ? false : (!p2f || !zbuf || !bary || !dists)) return fail(DR_ERR_USAGE, "null output pointer");
   if (alpha && !(sigma > 0.0)) return fail(DR_ERR_RANGE, "silhouette sigma must be > 0 (got %g)", sigma);
   if (!ws || ws_bytes < p.total)
     return fail(DR_ERR_OOM, "workspace too small: %zu bytes given, %zu needed", ws_bytes, p.total);
@@ -308,6 +309,8 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   A.dists = dists;
   A.alpha = alpha;
   A.sigma = sigma;
+  A.image = image;
+  if (blend) A.blend = *blend;
   cudaError_t e = cudaMemsetAsync(A.work_counter, 0, sizeof(unsigned long long), st);
   if (e == cudaSuccess) {
     ProfScope ps(st, KN_FINE);
@@ -560,9 +563,94 @@ int points_bwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   return DR_OK;
 }
 
+drb::BlendArgs blend_args(const dr_blend_params* bp, const double* vert_colors, const int64_t* faces, int64_t V) {
+  drb::BlendArgs b;
+  b.vert_colors = vert_colors;
+  b.faces = faces;
+  b.V = V;
+  b.sigma = bp->sigma;
+  b.gamma = bp->gamma;
+  for (int c = 0; c < 3; ++c) b.background[c] = bp->background[c];
+  b.znear = bp->znear;
+  b.zfar = bp->zfar;
+  return b;
+}
+
+int check_blend(const dr_blend_params* bp, const double* vert_colors, const int64_t* faces, int64_t V, int64_t F) {
+  if (!bp) return fail(DR_ERR_USAGE, "blend params pointer is null");
+  if (!(bp->sigma > 0.0) || !(bp->gamma > 0.0))
+    return fail(DR_ERR_RANGE, "blend sigma/gamma must be > 0 (got %g, %g)", bp->sigma, bp->gamma);
+  if (!(bp->zfar > bp->znear)) return fail(DR_ERR_RANGE, "zfar (%g) must exceed znear (%g)", bp->zfar, bp->znear);
+  if (V < 0) return fail(DR_ERR_SHAPE, "negative vertex count");
+  if (F > 0 && (!vert_colors || !faces)) return fail(DR_ERR_USAGE, "null vertex colours / faces");
+  return DR_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int dr_rasterize_softmax_fwd(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                             const dr_raster_settings* s, const dr_blend_params* bp, const double* vert_colors,
+                             const int64_t* faces, int64_t V, int64_t* p2f, float* image, void* ws, size_t ws_bytes,
+                             dr_stream_t stream) {
+  if (!image) return fail(DR_ERR_USAGE, "image is null");
+  int rc = check_blend(bp, vert_colors, faces, V, F);
+  if (rc) return rc;
+  const drb::BlendArgs b = blend_args(bp, vert_colors, faces, V);
+  return fwd_impl<float>(fv, first, num, N, F, s, p2f, nullptr, nullptr, nullptr, ws, ws_bytes,
+                         reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, nullptr, 0.0, image, &b);
+}
+
+int dr_rasterize_softmax_bwd(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                             const dr_raster_settings* s, const dr_blend_params* bp, const double* vert_colors,
+                             const int64_t* faces, int64_t V, const int64_t* p2f, const float* grad_image,
+                             double* grad_face_verts, double* grad_vert_colors, dr_stream_t stream) {
+  Plan p;
+  int rc = make_plan(N, F, s, p);
+  if (rc) return rc;
+  rc = check_blend(bp, vert_colors, faces, V, F);
+  if (rc) return rc;
+  if (!first || !num || !p2f || !grad_image || (F > 0 && (!fv || !grad_face_verts)) || (V > 0 && !grad_vert_colors))
+    return fail(DR_ERR_USAGE, "null input/output pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int64_t mx;
+  std::vector<int64_t> ranges;
+  rc = read_ranges(first, num, N, F, st, &mx, &ranges);
+  if (rc) return rc;
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_MEMSET);
+    e = zero_rows(grad_face_verts, 9, ranges, N, st);
+    if (e == cudaSuccess && V > 0) e = cudaMemsetAsync(grad_vert_colors, 0, sizeof(double) * 3 * (size_t)V, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "zeroing gradients");
+  if (F == 0) return DR_OK;
+  drb::SoftBwdArgs A;
+  A.fv = fv;
+  A.p2f = p2f;
+  A.d_image = grad_image;
+  A.grad = grad_face_verts;
+  A.grad_colors = grad_vert_colors;
+  A.npix = N * (int64_t)p.H * p.W;
+  A.F = F;
+  A.H = p.H;
+  A.W = p.W;
+  A.K = p.K;
+  A.persp = s->perspective_correct != 0;
+  A.clip = s->clip_barycentric_coords != 0;
+  A.blur = s->blur_radius;
+  A.znear = s->znear;
+  A.blend = blend_args(bp, vert_colors, faces, V);
+  {
+    ProfScope ps(st, KN_SOFT_BWD);
+    e = drb::launch_softmax_backward(A, st);
+  }
+  if (e == cudaErrorInvalidConfiguration)
+    return fail(DR_ERR_RANGE, "faces_per_pixel=%d too large for the fused softmax backward (<= 64)", p.K);
+  if (e != cudaSuccess) return cuda_fail(e, "rasterize_softmax backward");
+  return DR_OK;
+}
 
 void dr_point_raster_settings_default(dr_point_raster_settings* s) {
   if (!s) return;

@@ -491,6 +491,220 @@ cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
   return store ? go(k_silhouette_backward<true>) : go(k_silhouette_backward<false>);
 }
 
+// ------------------------------------------------------------------------------------------------
+// Fused softmax render backward: the reference's differentiable softmax render (grad.cpp:177-209) is
+// rasterize_meshes -> interpolate_face_attributes(vertex colours) -> softmax_blend; its vjp chains
+// softmax_blend_backward (shading.cpp:162-230) -> interpolate_face_attributes_backward (shading.cpp:35-73) ->
+// rasterize_backward (MR:329-378). Here one lane per pixel walks its K slots: pass 1 re-evaluates each slot
+// EXACTLY (the forward's depth, clamped barycentrics and distance, bit for bit — so depth ties pick the same
+// argmax as the reference) and keeps inverse depth, opacity and interpolated colour in shared memory; passes 2-3
+// form the softmax weights and the per-pixel mean term; pass 4 produces d_colors / d_dists / d_zbuf per slot
+// (plus the zinv_max term on the argmax slot), d_bary_i = d_color . colour(v_i), the vertex-colour cotangent
+// and the K3 per-slot chain, summed per face across the warp before the fp64 atomics.
+
+constexpr int kSoftThreads = 128;
+constexpr int kSoftMaxK = 64;
+
+__device__ __forceinline__ double blend_zinv_b(double z, const BlendArgs& bl, bool& clamped) {
+  clamped = z < bl.znear || z > bl.zfar;  // shading.cpp:199
+  const double zc = z < bl.znear ? bl.znear : (bl.zfar < z ? bl.zfar : z);
+  return (bl.zfar - zc) / (bl.zfar - bl.znear);
+}
+
+__global__ void __launch_bounds__(kSoftThreads) k_softmax_backward(SoftBwdArgs A) {
+  extern __shared__ double soft_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int K = A.K;
+  const size_t per_warp = (size_t)K * 32 * 6 + (size_t)K * 16;  // doubles
+  double* ZI = soft_smem + (size_t)wid * per_warp;  // [K][32] zinv (-1: empty slot; +2: clamped)
+  double* PR = ZI + K * 32;                         // [K][32] prob
+  double* WT = PR + K * 32;                         // [K][32] softmax weight
+  double* C0 = WT + K * 32;                         // [K][32] interpolated colour
+  double* C1 = C0 + K * 32;
+  double* C2 = C1 + K * 32;
+  int32_t* FID = reinterpret_cast<int32_t*>(C2 + K * 32);  // [32][K] the warp's pix_to_face block
+  BwdArgs<double> BA;  // the K3 per-slot chain's flags
+  BA.persp = A.persp;
+  BA.clip = A.clip;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t HW = (int64_t)A.H * A.W;
+  const double zrange = A.blend.zfar - A.blend.znear;
+  for (int64_t base = warp * 32; base < A.npix; base += nwarps * 32) {
+    const int64_t pix = base + lane;
+    double dimg[3] = {0.0, 0.0, 0.0};
+    if (pix < A.npix) {
+      dimg[0] = (double)A.d_image[3 * pix];
+      dimg[1] = (double)A.d_image[3 * pix + 1];
+      dimg[2] = (double)A.d_image[3 * pix + 2];
+    }
+    {
+      const int64_t n = (A.npix - base < 32 ? A.npix - base : 32) * K;
+      const int64_t* src = A.p2f + base * K;
+      for (int t = lane; t < 32 * K; t += 32) {
+        const int64_t f = t < n ? __ldcs(src + t) : -1;
+        FID[t] = (f >= 0 && f < A.F) ? (int32_t)f : -1;
+      }
+      __syncwarp();
+    }
+    const int32_t* row = FID + lane * K;
+    const int rem = pix < A.npix ? (int)(pix % HW) : 0;
+    const int i = rem / A.W, j = rem - (rem / A.W) * A.W;
+    const V2 p{pixel_x(A.W, j), pixel_y(A.H, i)};
+    // pass 1: exact slot evaluation, zinv_max / argmax (shading.cpp:185-197)
+    double zinv_max = -1.0;
+    int argmax = -1;
+    bool any = false;
+    for (int s = 0; s < K; ++s) {
+      const int32_t f = pix < A.npix ? row[s] : -1;
+      double zi = -1.0;
+      if (f >= 0) {
+        any = true;
+        double v[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)f + t);
+        const FaceGeom g = make_face_geom(v);
+        PixelFaceResult r;
+        eval_pixel_face<true, true>(p, g, A.blur, A.znear, A.persp, A.clip, r);  // the forward's exact bits
+        bool clamped;
+        zi = blend_zinv_b(r.z, A.blend, clamped);
+        if (zi > zinv_max) {
+          zinv_max = zi;
+          argmax = s;
+        }
+        double c[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {  // interpolate_face_attributes (shading.cpp:21-29)
+          const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)f + q];
+          c[0] += r.bary[q] * __ldg(a);
+          c[1] += r.bary[q] * __ldg(a + 1);
+          c[2] += r.bary[q] * __ldg(a + 2);
+        }
+        C0[s * 32 + lane] = c[0];
+        C1[s * 32 + lane] = c[1];
+        C2[s * 32 + lane] = c[2];
+        PR[s * 32 + lane] = 1.0 / (1.0 + exp(r.dist / A.blend.sigma));  // sigmoid(-dists / sigma)
+        if (clamped) zi += 2.0;
+      }
+      ZI[s * 32 + lane] = zi;
+    }
+    // pass 2: weights and their sum (shading.cpp:202-209)
+    double wsum = 0.0;
+    for (int s = 0; s < K; ++s) {
+      double zi = ZI[s * 32 + lane];
+      if (zi < -0.5) continue;
+      if (zi > 1.5) zi -= 2.0;
+      const double w = PR[s * 32 + lane] * exp((zi - zinv_max) / A.blend.gamma);
+      WT[s * 32 + lane] = w;
+      wsum += w;
+    }
+    // pass 3: the mean term (shading.cpp:218-222; identical for every slot, computed once in the same order)
+    double mean_term = 0.0;
+    for (int s = 0; s < K; ++s) {
+      if (ZI[s * 32 + lane] < -0.5) continue;
+      const double dc = dimg[0] * C0[s * 32 + lane] + dimg[1] * C1[s * 32 + lane] + dimg[2] * C2[s * 32 + lane];
+      mean_term += dc * (WT[s * 32 + lane] / wsum);
+    }
+    // d_zinv_max (shading.cpp:228) before the per-slot pass that adds it to the argmax slot
+    double d_zinv_max = 0.0;
+    for (int s = 0; s < K; ++s) {
+      if (ZI[s * 32 + lane] < -0.5) continue;
+      const double w = WT[s * 32 + lane];
+      const double d_what = dimg[0] * C0[s * 32 + lane] + dimg[1] * C1[s * 32 + lane] + dimg[2] * C2[s * 32 + lane];
+      const double d_w = (d_what - mean_term) / wsum;
+      d_zinv_max += -d_w * w / A.blend.gamma;
+    }
+    // pass 4: per-slot cotangents -> colours, barycentrics, the K3 chain
+    for (int s = 0; s < K; ++s) {
+      const double zis = (pix < A.npix && any) ? ZI[s * 32 + lane] : -1.0;
+      int32_t fid = -1;
+      double g[9], gc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) g[k] = gc[k] = 0.0;
+      if (zis >= -0.5) {
+        fid = row[s];
+        const bool clamped = zis > 1.5;
+        const double w = WT[s * 32 + lane], pr = PR[s * 32 + lane];
+        const double c[3] = {C0[s * 32 + lane], C1[s * 32 + lane], C2[s * 32 + lane]};
+        const double what = w / wsum;
+        const double d_col[3] = {dimg[0] * what, dimg[1] * what, dimg[2] * what};  // g.d_colors = dimg * what
+        const double d_what = dimg[0] * c[0] + dimg[1] * c[1] + dimg[2] * c[2];
+        const double d_w = (d_what - mean_term) / wsum;
+        const double d_prob = d_w * w / pr;
+        const double d_zinv = d_w * w / A.blend.gamma;
+        const double d_dists = d_prob * (-pr * (1.0 - pr) / A.blend.sigma);
+        double d_zbuf = clamped ? 0.0 : d_zinv * (-1.0 / zrange);
+        if (s == argmax && !clamped) d_zbuf += d_zinv_max * (-1.0 / zrange);
+        // interpolate_face_attributes_backward (shading.cpp:46-72): d_bary_i = d_col . a_i, d_attr_i += w_i d_col
+        double v[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)fid + t);
+        const FaceGeom fg = make_face_geom(v);
+        PixelFaceResult r;
+        eval_pixel_face<true, true>(p, fg, A.blur, A.znear, A.persp, A.clip, r);
+        SlotIn<double> in;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)fid + q];
+          in.db[q] = d_col[0] * __ldg(a) + d_col[1] * __ldg(a + 1) + d_col[2] * __ldg(a + 2);
+          in.w[q] = r.bary[q];
+          gc[3 * q + 0] = r.bary[q] * d_col[0];
+          gc[3 * q + 1] = r.bary[q] * d_col[1];
+          gc[3 * q + 2] = r.bary[q] * d_col[2];
+        }
+        in.dz = d_zbuf;
+        in.dd = d_dists;
+#if DR_BWD_PREFETCH_FV
+#pragma unroll
+        for (int t = 0; t < 9; ++t) in.v[t] = v[t];
+#endif
+        slot_backward(BA, p, fid, in, g);
+      }
+      // one reduction over 18 values: the face_verts cotangent and the face's vertex-colour cotangents
+      double gg[18];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        gg[k] = g[k];
+        gg[9 + k] = gc[k];
+      }
+      if (reduce_by_face<18>(fid, lane, gg)) {
+        double* out = A.grad + 9 * (int64_t)fid;
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+          if (gg[k] != 0.0) atomicAdd(out + k, gg[k]);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          double* oc = A.grad_colors + 3 * A.blend.faces[3 * (int64_t)fid + q];
+          for (int d = 0; d < 3; ++d)
+            if (gg[9 + 3 * q + d] != 0.0) atomicAdd(oc + d, gg[9 + 3 * q + d]);
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
+  if (A.npix <= 0) return cudaSuccess;
+  if (A.K > kSoftMaxK) return cudaErrorInvalidConfiguration;
+  const size_t per_warp = ((size_t)A.K * 32 * 6 + (size_t)A.K * 16) * sizeof(double);
+  const int warps = (int)std::min<size_t>(kSoftThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));
+  const size_t smem = per_warp * warps;
+  cudaError_t e = cudaFuncSetAttribute(k_softmax_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(smem, 48 * 1024));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_softmax_backward, warps * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int64_t blocks = (int64_t)sms * per_sm;
+  const int64_t need = (A.npix + warps * 32 - 1) / (warps * 32);
+  if (blocks > need) blocks = need;
+  k_softmax_backward<<<(unsigned)blocks, warps * 32, smem, st>>>(A);
+  return cudaGetLastError();
+}
+
 template <typename InT>
 static cudaError_t launch_backward_t(const BwdArgs<InT>& A, cudaStream_t st) {
   if (A.S <= 0) return cudaSuccess;

@@ -481,6 +481,34 @@ __device__ __forceinline__ double silhouette_prob(const double* v, double px, do
   return 1.0 / (1.0 + exp(-x));
 }
 
+// softmax_blend's clamped inverse depth (shading.cpp:136-137): (zfar - clamp(z, znear, zfar)) / (zfar - znear)
+__device__ __forceinline__ double blend_zinv(double z, const BlendArgs& bl) {
+  const double zc = z < bl.znear ? bl.znear : (bl.zfar < z ? bl.zfar : z);  // std::clamp
+  return (bl.zfar - zc) / (bl.zfar - bl.znear);
+}
+
+// one occupied slot of the softmax render: interpolate_face_attributes of the vertex colours with the slot's
+// clamped barycentrics (shading.cpp:11-32: o[d] += w_i * a_i[d], i = 0..2) and the slot's opacity
+// sigmoid(-dists / sigma) (shading.cpp:146); fast divisions (values are consumed within tolerance)
+template <typename OutT>
+__device__ __forceinline__ void softmax_slot(const FineArgs<OutT>& A, const double* v, int32_t f, double px,
+                                             double py, double c[3], double& prob) {
+  const FaceGeom g = make_face_geom(v);
+  PixelFaceResult r;
+  eval_pixel_face<true, false>(V2{px, py}, g, A.blur, A.znear, A.persp, A.clip, r);
+  c[0] = c[1] = c[2] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int64_t vi = A.blend.faces[3 * (int64_t)f + i];
+    const double* a = A.blend.vert_colors + 3 * vi;
+    c[0] += r.bary[i] * __ldg(a);
+    c[1] += r.bary[i] * __ldg(a + 1);
+    c[2] += r.bary[i] * __ldg(a + 2);
+  }
+  const double x = -r.dist / A.blend.sigma;
+  prob = 1.0 / (1.0 + exp(-x));
+}
+
 // Insert (zc, f) into pixel p's sorted list (column p of [K][32]) in shared memory: shifting loop.
 // kCounted (the shared-memory list path, KMAX == 0): ws.tcnt[p] = entries held, so a list that is not full grows
 // at its end instead of shifting +inf padding down from slot K-1 (for K = 50 that padding walk was most of the
@@ -692,9 +720,10 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
 
 // 128 registers per thread (16 resident warps per SM) is the measured sweet spot: capping lower spills, and
 // fewer resident warps cannot hide the fp64 dependency latency (profiles/r01/README.md).
-// kSil: fused silhouette emit (alpha, optional pix_to_face) instead of the fragment payload — a separate
-// instantiation so the fragment path's code (and register allocation) does not carry it
-template <typename OutT, int NW, int KMAX, bool kSil>
+// kMode: 0 = the fragment payload; 1 = fused silhouette emit (alpha, optional pix_to_face); 2 = fused softmax
+// render emit (interpolated vertex colours + softmax_blend -> image, optional pix_to_face) — separate
+// instantiations so the fragment path's code (and register allocation) does not carry them
+template <typename OutT, int NW, int KMAX, int kMode>
 __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS : 16 / NW) k_fine(FineArgs<OutT> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -863,6 +892,17 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
         for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
       }
       double keep = 1.0;  // silhouette mode: prod over occupied slots of (1 - prob)
+      // softmax mode (shading.cpp:123-160): zinv_max over the occupied slots from the exact depths in the list
+      double zinv_max = -1.0, wsum = 0.0, acc[3] = {0.0, 0.0, 0.0};
+      bool any = false;
+      if constexpr (kMode == 2) {
+        for (int s = 0; s < K; ++s) {
+          if (ws.tid[s * 32 + lane] == INT_MAX) continue;
+          any = true;
+          const double zi = blend_zinv(ws.tz[s * 32 + lane], A.blend);
+          zinv_max = zinv_max < zi ? zi : zinv_max;  // std::max(zinv_max, zinv)
+        }
+      }
       for (int s = 0; s < K; ++s) {
         const int32_t f = fnext;
         double v[9];
@@ -873,14 +913,39 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 #pragma unroll
           for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
         }
-        if constexpr (kSil) {
+        if constexpr (kMode == 1) {
           if (A.p2f) A.p2f[slot0 + s] = f != INT_MAX ? (int64_t)f : -1;
           if (f != INT_MAX) keep *= 1.0 - silhouette_prob(v, px, py, A.sigma);
+        } else if constexpr (kMode == 2) {
+          if (A.p2f) A.p2f[slot0 + s] = f != INT_MAX ? (int64_t)f : -1;
+          if (f != INT_MAX) {
+            double c[3], prob;
+            softmax_slot(A, v, f, px, py, c, prob);
+            const double zi = blend_zinv(ws.tz[s * 32 + lane], A.blend);
+            const double w = prob * exp((zi - zinv_max) / A.blend.gamma);
+            wsum += w;
+            acc[0] += c[0] * w;  // Vec3 += Vec3 * double
+            acc[1] += c[1] * w;
+            acc[2] += c[2] * w;
+          }
         } else {
           emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, v, px, py);
         }
       }
-      if constexpr (kSil) A.alpha[((int64_t)b * A.H + pi) * A.W + pj] = (OutT)(1.0 - keep);  // shading.cpp:86
+      if constexpr (kMode == 1) A.alpha[((int64_t)b * A.H + pi) * A.W + pj] = (OutT)(1.0 - keep);  // shading.cpp:86
+      if constexpr (kMode == 2) {
+        OutT* img = A.image + 3 * (((int64_t)b * A.H + pi) * A.W + pj);
+        if (!any) {
+          img[0] = (OutT)A.blend.background[0];  // shading.cpp:130, 141
+          img[1] = (OutT)A.blend.background[1];
+          img[2] = (OutT)A.blend.background[2];
+        } else {
+          const double inv = 1.0 / wsum;  // image = acc * (1.0 / wsum), shading.cpp:153
+          img[0] = (OutT)(acc[0] * inv);
+          img[1] = (OutT)(acc[1] * inv);
+          img[2] = (OutT)(acc[2] * inv);
+        }
+      }
     }
     __syncwarp();
   }
@@ -951,20 +1016,26 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
   auto by_k = [&](auto nw_c) -> cudaError_t {
     constexpr int NW = decltype(nw_c)::value;
     // register-resident merge for small K, shared-memory shifting loop otherwise
-    if (A.alpha) {
-      if constexpr (std::is_same<OutT, float>::value) {
-        if (A.K == 1) return go(k_fine<OutT, NW, 1, true>);
-        if (A.K <= 4) return go(k_fine<OutT, NW, 4, true>);
-        if (A.K <= 8) return go(k_fine<OutT, NW, 8, true>);
-        return go(k_fine<OutT, NW, 0, true>);
+    if (A.alpha || A.image) {
+      if constexpr (std::is_same<OutT, float>::value) {  // the fused consumers write fp32 images only
+        if (A.alpha) {
+          if (A.K == 1) return go(k_fine<OutT, NW, 1, 1>);
+          if (A.K <= 4) return go(k_fine<OutT, NW, 4, 1>);
+          if (A.K <= 8) return go(k_fine<OutT, NW, 8, 1>);
+          return go(k_fine<OutT, NW, 0, 1>);
+        }
+        if (A.K == 1) return go(k_fine<OutT, NW, 1, 2>);
+        if (A.K <= 4) return go(k_fine<OutT, NW, 4, 2>);
+        if (A.K <= 8) return go(k_fine<OutT, NW, 8, 2>);
+        return go(k_fine<OutT, NW, 0, 2>);
       } else {
-        return cudaErrorInvalidValue;  // the fused silhouette writes fp32 alpha only
+        return cudaErrorInvalidValue;
       }
     }
-    if (A.K == 1) return go(k_fine<OutT, NW, 1, false>);
-    if (A.K <= 4) return go(k_fine<OutT, NW, 4, false>);
-    if (A.K <= 8) return go(k_fine<OutT, NW, 8, false>);
-    return go(k_fine<OutT, NW, 0, false>);
+    if (A.K == 1) return go(k_fine<OutT, NW, 1, 0>);
+    if (A.K <= 4) return go(k_fine<OutT, NW, 4, 0>);
+    if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0>);
+    return go(k_fine<OutT, NW, 0, 0>);
   };
   if (nw == 8) return by_k(std::integral_constant<int, 8>{});
   return by_k(std::integral_constant<int, 2>{});

@@ -8,6 +8,16 @@
 
 namespace drb {
 
+// softmax render (shading.cpp:123-230 over interpolate_face_attributes, shading.cpp:11-73; grad.cpp:177-209)
+struct BlendArgs {
+  const double* vert_colors = nullptr;  // [V,3] packed per-vertex colours
+  const int64_t* faces = nullptr;       // [F,3] packed faces, global vertex ids
+  int64_t V = 0;
+  double sigma = 1e-4, gamma = 1e-4;    // BlendParams (shading.hpp:13-17)
+  double background[3] = {0.0, 0.0, 0.0};
+  double znear = 0.1, zfar = 100.0;     // Camera.znear / zfar
+};
+
 template <typename OutT>
 struct FineArgs {
   const double* fv;         // [F,3,3] face_verts
@@ -34,6 +44,8 @@ struct FineArgs {
   OutT* dists;
   OutT* alpha;   // non-null => fused silhouette_blend (shading.cpp:75-91): alpha [N,H,W] (+ p2f if non-null)
   double sigma;  // silhouette opacity falloff (BlendParams.sigma)
+  OutT* image;   // non-null => fused softmax render: image [N,H,W,3] (+ p2f if non-null)
+  BlendArgs blend;
 };
 
 // Unsigned 32-bit division by a run-time invariant divisor with one multiply-high (Granlund & Montgomery,
@@ -112,6 +124,22 @@ cudaError_t launch_points_backward(const double* pts, const int64_t* idx, const 
                                    int64_t P, int H, int W, int K, double* grad, cudaStream_t st);
 cudaError_t launch_points_backward(const double* pts, const int64_t* idx, const double* gz, const double* gd,
                                    int64_t S, int64_t P, int H, int W, int K, double* grad, cudaStream_t st);
+
+// fused softmax render backward (grad.cpp:195-206: softmax_blend_backward -> interpolate_face_attributes_backward
+// -> rasterize_backward)
+struct SoftBwdArgs {
+  const double* fv;
+  const int64_t* p2f;      // [N,H,W,K]
+  const float* d_image;    // [N,H,W,3]
+  double* grad;            // [F,3,3] face_verts cotangent
+  double* grad_colors;     // [V,3] vertex-colour cotangent
+  int64_t npix, F;
+  int H, W, K;
+  bool persp, clip;
+  double blur, znear;      // raster settings (exact re-evaluation of each slot)
+  BlendArgs blend;
+};
+cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st);
 
 // Camera (dr_camera / dr::Camera, camera.hpp:19-35) as kernel arguments.
 struct CameraArgs {

@@ -299,6 +299,108 @@ class RasterizeSilhouette(torch.autograd.Function):
         return g.to(fv.dtype), None, None, None, None
 
 
+@dataclass
+class BlendParams:
+    """BlendParams (shading.hpp:13-17) + the camera's znear / zfar used by softmax_blend's depth normalisation."""
+
+    sigma: float = 1e-4
+    gamma: float = 1e-4
+    background_color: tuple = (0.0, 0.0, 0.0)
+    znear: float = 0.1
+    zfar: float = 100.0
+
+    def to_c(self) -> _lib.DrBlendParams:
+        b = _lib.DrBlendParams()
+        b.sigma, b.gamma = float(self.sigma), float(self.gamma)
+        for i in range(3):
+            b.background[i] = float(self.background_color[i])
+        b.znear, b.zfar = float(self.znear), float(self.zfar)
+        return b
+
+
+def _blend_inputs(vert_colors, faces, dev):
+    vc = torch.as_tensor(vert_colors).to(device=dev, dtype=torch.float64).contiguous()
+    fc = torch.as_tensor(faces).to(device=dev, dtype=torch.int64).contiguous()
+    if vc.dim() != 2 or vc.shape[1] != 3 or fc.dim() != 2 or fc.shape[1] != 3:
+        raise ShapeError(f"vert_colors must be [V,3] and faces [F,3], got {tuple(vc.shape)} / {tuple(fc.shape)}")
+    return vc, fc
+
+
+def rasterize_softmax(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
+                      blend: BlendParams, vert_colors, faces, want_pix_to_face: bool = True, workspace=None):
+    """Fused softmax render (grad.cpp:177-193): rasterize_meshes -> interpolate_face_attributes(vert_colors) ->
+    softmax_blend. Returns (pix_to_face int64 [N,H,W,K] or None, image float32 [N,H,W,3])."""
+    L = _lib.load()
+    fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
+    vc, fc = _blend_inputs(vert_colors, faces, fv.device)
+    if fc.shape[0] != fv.shape[0]:
+        raise ShapeError(f"faces [{fc.shape[0]},3] does not match face_verts [{fv.shape[0]},3,3]")
+    N, F = int(first.numel()), int(fv.shape[0])
+    H, W = settings.hw
+    K = int(settings.faces_per_pixel)
+    s = settings.to_c()
+    b = blend.to_c()
+    dev = fv.device
+    ws_n = L.dr_rasterize_meshes_workspace_bytes(N, F, C.byref(s))
+    if ws_n == 0:
+        _check(_lib.DR_ERR_RANGE if N >= 1 else _lib.DR_ERR_SHAPE, "rasterize_softmax")
+    if workspace is None or workspace.numel() < ws_n:
+        workspace = torch.empty(ws_n, dtype=torch.uint8, device=dev)
+    p2f = torch.empty((N, H, W, K), dtype=torch.int64, device=dev) if want_pix_to_face else None
+    image = torch.empty((N, H, W, 3), dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        rc = L.dr_rasterize_softmax_fwd(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), C.byref(b), _ptr(vc),
+                                        _ptr(fc), vc.shape[0], _ptr(p2f), _ptr(image), _ptr(workspace),
+                                        workspace.numel(), _stream(dev))
+    _check(rc, "rasterize_softmax")
+    return p2f, image
+
+
+def rasterize_softmax_backward(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
+                               blend: BlendParams, vert_colors, faces, pix_to_face, grad_image):
+    """Fused vjp of the softmax render (grad.cpp:195-206): returns (grad_face_verts [F,3,3] f64,
+    grad_vert_colors [V,3] f64)."""
+    L = _lib.load()
+    fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
+    vc, fc = _blend_inputs(vert_colors, faces, fv.device)
+    N, F = int(first.numel()), int(fv.shape[0])
+    H, W = settings.hw
+    K = int(settings.faces_per_pixel)
+    if tuple(pix_to_face.shape) != (N, H, W, K) or tuple(grad_image.shape) != (N, H, W, 3):
+        raise ShapeError("rasterize_softmax_backward: pix_to_face / grad_image do not match [N,H,W,K] / [N,H,W,3]")
+    p2f = pix_to_face.to(torch.int64).contiguous()
+    gi = grad_image.to(torch.float32).contiguous()
+    g_fv = torch.zeros((F, 3, 3), dtype=torch.float64, device=fv.device)
+    g_vc = torch.zeros_like(vc)
+    s = settings.to_c()
+    b = blend.to_c()
+    with torch.cuda.device(fv.device):
+        rc = L.dr_rasterize_softmax_bwd(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), C.byref(b), _ptr(vc),
+                                        _ptr(fc), vc.shape[0], _ptr(p2f), _ptr(gi), _ptr(g_fv), _ptr(g_vc),
+                                        _stream(fv.device))
+    _check(rc, "rasterize_softmax_backward")
+    return g_fv, g_vc
+
+
+class RasterizeSoftmax(torch.autograd.Function):
+    """Autograd wrapper of the fused softmax render: (face_verts, vert_colors) -> image [N,H,W,3]."""
+
+    @staticmethod
+    def forward(ctx, face_verts, vert_colors, faces, first, num, settings: RasterSettings, blend: BlendParams):
+        p2f, image = rasterize_softmax(face_verts, first, num, settings, blend, vert_colors, faces)
+        ctx.settings, ctx.blend = settings, blend
+        ctx.save_for_backward(face_verts, vert_colors, torch.as_tensor(faces, device=face_verts.device),
+                              torch.as_tensor(first, device=face_verts.device),
+                              torch.as_tensor(num, device=face_verts.device), p2f)
+        return image
+
+    @staticmethod
+    def backward(ctx, g_image):
+        fv, vc, faces, first, num, p2f = ctx.saved_tensors
+        g_fv, g_vc = rasterize_softmax_backward(fv, first, num, ctx.settings, ctx.blend, vc, faces, p2f, g_image)
+        return g_fv.to(fv.dtype), g_vc.to(vc.dtype), None, None, None, None, None
+
+
 def bin_stats(num_meshes, num_faces, settings: RasterSettings, workspace: torch.Tensor) -> dict:
     """Coarse-stage counters left in the workspace by the last forward (synchronises)."""
     L = _lib.load()
