@@ -495,12 +495,14 @@ cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
 // Fused softmax render backward: the reference's differentiable softmax render (grad.cpp:177-209) is
 // rasterize_meshes -> interpolate_face_attributes(vertex colours) -> softmax_blend; its vjp chains
 // softmax_blend_backward (shading.cpp:162-230) -> interpolate_face_attributes_backward (shading.cpp:35-73) ->
-// rasterize_backward (MR:329-378). Here one lane per pixel walks its K slots: pass 1 re-evaluates each slot
-// EXACTLY (the forward's depth, clamped barycentrics and distance, bit for bit — so depth ties pick the same
-// argmax as the reference) and keeps inverse depth, opacity and interpolated colour in shared memory; passes 2-3
-// form the softmax weights and the per-pixel mean term; pass 4 produces d_colors / d_dists / d_zbuf per slot
-// (plus the zinv_max term on the argmax slot), d_bary_i = d_color . colour(v_i), the vertex-colour cotangent
+// rasterize_backward (MR:329-378). Here one lane per pixel walks its K slots: pass 1 re-evaluates each slot (fast
+// divisions: values within tolerance) and keeps inverse depth, opacity and interpolated colour in shared memory;
+// passes 2-3 form the softmax weights and the per-pixel mean term; pass 4 produces d_colors / d_dists / d_zbuf per
+// slot (plus the zinv_max term on the argmax slot), d_bary_i = d_color . colour(v_i), the vertex-colour cotangent
 // and the K3 per-slot chain, summed per face across the warp before the fp64 atomics.
+// The argmax of zinv (shading.cpp:190-193, first strict maximum) is always the first occupied slot: slots are
+// sorted ascending by (z, id) and zinv is non-increasing in z (clamping only creates equal values, and the first
+// of equal values wins), so no exact depth is needed to reproduce the reference's choice under depth ties.
 
 constexpr int kSoftThreads = 128;
 constexpr int kSoftMaxK = 64;
@@ -565,10 +567,10 @@ __global__ void __launch_bounds__(kSoftThreads) k_softmax_backward(SoftBwdArgs A
         for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)f + t);
         const FaceGeom g = make_face_geom(v);
         PixelFaceResult r;
-        eval_pixel_face<true, true>(p, g, A.blur, A.znear, A.persp, A.clip, r);  // the forward's exact bits
+        eval_pixel_face<true, false>(p, g, A.blur, A.znear, A.persp, A.clip, r);
         bool clamped;
         zi = blend_zinv_b(r.z, A.blend, clamped);
-        if (zi > zinv_max) {
+        if (argmax < 0) {  // the first occupied slot (see above)
           zinv_max = zi;
           argmax = s;
         }
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(kSoftThreads) k_softmax_backward(SoftBwdArgs A
         for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)fid + t);
         const FaceGeom fg = make_face_geom(v);
         PixelFaceResult r;
-        eval_pixel_face<true, true>(p, fg, A.blur, A.znear, A.persp, A.clip, r);
+        eval_pixel_face<true, false>(p, fg, A.blur, A.znear, A.persp, A.clip, r);
         SlotIn<double> in;
 #pragma unroll
         for (int q = 0; q < 3; ++q) {

@@ -6,6 +6,8 @@ fused:    rasterize_silhouette + rasterize_silhouette_backward (alpha / pix_to_f
 unfused:  rasterize_meshes -> silhouette_blend in torch ops (fp64) -> autograd d_dists ->
           rasterize_meshes_backward (fragments + cotangents round-trip through HBM)
 fragments: the bench step (rasterize_meshes + rasterize_meshes_backward with random cotangents), for scale.
+softmax:  the same comparison for the softmax render (vertex colours + softmax_blend, grad.cpp:177-209); the
+          unfused arm's torch ops skip the reference's exact tie rule for zinv_max's argmax (timing arm only).
 Prints one JSON line with ms per step of each and the kernels' share.
 """
 import argparse
@@ -79,12 +81,47 @@ def main():
         p2f, zbuf, bary, dists = rasterize_meshes(fv, first, num, rs, workspace=ws)
         return rasterize_meshes_backward(fv, first, num, rs, p2f, bary, dz, db, dd)
 
+    # softmax render (grad.cpp:177-209): vertex colours interpolated with the clamped barycentrics, softmax blend
+    from paper_2007_08501_b200 import BlendParams, rasterize_softmax, rasterize_softmax_backward
+
+    V = len(m.verts_packed())
+    vc = torch.rand((V, 3), generator=g, device=dev, dtype=torch.float64)
+    faces = torch.as_tensor(m.faces_packed(), device=dev)
+    bp = BlendParams(sigma=a.sigma, gamma=1e-4, znear=cam.znear, zfar=cam.zfar)
+    d_image = torch.randn((N, H, W, 3), generator=g, device=dev)
+
+    def soft_fused():
+        p2f, image = rasterize_softmax(fv, first, num, rs, bp, vc, faces, workspace=ws)
+        return rasterize_softmax_backward(fv, first, num, rs, bp, vc, faces, p2f, d_image)[0]
+
+    def soft_unfused():
+        p2f, zbuf, bary, dists = rasterize_meshes(fv, first, num, rs, workspace=ws)
+        occ = p2f >= 0
+        fidx = torch.where(occ, p2f, torch.zeros_like(p2f))
+        b = bary.double().requires_grad_(True)
+        d = dists.double().requires_grad_(True)
+        z = zbuf.double().requires_grad_(True)
+        col = (b.unsqueeze(-1) * vc[faces[fidx]]).sum(-2)  # interpolate_face_attributes
+        zc = z.clamp(bp.znear, bp.zfar)
+        zinv = torch.where(occ, (bp.zfar - zc) / (bp.zfar - bp.znear), torch.full_like(zc, -1.0))
+        zmax = zinv.max(-1, keepdim=True).values
+        prob = torch.sigmoid(-d / bp.sigma)
+        w = torch.where(occ, prob * torch.exp((zinv - zmax) / bp.gamma), torch.zeros_like(prob))
+        img = (w.unsqueeze(-1) * col).sum(-2) / w.sum(-1, keepdim=True).clamp_min(1e-300)
+        gz, gb, gdd = torch.autograd.grad(img, (z, b, d), d_image.double())
+        return rasterize_meshes_backward(fv, first, num, rs, p2f, bary, gz.float(), gb.float(), gdd.float())
+
     gf, gu = fused(), unfused()
     err = float((gf - gu).abs().max() / gu.abs().max())
+    sf, su = soft_fused(), soft_unfused()
+    serr = float((sf - su).abs().max() / su.abs().max())
     out = {"config": a.config, "sigma": a.sigma,
            "fused_ms": timed(fused, a.steps, a.warmup), "unfused_ms": timed(unfused, a.steps, a.warmup),
-           "fragments_ms": timed(fragments, a.steps, a.warmup), "fused_vs_unfused_grad_rel_err": err}
+           "fragments_ms": timed(fragments, a.steps, a.warmup), "fused_vs_unfused_grad_rel_err": err,
+           "softmax_fused_ms": timed(soft_fused, a.steps, a.warmup),
+           "softmax_unfused_ms": timed(soft_unfused, a.steps, a.warmup), "softmax_grad_rel_err": serr}
     out["speedup"] = out["unfused_ms"] / out["fused_ms"]
+    out["softmax_speedup"] = out["softmax_unfused_ms"] / out["softmax_fused_ms"]
     print(json.dumps(out))
 
 
