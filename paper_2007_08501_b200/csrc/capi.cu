@@ -414,7 +414,8 @@ struct PointPlan {
   int H = 0, W = 0, K = 0, bs = 16, nbx = 0, nby = 0;
   bool binned = false;
   int64_t nbins_total = 0, pool = 0;
-  size_t off_ibbox = 0, off_bounds = 0, off_counts = 0, off_cursor = 0, off_binoff = 0, off_lists = 0, total = 0;
+  size_t off_ibbox = 0, off_zkey = 0, off_bounds = 0, off_counts = 0, off_cursor = 0, off_binoff = 0, off_lists = 0,
+         total = 0;
 };
 
 int make_point_plan(int64_t N, int64_t P, const dr_point_raster_settings* s, PointPlan& p) {
@@ -441,6 +442,8 @@ int make_point_plan(int64_t N, int64_t P, const dr_point_raster_settings* s, Poi
   size_t off = 0;
   p.off_ibbox = off;
   off = align_up(off + sizeof(int4) * (size_t)std::max<int64_t>(P, 1));
+  p.off_zkey = off;
+  off = align_up(off + sizeof(float) * (size_t)std::max<int64_t>(P, 1));
   p.off_bounds = off;
   off = align_up(off + sizeof(double) * 2 * (size_t)(p.nbx + p.nby));
   p.off_counts = off;
@@ -482,6 +485,7 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   char* base = static_cast<char*>(ws);
   int4* ibbox = reinterpret_cast<int4*>(base + p.off_ibbox);
   double* bounds = reinterpret_cast<double*>(base + p.off_bounds);
+  float* zkey = reinterpret_cast<float*>(base + p.off_zkey);
   int* counts = reinterpret_cast<int*>(base + p.off_counts);
   int* cursor = reinterpret_cast<int*>(base + p.off_cursor);
   int64_t* bin_off = reinterpret_cast<int64_t*>(base + p.off_binoff);
@@ -490,7 +494,7 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   {
     ProfScope ps(st, KN_PT_SETUP);
     e = drb::launch_point_setup(pts, p_lo, p_hi, p.H, p.W, p.bs, p.nbx, p.nby, s->radius, s->znear,
-                                s->clip_nonpositive_z, bounds, ibbox, st);
+                                s->clip_nonpositive_z, bounds, ibbox, zkey, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "rasterize_points setup");
   if (p.binned) {
@@ -502,8 +506,14 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
     ProfScope ps(st, KN_BIN);
     drb::launch_bin_faces(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, st);
     drb::launch_scan_bins(counts, p.nbins_total, bin_off, st);
-    drb::launch_fill_bins(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool, nullptr,
+    drb::launch_fill_bins(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool, zkey,
                           entries, st);
+  }
+  const bool sorted = p.binned && zsort_enabled();
+  if (sorted) {
+    ProfScope ps(st, KN_SORT);
+    e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, 0, st);
+    if (e != cudaSuccess) return cuda_fail(e, "sorting point bins");
   }
   drb::PointFineArgs<OutT> A;
   A.pts = pts;
@@ -518,6 +528,7 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   A.bs = p.bs;
   A.nbx = p.nbx;
   A.nby = p.nby;
+  A.sorted = sorted ? 1 : 0;
   A.sub_x = (p.bs + 15) / 16;
   A.sub_y = (p.bs + 15) / 16;
   A.H = p.H;

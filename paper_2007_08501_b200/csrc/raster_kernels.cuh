@@ -107,6 +107,7 @@ struct PointFineArgs {  // rasterize_points (point_render.cpp:105-155)
   const int4* bin_entries;
   int64_t pool;
   int binned, bs, nbx, nby, sub_x, sub_y;  // sub_x/sub_y: 16x16 blocks per bin row / column
+  int sorted;                              // bins sorted ascending by depth key (early exit)
   int H, W, K;
   double r2;
   int N;
@@ -117,7 +118,7 @@ struct PointFineArgs {  // rasterize_points (point_render.cpp:105-155)
 
 cudaError_t launch_point_setup(const double* pts, int64_t p_lo, int64_t p_hi, int H, int W, int ts, int nbx, int nby,
                                double radius, double znear, int clip_z, double* bounds /*[2*nbx + 2*nby]*/,
-                               int4* ibbox, cudaStream_t st);
+                               int4* ibbox, float* zkey, cudaStream_t st);
 cudaError_t launch_points_fine(const PointFineArgs<float>& A, cudaStream_t st);
 cudaError_t launch_points_fine(const PointFineArgs<double>& A, cudaStream_t st);
 cudaError_t launch_points_backward(const double* pts, const int64_t* idx, const float* gz, const float* gd, int64_t S,

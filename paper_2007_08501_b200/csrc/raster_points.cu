@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(256) k_point_setup(const double* __restrict__ 
                                                      const double* __restrict__ bx_min,
                                                      const double* __restrict__ bx_max,
                                                      const double* __restrict__ by_min,
-                                                     const double* __restrict__ by_max, int4* __restrict__ ibbox) {
+                                                     const double* __restrict__ by_max, int4* __restrict__ ibbox,
+                                                     float* __restrict__ zkey) {
   const int64_t p = p_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= p_hi) return;
   const double x = pts[3 * p], y = pts[3 * p + 1], z = pts[3 * p + 2];
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(256) k_point_setup(const double* __restrict__ 
     if (tx0 <= tx1 && ty0 <= ty1) out = make_int4(ty0 * ts, ty1 * ts, tx0 * ts, tx1 * ts);  // as pixel ranges
   }
   ibbox[p] = out;
+  zkey[p] = keep ? __double2float_rd(z) : __int_as_float(0x7f800000);  // <= z: a point's depth IS its candidate z
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -115,6 +117,7 @@ template <typename OutT, int KMAX>
 __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> A) {
   __shared__ double sx[kPtThreads], sy[kPtThreads], sz[kPtThreads];
   __shared__ int32_t sid[kPtThreads];
+  __shared__ double s_kth[kPtThreads / 32];
   // per-pixel sorted (z, id) list: KMAX > 0 => registers (fully unrolled, +inf padded), else local memory
   constexpr int KL = KMAX > 0 ? KMAX : kPtMaxK;
   double lz[KL];
@@ -138,6 +141,7 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
     // candidate points: the bin list, or the whole cloud (naive / spilled bin)
     const int64_t p0 = A.first[b], np = A.num[b];
     const int4* list = nullptr;
+    bool sorted = false;
     int64_t nsrc = np;
     if (A.binned) {
       const int64_t gb = (int64_t)b * nbins + bin;
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
       if (bin_fits(o, c, A.pool, 0)) {
         list = A.bin_entries + o;
         nsrc = c;
+        sorted = A.sorted && c <= kSortMaxBig;  // longer bins stay unsorted (k_sort_bins)
       }
     }
     int n = 0;  // candidates held (generic path)
@@ -157,6 +162,22 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
       }
     }
     for (int64_t c0 = 0; c0 < nsrc; c0 += kPtThreads) {
+      // depth-ordered bin: once every pixel of the block holds K points nearer than the next point's depth key,
+      // no later point can enter any list (strict (z, id) order, PR:37)
+      if (sorted) {
+        double kth = -__longlong_as_double(0x7ff0000000000000LL);
+        if (valid) {
+          if constexpr (KMAX > 0) kth = lz[KMAX - 1];  // >= the K-th depth (== it when K == KMAX)
+          else kth = n < K ? __longlong_as_double(0x7ff0000000000000LL) : lz[K - 1];
+        }
+        for (int d = 16; d >= 1; d >>= 1) kth = fmax(kth, __shfl_xor_sync(0xffffffffu, kth, d));
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) s_kth[threadIdx.x >> 5] = kth;
+        __syncthreads();
+        double T = s_kth[0];
+        for (int w = 1; w < kPtThreads / 32; ++w) T = fmax(T, s_kth[w]);
+        if ((double)__int_as_float(list[c0].y) > T) break;
+      }
       __syncthreads();
       const int64_t ci = c0 + threadIdx.x;
       if (ci < nsrc) {
@@ -293,7 +314,7 @@ __global__ void __launch_bounds__(256) k_points_backward(const double* __restric
 // launchers
 
 cudaError_t launch_point_setup(const double* pts, int64_t p_lo, int64_t p_hi, int H, int W, int ts, int nbx, int nby,
-                               double radius, double znear, int clip_z, double* bounds, int4* ibbox,
+                               double radius, double znear, int clip_z, double* bounds, int4* ibbox, float* zkey,
                                cudaStream_t st) {
   const int nt = std::max(nbx, nby);
   double* bx_min = bounds;
@@ -303,7 +324,8 @@ cudaError_t launch_point_setup(const double* pts, int64_t p_lo, int64_t p_hi, in
   k_point_tile_bounds<<<(nt + 255) / 256, 256, 0, st>>>(H, W, ts, nbx, nby, radius, bx_min, bx_max, by_min, by_max);
   if (p_hi > p_lo)
     k_point_setup<<<(unsigned)((p_hi - p_lo + 255) / 256), 256, 0, st>>>(pts, p_lo, p_hi, ts, nbx, nby, znear, clip_z,
-                                                                         bx_min, bx_max, by_min, by_max, ibbox);
+                                                                         bx_min, bx_max, by_min, by_max, ibbox,
+                                                                         zkey);
   return cudaGetLastError();
 }
 
