@@ -296,11 +296,13 @@ def main():
     db = torch.randn((N, H, W, K, 3), generator=gen, device=dev)
     dd = torch.randn((N, H, W, K), generator=gen, device=dev)
 
+    host_ranges = (first_np, num_np)  # host copies of the mesh ranges: the calls never synchronise the stream
+
     def step():
-        p2f, zbuf, bary, dists = rasterize_meshes(fv, first, num, rs, workspace=ws)
+        p2f, zbuf, bary, dists = rasterize_meshes(fv, first, num, rs, workspace=ws, host_ranges=host_ranges)
         grad = None
         if c["backward"]:
-            grad = rasterize_meshes_backward(fv, first, num, rs, p2f, bary, dz, db, dd)
+            grad = rasterize_meshes_backward(fv, first, num, rs, p2f, bary, dz, db, dd, host_ranges=host_ranges)
         return p2f, grad
 
     def barrier():

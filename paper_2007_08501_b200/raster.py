@@ -188,6 +188,18 @@ def rasterize_meshes_naive(face_verts, mesh_to_face_first_idx, num_faces_per_mes
     return rasterize_meshes(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings, out_dtype=out_dtype)
 
 
+def _covers(host_ranges, F: int) -> bool:
+    """True when the meshes' face ranges cover [0, F) (the backward then overwrites every row of its output)."""
+    first, num = (np.asarray(x, dtype=np.int64) for x in host_ranges)
+    iv = sorted((int(a), int(a + n)) for a, n in zip(first, num) if n > 0)
+    hi = 0
+    for a, b in iv:
+        if a > hi:
+            return False
+        hi = max(hi, b)
+    return hi >= F
+
+
 def rasterize_meshes_backward(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
                               pix_to_face, bary_coords, grad_zbuf, grad_bary, grad_dists, out=None,
                               host_ranges=None):
@@ -214,6 +226,8 @@ def rasterize_meshes_backward(face_verts, mesh_to_face_first_idx, num_faces_per_
         if tuple(out.shape) != (F, 3, 3) or out.dtype != torch.float64 or not out.is_contiguous():
             raise ShapeError(f"out must be a contiguous [F,3,3] float64 tensor, got {tuple(out.shape)}")
         grad = out
+    elif host_ranges is not None and _covers(host_ranges, F):
+        grad = torch.empty((F, 3, 3), dtype=torch.float64, device=fv.device)  # every row is overwritten
     else:
         grad = torch.zeros((F, 3, 3), dtype=torch.float64, device=fv.device)
     s = settings.to_c()
