@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
 #ifndef DR_COMPACT
 #define DR_COMPACT 1  // compact the pairs the K-th-depth cull leaves before evaluating them
 #endif
+constexpr int kPairQ = 64;  // < 32 pending + one enumeration step of 32
 #ifndef DR_LIST_PREFETCH
 #define DR_LIST_PREFETCH 1
 #endif
@@ -359,7 +360,7 @@ struct WarpSmem {
   int32_t* bid;     // [kBuf][32]
   int32_t* bcnt;    // [32]
   double* pxy;      // [12] pixel-centre NDC coordinates of the micro-tile: x of its 8 columns, y of its 4 rows
-  uint32_t* pairq;  // [64] queued (ring slot << 5 | pixel) pairs awaiting evaluation
+  uint32_t* pairq;  // [kPairQ] queued (ring slot << 5 | pixel) pairs awaiting evaluation
   int32_t* tcnt;    // [32] entries held by each pixel's list (shared-memory list path, KMAX == 0)
 
   __device__ __forceinline__ double get(int f, int k) const { return d[f * kRing + k]; }
@@ -421,7 +422,7 @@ __host__ __device__ constexpr size_t warp_smem_bytes(int K) {
   return (size_t)kNF * kRing * sizeof(double) + (size_t)K * 32 * sizeof(double) + (size_t)kBuf * 32 * sizeof(double) +
          12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) + (size_t)K * 32 * sizeof(int32_t) +
          (size_t)kBuf * 32 * sizeof(int32_t) + (size_t)kRing * (sizeof(uint32_t) + sizeof(float)) +
-         32 * sizeof(int32_t) + 64 * sizeof(uint32_t) + 32 * sizeof(int32_t) +
+         32 * sizeof(int32_t) + kPairQ * sizeof(uint32_t) + 32 * sizeof(int32_t) +
          8;  // + pad keeps the next warp's base 8-byte aligned
 }
 
@@ -588,10 +589,43 @@ __device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane)
   }
 }
 
+// Append a passing candidate to its pixel's buffer (merging every buffer first if one would overflow).
+template <int KMAX, typename OutT>
+__device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const WarpSmem& ws, bool pass, int p,
+                                                 int32_t f, double z, int lane) {
+  const int K = A.K;
+  if (__any_sync(0xffffffffu, pass)) {
+    // append to the pixel's buffer; merge every buffer first if one would overflow
+    const unsigned peers = __match_any_sync(0xffffffffu, pass ? p : 32 + lane);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    const int n_same = __popc(peers);
+    int base = pass ? ws.bcnt[p] : 0;
+    if (__any_sync(0xffffffffu, pass && base + n_same > kBuf)) {
+      __syncwarp();
+      merge_buffers<KMAX>(ws, K, lane);
+      __syncwarp();
+      base = 0;
+    }
+    if (pass) {
+      if (rank < kBuf) {
+        ws.bz[(base + rank) * 32 + p] = z;
+        ws.bid[(base + rank) * 32 + p] = f;
+      }
+      if (rank == 0) ws.bcnt[p] = base + min(n_same, kBuf);
+    }
+    __syncwarp();
+    // more than kBuf candidates for one pixel in one step (rare): insert the excess directly, one at a time
+    const int extra = __reduce_max_sync(0xffffffffu, pass ? n_same - kBuf : 0);
+    for (int rr = 0; rr < extra; ++rr) {
+      if (pass && rank == kBuf + rr) list_insert<KMAX == 0>(ws, K, p, z, f);
+      __syncwarp();
+    }
+  }
+}
+
 // Evaluate the first n (<= 32) queued (face slot, pixel) pairs, one per lane, and insert the survivors.
 template <int KMAX, typename OutT>
 __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSmem& ws, int n, int lane) {
-  const int K = A.K;
   const uint32_t e = lane < n ? ws.pairq[lane] : 0x80000000u;
   const bool act = !(e >> 31);  // bit 31: culled (DR_COMPACT=0 keeps culled pairs in place)
   bool pass = false;
@@ -609,34 +643,9 @@ __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSm
   STAT_ADD(3, __popc(__ballot_sync(0xffffffffu, act)));
   STAT_ADD(4, __popc(__ballot_sync(0xffffffffu, pass)));
   STAT_ADD(7, 1);
-  if (__any_sync(0xffffffffu, pass)) {
-    // append to the pixel's buffer; merge every buffer first if one would overflow
-    const unsigned peers = __match_any_sync(0xffffffffu, pass ? p : 32 + lane);
-    const int rank = __popc(peers & ((1u << lane) - 1u));
-    const int n_same = __popc(peers);
-    int base = pass ? ws.bcnt[p] : 0;
-    if (__any_sync(0xffffffffu, pass && base + n_same > kBuf)) {
-      __syncwarp();
-      merge_buffers<KMAX>(ws, K, lane);
-      __syncwarp();
-      base = 0;
-    }
-    if (pass) {
-      if (rank < kBuf) {
-        ws.bz[(base + rank) * 32 + p] = res.z;
-        ws.bid[(base + rank) * 32 + p] = f;
-      }
-      if (rank == 0) ws.bcnt[p] = base + min(n_same, kBuf);
-    }
-    __syncwarp();
-    // more than kBuf candidates for one pixel in one step (rare): insert the excess directly, one at a time
-    const int extra = __reduce_max_sync(0xffffffffu, pass ? n_same - kBuf : 0);
-    for (int rr = 0; rr < extra; ++rr) {
-      if (pass && rank == kBuf + rr) list_insert<KMAX == 0>(ws, K, p, res.z, f);
-      __syncwarp();
-    }
-  }
+  insert_candidate<KMAX>(A, ws, pass, p, f, res.z, lane);
 }
+
 
 // Enumerate the (face, pixel) pairs of ring slots [head, head+G) (mod kRing): prefix sum of the covered
 // rectangle areas across lanes, then 32 pairs per step, one per lane (binary search over the prefix with
@@ -742,7 +751,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     ws.fkey = reinterpret_cast<float*>(ws.rect + kRing);
     ws.bcnt = reinterpret_cast<int32_t*>(ws.fkey + kRing);
     ws.pairq = reinterpret_cast<uint32_t*>(ws.bcnt + 32);
-    ws.tcnt = reinterpret_cast<int32_t*>(ws.pairq + 64);
+    ws.tcnt = reinterpret_cast<int32_t*>(ws.pairq + kPairQ);
   }
   const int nbins = A.nbx * A.nby;
   const int mtx = (A.bs + 7) >> 3, mty = (A.bs + 3) >> 2;  // micro-tiles per bin row / column
