@@ -361,12 +361,21 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
     const int rem = act ? (int)(pix % HW) : 0;
     const int i = rem / A.W, j = rem - (rem / A.W) * A.W;
     const V2 p{pixel_x(A.W, j), pixel_y(A.H, i)};
-    {
+    {  // coalesced, 8 loads in flight per lane
       const int64_t n = (A.npix - base < 32 ? A.npix - base : 32) * K;
       const int64_t* src = A.p2f + base * K;
-      for (int t = lane; t < 32 * K; t += 32) {
-        const int64_t f = t < n ? __ldcs(src + t) : -1;
-        FID[t] = (f >= 0 && f < A.F) ? (int32_t)f : -1;
+      for (int t0 = 0; t0 < 32 * K; t0 += 256) {
+        int64_t f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u * 32 + lane;
+          f[u] = t < n && t < 32 * K ? __ldcs(src + t) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u * 32 + lane;
+          if (t < 32 * K) FID[t] = (f[u] >= 0 && f[u] < A.F) ? (int32_t)f[u] : -1;
+        }
       }
       __syncwarp();
     }
@@ -396,8 +405,8 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
           int be;
           V2 qq;
           silhouette_envelope(v, p, dist, be, bt, qq, sign);
-          const double x = -dist / A.sigma;
-          prob = 1.0 / (1.0 + exp(-x));  // sigmoid, shading.cpp:9
+          // sigmoid(-dist / sigma) (shading.cpp:9, 82); fp32 exp: the value enters gradients within tolerance
+          prob = 1.0 / (1.0 + (double)expf((float)(dist / A.sigma)));
           if constexpr (kStore) {
             EX[s * 32 + lane] = (qq.x - p.x) * (2.0 * sign);
             EY[s * 32 + lane] = (qq.y - p.y) * (2.0 * sign);
