@@ -268,6 +268,11 @@ const char* dr_last_error(void);
 int dr_rasterize_meshes_bin_stats(int64_t N, int64_t F, const dr_raster_settings* s, const void* workspace,
                                   dr_stream_t stream, int64_t out[4]);
 
+/* Device self-test of the grouped exact division every selection-path quotient uses (raster_math.cuh xdiv_*):
+ * compares it bit for bit with IEEE a/b on n pseudo-random hard-case triples. Writes the mismatch count (and the
+ * first mismatching a, b) and returns 0, or DR_ERR_CUDA. Synchronous. */
+int dr_selftest_division(uint64_t n, uint64_t seed, uint64_t* mismatches, double first_bad_ab[2]);
+
 /* Number of kernels this library has launched in this process. */
 uint64_t dr_launch_count(void);
 

@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "dr_profile_enable",
     "dr_profile_read",
     "dr_profile_kernel_name",
+    "dr_selftest_division",
 )
 
 
@@ -136,6 +137,8 @@ def load() -> C.CDLL:
                                               C.c_size_t, _vp]
     L.dr_rasterize_silhouette_bwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp,
                                               _vp]
+    L.dr_selftest_division.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+    L.dr_selftest_division.restype = C.c_int
     bpp = C.POINTER(DrBlendParams)
     L.dr_rasterize_softmax_fwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, bpp, _vp, _vp, C.c_int64, _vp, _vp,
                                            _vp, C.c_size_t, _vp]

@@ -407,3 +407,17 @@ def test_host_pipeline_matches_device_calls(cuda):
                                      ref[0], ref[2], *(c.to(cuda) for c in cot))
     assert rel_err(grad_h.numpy(), gref.cpu().numpy()) < 1e-12
 
+
+
+def test_grouped_exact_division_is_ieee(cuda):
+    """xdiv_* (raster_math.cuh) == IEEE a/b bit for bit on hard cases: every selection-path quotient uses it."""
+    import ctypes as C
+
+    from paper_2007_08501_b200 import _lib
+
+    L = _lib.load()
+    bad = C.c_uint64(0)
+    ab = (C.c_double * 2)()
+    for seed in (1, 2, 3):
+        assert L.dr_selftest_division(1 << 27, seed, C.byref(bad), ab) == 0
+        assert bad.value == 0, f"grouped division differs from IEEE for a={ab[0]!r}, b={ab[1]!r}"
