@@ -134,12 +134,22 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
+def _ncu_summaries():
+    """Committed ncu summaries, newest first (round, then capture version, compared numerically)."""
+    import glob
+    import re
+
+    def key(path):
+        nums = [int(x) for x in re.findall(r"\d+", os.path.relpath(path, ROOT))]
+        return nums
+
+    return sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_*_summary.json")), key=key, reverse=True)
+
+
 def ncu_issue(cfg, kernel):
     """Issue-side utilisation of `kernel` from the newest committed ncu capture (the kernel is fp64-issue/latency
     bound, not HBM bound): fp64 pipe active and issue-slot active fractions, or None."""
-    import glob
-
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_*_summary.json")), reverse=True):
+    for path in _ncu_summaries():
         try:
             with open(path) as f:
                 k = json.load(f)[cfg][kernel]
@@ -155,9 +165,7 @@ def ncu_issue(cfg, kernel):
 def ncu_traffic(cfg, kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed ncu --set full capture of this
     bench command (profiles/*/ncu_*_summary.json, newest round first); None if there is none."""
-    import glob
-
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_*_summary.json")), reverse=True):
+    for path in _ncu_summaries():
         try:
             with open(path) as f:
                 d = json.load(f)
