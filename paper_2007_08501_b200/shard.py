@@ -33,13 +33,28 @@ def shard_loads(costs, shards) -> list:
     return [float(costs[s].sum()) for s in shards]
 
 
-def gather_fragments(local: dict, shards: list, rank: int, world: int, root: int = 0):
+def globalize_face_ids(pix_to_face, local_first, global_first):
+    """pix_to_face [n, H, W, K] of a rank that packed only its own meshes -> global packed face ids:
+    id - local_first[m] + global_first[m] per mesh m on occupied slots (-1 stays -1)."""
+    import torch
+
+    lf = torch.as_tensor(local_first, dtype=torch.int64, device=pix_to_face.device)
+    gf = torch.as_tensor(global_first, dtype=torch.int64, device=pix_to_face.device)
+    shift = (gf - lf).view(-1, *([1] * (pix_to_face.dim() - 1)))
+    return torch.where(pix_to_face >= 0, pix_to_face + shift, pix_to_face)
+
+
+def gather_fragments(local: dict, shards: list, rank: int, world: int, root: int = 0, face_ids=None):
     """Gather per-rank fragment blocks {name: tensor [n_r, ...]} into [N, ...] tensors on `root`, in global
-    mesh order. Uses torch.distributed point-to-point sends (NCCL over NVLink on GPUs). Returns the gathered
-    dict on root, None elsewhere."""
+    mesh order. Uses torch.distributed point-to-point sends (NCCL over NVLink on GPUs). ``face_ids`` =
+    (local_first, global_first) of this rank's meshes: its 'pix_to_face' block is converted from rank-local to
+    global packed face ids before it leaves the rank. Returns the gathered dict on root, None elsewhere."""
     import torch
     import torch.distributed as dist
 
+    if face_ids is not None and "pix_to_face" in local and len(shards[rank]):
+        local = dict(local)
+        local["pix_to_face"] = globalize_face_ids(local["pix_to_face"], *face_ids)
     names = sorted(local)
     if rank != root:
         if not shards[rank]:

@@ -40,9 +40,17 @@ def _worker(rank, world, port, shards, result_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     # each rank fabricates the fragment blocks of its meshes: value = global mesh id
     idx = shards[rank]
-    loc = {"pix_to_face": torch.tensor(idx, dtype=torch.int64).view(-1, 1, 1, 1).expand(-1, 4, 4, 2).contiguous(),
+    # rank-local packing: this rank's meshes own faces [local_first[m], ...) of ITS face_verts; every occupied
+    # slot holds the mesh's first local face id, one slot per pixel is empty
+    counts = np.array([100, 5, 70, 30, 1])
+    gfirst = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    lcounts = counts[idx]
+    lfirst = np.concatenate([[0], np.cumsum(lcounts)[:-1]]) if len(idx) else np.zeros(0, np.int64)
+    p2f = torch.tensor(lfirst, dtype=torch.int64).view(-1, 1, 1, 1).expand(-1, 4, 4, 2).contiguous()
+    p2f[:, :, :, 1] = -1
+    loc = {"pix_to_face": p2f,
            "zbuf": torch.tensor(idx, dtype=torch.float32).view(-1, 1, 1, 1).expand(-1, 4, 4, 2).contiguous()}
-    out = gather_fragments(loc, shards, rank, world, root=0)
+    out = gather_fragments(loc, shards, rank, world, root=0, face_ids=(lfirst, gfirst[idx]))
     if rank == 0:
         result_q.put({k: v.numpy() for k, v in out.items()})
     dist.barrier()
@@ -64,5 +72,7 @@ def test_gather_fragments_gloo(world):
         p.join(timeout=120)
         assert p.exitcode == 0
     n = len(counts)
-    assert np.array_equal(res["pix_to_face"][:, 0, 0, 0], np.arange(n))
+    gfirst = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    assert np.array_equal(res["pix_to_face"][:, 0, 0, 0], gfirst)  # global packed ids on the root
+    assert np.all(res["pix_to_face"][:, :, :, 1] == -1)
     assert np.array_equal(res["zbuf"][:, 3, 3, 1], np.arange(n, dtype=np.float32))
