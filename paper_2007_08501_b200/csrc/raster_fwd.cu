@@ -331,6 +331,9 @@ constexpr int kPairQ = 64;  // < 32 pending + one enumeration step of 32
 #ifndef DR_LIST_PREFETCH
 #define DR_LIST_PREFETCH 1
 #endif
+#ifndef DR_EMIT_T
+#define DR_EMIT_T 1  // fragment emit with lanes over (pixel, slot) pairs: coalesced payload stores
+#endif
 #ifndef DR_T_REFRESH
 #define DR_T_REFRESH 1
 #endif
@@ -887,6 +890,46 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     __syncwarp();
     merge_buffers<KMAX>(ws, K, lane);
     __syncwarp();
+#if DR_EMIT_T
+    if constexpr (kMode == 0) {
+      // fragment payload (MR:178-197), lanes over (pixel, slot) in output order: q = (row * 8 + col) * K + s, so
+      // one step writes whole runs of consecutive slots of a micro-tile row (coalesced stores); the next step's
+      // face_verts are fetched before the current slot is evaluated
+      auto fetch = [&](int q, int32_t& f, double* v, int64_t& slot, double& z, double& qx, double& qy) {
+        f = INT_MAX;
+        slot = -1;
+        if (q >= 32 * K) return;
+        const int pix = q / K, s = q - pix * K;
+        const int row = pix >> 3, col = pix & 7;
+        if (row >= vh || col >= vw) return;
+        slot = (((int64_t)b * A.H + mi0 + row) * A.W + mj0 + col) * K + s;
+        f = ws.tid[s * 32 + pix];
+        z = ws.tz[s * 32 + pix];
+        qx = ws.pxy[col];
+        qy = ws.pxy[8 + row];
+        if (f != INT_MAX) {
+#pragma unroll
+          for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)f + t);
+        }
+      };
+      int32_t fn;
+      double vn[9], zn = 0.0, xn = 0.0, yn = 0.0;
+      int64_t sn;
+      fetch(lane, fn, vn, sn, zn, xn, yn);
+      for (int q0 = 0; q0 < 32 * K; q0 += 32) {
+        const int32_t f = fn;
+        const int64_t slot = sn;
+        const double z = zn, qx = xn, qy = yn;
+        double v[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) v[t] = vn[t];
+        fetch(q0 + 32 + lane, fn, vn, sn, zn, xn, yn);
+        if (slot >= 0) emit_slot<OutT>(A, slot, f != INT_MAX, z, f, v, qx, qy);
+      }
+      __syncwarp();
+      continue;
+    }
+#endif
     // emit this lane's pixel (MR:178-197); the next occupied slot's face_verts are fetched before the current
     // slot is evaluated so the global-load latency overlaps the fp64 work
     const int row = lane >> 3, col = lane & 7;
