@@ -75,3 +75,26 @@ def test_stress_bit_exact(seed, persp, K, blur, pc, clip, cull, bs, oracle, cuda
     if clip and seed % 5 != 0:
         both = occ[..., 1:] & occ[..., :-1]
         assert np.any((zb[..., 1:] == zb[..., :-1]) & both)
+
+
+@pytest.mark.parametrize("H,W,K", [(8192, 8192, 1), (1, 4096, 3), (4096, 1, 3), (3000, 17, 5)])
+def test_large_and_degenerate_image_shapes(H, W, K, oracle, cuda):
+    """Large (67M-pixel) and one-pixel-wide images: binned == naive bit for bit on the GPU; the small ones also vs
+    the oracle (index arithmetic, bin edges, micro-tile clipping)."""
+    from paper_2007_08501_b200 import rasterize_meshes
+
+    m, cam = S.ico_sphere(2), S.bench_camera()
+    fv, first, num = boundary(m, cam)
+    dev = lambda a: torch.as_tensor(a, device=cuda)  # noqa: E731
+    outs = []
+    for bs in (16, 0):
+        rs = raster_settings(H, K, 1e-4, cam, W=W, bin_size=bs)
+        outs.append([t.cpu().numpy() for t in rasterize_meshes(dev(fv), dev(first), dev(num), rs,
+                                                               out_dtype=torch.float64)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    assert (outs[0][0] >= 0).any()
+    if H * W <= 1 << 16:
+        want = oracle.forward(fv, first, num, orc_settings(H, K, 1e-4, cam, W=W))
+        for g, w in zip(outs[0], want):
+            assert np.array_equal(g, w)
