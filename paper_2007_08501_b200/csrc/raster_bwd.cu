@@ -64,9 +64,11 @@ __device__ __forceinline__ void load_slot(const BwdArgs<InT>& A, int64_t slot, i
 }
 
 // per-slot cotangents -> g[9] = (dx, dy, dz) for vertices a, b, c; p = the slot's pixel centre (MR:357)
-template <typename InT>
+// kInternalW: the clamped barycentrics used by the z-interpolation term are derived here from the recomputed
+// weights (and returned in w_out) instead of being read from the forward's bary output (fused consumers)
+template <typename InT, bool kInternalW = false>
 __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32_t fid, const SlotIn<InT>& in,
-                                              double g[9]) {
+                                              double g[9], double* w_out = nullptr) {
 #if DR_BWD_PREFETCH_FV
   const FaceGeom fg = make_face_geom(in.v);
 #else
@@ -78,7 +80,7 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32
 #endif
   const double z[3] = {fg.z0, fg.z1, fg.z2};
 
-  const double w_hat[3] = {(double)in.w[0], (double)in.w[1], (double)in.w[2]};
+  double w_hat[3] = {(double)in.w[0], (double)in.w[1], (double)in.w[2]};
   const double dz = (double)in.dz;
   // MR:363-365: cotangent on the clamped bary = direct input + z-interpolation path
   const double d_hat[3] = {(double)in.db[0] + dz * z[0], (double)in.db[1] + dz * z[1], (double)in.db[2] + dz * z[2]};
@@ -86,6 +88,26 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32
   double w_raw[3];
   barycentric<false>(fg, pa, pb, pc, w_raw);  // MR:366
   double d_w[3], dzv[3] = {0.0, 0.0, 0.0};
+  if constexpr (kInternalW) {  // w_hat = the forward's bary: clamp(persp(w_raw)) / clamp(w_raw) (MR:172)
+    double u[3];
+    if (A.persp) {
+      persp_correct<false>(w_raw, fg.z0, fg.z1, fg.z2, u);
+    } else {
+      u[0] = w_raw[0];
+      u[1] = w_raw[1];
+      u[2] = w_raw[2];
+    }
+    if (A.clip) {
+      clamp_barycentric<false>(u, w_hat);
+    } else {
+      w_hat[0] = u[0];
+      w_hat[1] = u[1];
+      w_hat[2] = u[2];
+    }
+    w_out[0] = w_hat[0];
+    w_out[1] = w_hat[1];
+    w_out[2] = w_hat[2];
+  }
   if (A.persp) {  // builder-defined: u = persp_correct(w_raw, z); bary = clamp(u)
     double u[3], d_u[3], d_top[3];
     const double den = persp_correct<false>(w_raw, fg.z0, fg.z1, fg.z2, u);
@@ -522,7 +544,7 @@ __device__ __forceinline__ double blend_zinv_b(double z, const BlendArgs& bl, bo
   return (bl.zfar - zc) / (bl.zfar - bl.znear);
 }
 
-__global__ void __launch_bounds__(kSoftThreads) k_softmax_backward(SoftBwdArgs A) {
+__global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArgs A) {
   extern __shared__ double soft_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
@@ -647,29 +669,27 @@ __global__ void __launch_bounds__(kSoftThreads) k_softmax_backward(SoftBwdArgs A
         double d_zbuf = clamped ? 0.0 : d_zinv * (-1.0 / zrange);
         if (s == argmax && !clamped) d_zbuf += d_zinv_max * (-1.0 / zrange);
         // interpolate_face_attributes_backward (shading.cpp:46-72): d_bary_i = d_col . a_i, d_attr_i += w_i d_col
-        double v[9];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)fid + t);
-        const FaceGeom fg = make_face_geom(v);
-        PixelFaceResult r;
-        eval_pixel_face<true, false>(p, fg, A.blur, A.znear, A.persp, A.clip, r);
         SlotIn<double> in;
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)fid + q];
           in.db[q] = d_col[0] * __ldg(a) + d_col[1] * __ldg(a + 1) + d_col[2] * __ldg(a + 2);
-          in.w[q] = r.bary[q];
-          gc[3 * q + 0] = r.bary[q] * d_col[0];
-          gc[3 * q + 1] = r.bary[q] * d_col[1];
-          gc[3 * q + 2] = r.bary[q] * d_col[2];
+          in.w[q] = 0.0;
         }
         in.dz = d_zbuf;
         in.dd = d_dists;
 #if DR_BWD_PREFETCH_FV
 #pragma unroll
-        for (int t = 0; t < 9; ++t) in.v[t] = v[t];
+        for (int t = 0; t < 9; ++t) in.v[t] = __ldg(A.fv + 9 * (int64_t)fid + t);
 #endif
-        slot_backward(BA, p, fid, in, g);
+        double wh[3];
+        slot_backward<double, true>(BA, p, fid, in, g, wh);  // the slot's clamped barycentrics come back in wh
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          gc[3 * q + 0] = wh[q] * d_col[0];
+          gc[3 * q + 1] = wh[q] * d_col[1];
+          gc[3 * q + 2] = wh[q] * d_col[2];
+        }
       }
       // one reduction over 18 values: the face_verts cotangent and the face's vertex-colour cotangents
       double gg[18];
