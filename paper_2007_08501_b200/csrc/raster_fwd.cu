@@ -186,29 +186,79 @@ __global__ void __launch_bounds__(256) k_bin_faces(const int4* __restrict__ ibbo
   }
 }
 
-// exclusive scan of the bin counts (one CTA; N * bins is at most a few million)
+// exclusive scan of the bin counts without extra workspace: (1) every CTA scans a segment of kScanSeg counts
+// locally (exclusive, into off); (2) every CTA adds the sum of all earlier segments to its elements except the
+// segment's last one — it reads those sums back as off[last] + counts[last] of each earlier segment, values no
+// block of this pass modifies; (3) one thread walks the segments and fixes their last elements in order.
 constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads) k_scan_bins(const int* __restrict__ counts, int64_t n,
-                                                            int64_t* __restrict__ off) {
-  __shared__ int64_t part[kScanThreads];
-  const int t = threadIdx.x;
-  const int64_t per = (n + kScanThreads - 1) / kScanThreads;
-  const int64_t lo = min(n, (int64_t)t * per), hi = min(n, lo + per);
+constexpr int kScanPer = 4;
+constexpr int kScanSeg = kScanThreads * kScanPer;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_local(const int* __restrict__ counts, int64_t n,
+                                                             int64_t* __restrict__ off) {
+  __shared__ int64_t warp_tot[kScanThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kScanSeg + (int64_t)t * kScanPer;
+  int c[kScanPer];
   int64_t sum = 0;
-#pragma unroll 8
-  for (int64_t i = lo; i < hi; ++i) sum += counts[i];
-  part[t] = sum;
+#pragma unroll
+  for (int u = 0; u < kScanPer; ++u) {
+    c[u] = base + u < n ? counts[base + u] : 0;
+    sum += c[u];
+  }
+  int64_t incl = sum;  // warp inclusive scan of the per-thread sums
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) warp_tot[w] = incl;
   __syncthreads();
-  for (int d = 1; d < kScanThreads; d <<= 1) {  // Hillis-Steele inclusive scan of the partial sums
-    const int64_t v = t >= d ? part[t - d] : 0;
-    __syncthreads();
-    part[t] += v;
+  if (w == 0) {
+    int64_t x = warp_tot[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t v = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += v;
+    }
+    warp_tot[lane] = x;
+  }
+  __syncthreads();
+  int64_t run = incl - sum + (w > 0 ? warp_tot[w - 1] : 0);
+#pragma unroll
+  for (int u = 0; u < kScanPer; ++u) {
+    if (base + u < n) off[base + u] = run;
+    run += c[u];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scan_fix(const int* __restrict__ counts, int64_t n,
+                                                  int64_t* __restrict__ off) {
+  __shared__ int64_t red[256];
+  const int seg = blockIdx.x;
+  if (seg == 0) return;
+  int64_t s = 0;
+  for (int q = threadIdx.x; q < seg; q += 256) {  // totals of the earlier segments
+    const int64_t last = (int64_t)(q + 1) * kScanSeg - 1;
+    s += off[last] + counts[last];
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int d = 128; d > 0; d >>= 1) {
+    if (threadIdx.x < d) red[threadIdx.x] += red[threadIdx.x + d];
     __syncthreads();
   }
-  int64_t run = part[t] - sum;
-  for (int64_t i = lo; i < hi; ++i) {
-    off[i] = run;
-    run += counts[i];
+  const int64_t prefix = red[0];
+  const int64_t lo = (int64_t)seg * kScanSeg, hi = min(n, lo + kScanSeg - 1);  // the last element: k_scan_last
+  for (int64_t i = lo + threadIdx.x; i < hi; i += 256) off[i] += prefix;
+}
+
+__global__ void k_scan_last(const int* __restrict__ counts, int64_t n, int64_t* __restrict__ off) {
+  int64_t prefix = 0;
+  for (int64_t last = kScanSeg - 1; last < n; last += kScanSeg) {
+    const int64_t tot = off[last] + counts[last];  // still the segment-local value
+    off[last] += prefix;
+    prefix += tot;
   }
 }
 
@@ -1023,7 +1073,12 @@ void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* nu
 
 void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cudaStream_t st) {
   if (nbins_total <= 0) return;
-  k_scan_bins<<<1, kScanThreads, 0, st>>>(counts, nbins_total, off);
+  const unsigned nseg = (unsigned)((nbins_total + kScanSeg - 1) / kScanSeg);
+  k_scan_local<<<nseg, kScanThreads, 0, st>>>(counts, nbins_total, off);
+  if (nseg > 1) {
+    k_scan_fix<<<nseg, 256, 0, st>>>(counts, nbins_total, off);
+    k_scan_last<<<1, 1, 0, st>>>(counts, nbins_total, off);
+  }
 }
 
 void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
