@@ -381,6 +381,9 @@ constexpr int kPairQ = 64;  // < 32 pending + one enumeration step of 32
 #ifndef DR_LIST_PREFETCH
 #define DR_LIST_PREFETCH 1
 #endif
+#ifndef DR_EARLY_EXIT
+#define DR_EARLY_EXIT 0  // measured: the per-chunk exit test costs more than the chunks it skips
+#endif
 #ifndef DR_EMIT_T
 #define DR_EMIT_T 1  // fragment emit with lanes over (pixel, slot) pairs: coalesced payload stores
 #endif
@@ -870,7 +873,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 #if DR_LIST_PREFETCH
       const int4 e_cur = e_next;
       if (list && ci + 32 < nsrc) e_next = list[ci + 32];
-      if (sorted && (double)__int_as_float(__shfl_sync(0xffffffffu, e_cur.y, 0)) > T) {
+      if (DR_EARLY_EXIT && sorted && (double)__int_as_float(__shfl_sync(0xffffffffu, e_cur.y, 0)) > T) {
 #else
       if (sorted && (double)__int_as_float(list[c0].y) > T) {
 #endif
