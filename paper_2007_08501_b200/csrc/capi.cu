@@ -258,7 +258,11 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
       drb::launch_fill_bins(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool,
                             p.zsort ? zkey : nullptr, entries, st);
     }
-    if (p.zsort) {
+    static const bool sort_on = [] {  // DR_SORT=0: keep the fill order (A/B of the depth ordering)
+      const char* e = std::getenv("DR_SORT");
+      return !(e && e[0] == '0');
+    }();
+    if (p.zsort && sort_on) {
       ProfScope ps(st, KN_SORT);
       cudaError_t e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, p.cap, st);
       if (e != cudaSuccess) return cuda_fail(e, "sorting bins");
