@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-groups", type=int, default=16, help="mesh groups the host pipeline streams")
+    ap.add_argument("--e2e-groups", type=int, default=24, help="mesh groups the host pipeline streams")
+    ap.add_argument("--e2e-lookahead", type=int, default=3, help="H2D of group g waits for D2H of g - L (0: off)")
+    ap.add_argument("--e2e-ramp", type=int, default=2, help="smaller first/last pipeline groups (HostPipeline ramp)")
     ap.add_argument("--cpu-sample-faces", type=float, default=0.25,
                     help="fraction of the batch's faces the CPU sample covers")
     return ap.parse_args()
@@ -373,7 +375,8 @@ def main():
 
         del ws  # the pipeline owns its own device buffers
         torch.cuda.empty_cache()
-        pipe = HostPipeline(first_np, num_np, rs, F, dev, n_groups=args.e2e_groups, backward=c["backward"])
+        pipe = HostPipeline(first_np, num_np, rs, F, dev, n_groups=args.e2e_groups, backward=c["backward"],
+                            ramp=args.e2e_ramp, lookahead=args.e2e_lookahead)
         h_fv = torch.from_numpy(fv_np).pin_memory()
         cot_h = tuple(t.cpu().pin_memory() for t in (dz, db, dd)) if c["backward"] else None
         out_h = (torch.empty((N, H, W, K), dtype=torch.int64).pin_memory(),
@@ -398,7 +401,7 @@ def main():
             ems = float(t.item())
         e2e = {"value": total_fpx / (ems * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "pcie_gbs": (h2d + d2h) / (ems * 1e-3) / 1e9, "groups": len(pipe.groups),
+               "pcie_gbs": (h2d + d2h) / (ems * 1e-3) / 1e9, "groups": len(pipe.groups), "ramp": args.e2e_ramp, "lookahead": args.e2e_lookahead,
                "api": "paper_2007_08501_b200.pipeline.HostPipeline.run (pinned host in/out)"}
 
     cpu = None

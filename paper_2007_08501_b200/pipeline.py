@@ -22,26 +22,39 @@ import torch
 from .raster import RasterSettings, rasterize_meshes, rasterize_meshes_backward, workspace_bytes
 
 
-def contiguous_groups(num_faces_per_mesh, n_groups: int) -> list:
-    """Split meshes 0..N-1 into <= n_groups contiguous runs of roughly equal face count."""
-    counts = np.asarray(num_faces_per_mesh, dtype=np.int64)
+def contiguous_groups(costs, n_groups: int, ramp: int = 0) -> list:
+    """Split items 0..N-1 into <= n_groups contiguous runs of roughly equal total cost. ``ramp`` > 0 makes the
+    first and last ``ramp`` groups geometrically smaller (1/2, 1/4, ... of a full one): the pipeline's fill (the
+    first group's H2D + kernels, before any D2H) and drain (the last group's D2H) then run on small groups."""
+    counts = np.asarray(costs, dtype=np.float64)
     n = len(counts)
     n_groups = max(1, min(n_groups, n))
-    target = counts.sum() / n_groups
-    groups, start, acc = [], 0, 0
+    r = max(0, min(ramp, (n_groups - 1) // 2))
+    rel = np.ones(n_groups)
+    for i in range(r):
+        rel[r - 1 - i] = rel[n_groups - r + i] = 0.5 ** (i + 1)
+    bounds = np.cumsum(rel) / rel.sum() * counts.sum()
+    groups, start, acc = [], 0, 0.0
     for b in range(n):
         acc += counts[b]
-        if (acc >= target * (len(groups) + 1) and len(groups) < n_groups - 1) or b == n - 1:
+        if (acc >= bounds[len(groups)] - 1e-9 * counts.sum() and len(groups) < n_groups - 1) or b == n - 1:
             groups.append((start, b + 1))
             start = b + 1
     return [g for g in groups if g[1] > g[0]]
+
+
+def transfer_costs(num_faces_per_mesh, hw_k: int, backward: bool) -> np.ndarray:
+    """PCIe bytes per mesh of one e2e step: face_verts in (72 B/face) + fragments out (28 B/slot), and with the
+    backward cotangents in (20 B/slot) + grad_face_verts out (72 B/face)."""
+    f = np.asarray(num_faces_per_mesh, dtype=np.float64)
+    return 72.0 * f * (2 if backward else 1) + (48.0 if backward else 28.0) * hw_k
 
 
 class HostPipeline:
     """Streams forward (+ backward) of a fixed batch layout between pinned host buffers and the GPU."""
 
     def __init__(self, first, num, settings: RasterSettings, num_faces: int, device, n_groups: int = 8,
-                 backward: bool = True):
+                 backward: bool = True, ramp: int = 2, lookahead: int = 3):
         self.first = np.asarray(first, dtype=np.int64)
         self.num = np.asarray(num, dtype=np.int64)
         order = np.argsort(self.first, kind="stable")
@@ -52,9 +65,11 @@ class HostPipeline:
         self.N = len(self.num)
         self.dev = torch.device(device)
         self.backward = backward
+        self.lookahead = int(lookahead)  # 0: every H2D enqueued at once
         H, W = settings.hw
         K = settings.faces_per_pixel
-        self.groups = contiguous_groups(self.num, n_groups)
+        # groups balance PCIe bytes (the e2e bound), not faces: a mesh's slots cost as much as ~0.5M faces
+        self.groups = contiguous_groups(transfer_costs(self.num, H * W * K, backward), n_groups, ramp)
         d = self.dev
         self.fv = torch.empty((self.F, 3, 3), dtype=torch.float64, device=d)
         self.p2f = torch.empty((self.N, H, W, K), dtype=torch.int64, device=d)
@@ -84,23 +99,24 @@ class HostPipeline:
         main = torch.cuda.current_stream(self.dev)
         for st in (self.h2d, self.comp, self.d2h):
             st.wait_stream(main)
-        # all host->device copies are enqueued first (one event per group); the compute stream consumes them in
-        # order and the device->host stream drains each group as soon as its kernels are done. The *_hr entry
-        # points take host copies of the mesh ranges, so no call synchronises and the host runs ahead.
-        ev_in = []
-        for g0, g1 in self.groups:
+        # per group: H2D on h2d, kernels on comp, D2H on d2h. The device->host direction carries more bytes than
+        # the host->device one (fragments 28 B/slot vs cotangents 20 B/slot), and the two directions share the
+        # link's bidirectional budget: group g's H2D waits for the D2H of group g - lookahead, so the inputs arrive
+        # just in time instead of taking half the link while the outputs queue. The *_hr entry points take host
+        # copies of the mesh ranges, so no call synchronises and the host runs ahead.
+        ev_d2h = []
+        for gi, (g0, g1) in enumerate(self.groups):
             lo, hi = self.face_range(g0, g1)
+            if self.lookahead > 0 and gi >= self.lookahead:
+                self.h2d.wait_event(ev_d2h[gi - self.lookahead])
             with torch.cuda.stream(self.h2d):
                 self.fv[lo:hi].copy_(fv_h[lo:hi], non_blocking=True)
                 if self.backward:
                     for d, h in zip((self.dz, self.db, self.dd), cot_h):
                         d[g0:g1].copy_(h[g0:g1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(self.h2d)
-                ev_in.append(ev)
-        for gi, (g0, g1) in enumerate(self.groups):
-            lo, hi = self.face_range(g0, g1)
-            self.comp.wait_event(ev_in[gi])
+                ev_in = torch.cuda.Event()
+                ev_in.record(self.h2d)
+            self.comp.wait_event(ev_in)
             with torch.cuda.stream(self.comp):
                 outs = (self.p2f[g0:g1], self.zbuf[g0:g1], self.bary[g0:g1], self.dists[g0:g1])
                 rasterize_meshes(self.fv, self.g_first[gi], self.g_num[gi], self.s, workspace=self.ws, out=outs,
@@ -121,5 +137,8 @@ class HostPipeline:
                 self.d2h.wait_event(ev_out)
                 with torch.cuda.stream(self.d2h):
                     grad_h[lo:hi].copy_(self.grad[lo:hi], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.d2h)
+            ev_d2h.append(ev)
         for st in (self.h2d, self.comp, self.d2h):
             main.wait_stream(st)
