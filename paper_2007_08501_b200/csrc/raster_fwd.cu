@@ -714,6 +714,14 @@ __device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane)
   }
 }
 
+#ifndef DR_OVF_NOINLINE
+#define DR_OVF_NOINLINE 0
+#endif
+template <int KMAX>
+__device__ __noinline__ void merge_buffers_ool(const WarpSmem& ws, int K, int lane) {
+  merge_buffers<KMAX>(ws, K, lane);
+}
+
 // Append a passing candidate to its pixel's buffer (merging every buffer first if one would overflow).
 template <int KMAX, typename OutT>
 __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const WarpSmem& ws, bool pass, int p,
@@ -727,7 +735,11 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
     int base = pass ? ws.bcnt[p] : 0;
     if (__any_sync(0xffffffffu, pass && base + n_same > kBuf)) {
       __syncwarp();
+#if DR_OVF_NOINLINE
+      merge_buffers_ool<KMAX>(ws, K, lane);
+#else
       merge_buffers<KMAX>(ws, K, lane);
+#endif
       __syncwarp();
       base = 0;
     }
@@ -989,20 +1001,25 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
           pending -= G;
           ran = true;
         }
-        if (A.zsort && ran) {  // refresh T: merge the buffered candidates, then max of the K-th depths
-          // (every DR_T_REFRESH groups; the list tails alone are a valid, looser threshold in between)
-          if (++groups % DR_T_REFRESH == 0) {
+        if (ran) {  // merge the buffered candidates (the only merge site besides a buffer overflow), refresh T
+#if DR_T_REFRESH > 1
+          if (++groups % DR_T_REFRESH == 0 || (last && todo == 0u))
+#endif
+          {
             __syncwarp();
             merge_buffers<KMAX>(ws, K, lane);
             __syncwarp();
           }
-          double t = valid_px ? ws.tz[(K - 1) * 32 + lane] : -pos_inf();
+          if (A.zsort) {  // max of the K-th depths (the list tails alone are a valid, looser threshold)
+            double t = valid_px ? ws.tz[(K - 1) * 32 + lane] : -pos_inf();
 #pragma unroll
-          for (int d = 16; d >= 1; d >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, d));
-          T = t;
+            for (int d = 16; d >= 1; d >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, d));
+            T = t;
+          }
         }
       } while (todo);
     }
+#if DR_EARLY_EXIT
     while (pending > 0) {  // faces staged before an early exit
       const int G = min(pending, 32);
       process_group<KMAX>(A, ws, head, G, lane);
@@ -1011,6 +1028,8 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     }
     __syncwarp();
     merge_buffers<KMAX>(ws, K, lane);
+#endif
+    // every group's candidates were merged after it ran: the buffers are empty here
     __syncwarp();
 #if DR_EMIT_T
     if constexpr (kMode == 0) {
