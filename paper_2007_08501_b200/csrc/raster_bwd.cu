@@ -218,11 +218,12 @@ constexpr int kBwdChunk = 32 * 16;
 #define DR_BWD_CHUNKS_PER_WARP 4
 #endif
 #ifndef DR_BWD_MINBLOCKS
-#define DR_BWD_MINBLOCKS 4
+#define DR_BWD_MINBLOCKS 3
 #endif
-// 128-thread CTAs, 4 per SM (128 registers, no spills): with the chunk-wide pix_to_face loads and the
+// 128-thread CTAs, 3 per SM (155 registers, no spills): with the cp.async pix_to_face prefetch and the
 // one-batch-ahead input loads, latency is hidden by ILP rather than by more resident warps (C4: 80 registers x
-// 24 warps 3.47 ms, 96 x 20 3.33 ms, 128 x 16 3.10 ms; profiles/r01/README.md).
+// 24 warps 3.47 ms, 96 x 20 3.33 ms, 128 x 16 3.10 ms with the first design; with the prefetching one
+// 128 x 16 (36-byte spills) 2.54 ms, 155 x 12 2.48 ms; profiles/r01/README.md).
 constexpr int kBwdThreads = DR_BWD_THREADS;
 
 template <typename InT>
@@ -248,6 +249,129 @@ __device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, V2 p, int3
 // bary / cotangents loaded before the current step computes.
 constexpr int kPixTab = 2048;  // pixel-centre tables in shared memory when H + W fits
 
+#ifndef DR_BWD_V2
+#define DR_BWD_V2 1
+#endif
+#ifndef DR_BWD_CHUNKS_PER_CTA
+#define DR_BWD_CHUNKS_PER_CTA 32
+#endif
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <typename InT>
+__device__ __forceinline__ void backward_chunk(const BwdArgs<InT>& A, int64_t c0, int n, const uint16_t* qo,
+                                               const int32_t* qf, const double* pix_tab, bool tab, int lane) {
+  const int HW = A.H * A.W;
+  // slot -> pixel with one 64-bit division per chunk; 32-bit arithmetic per slot
+  const int64_t pix0 = c0 / A.K;
+  const int r0 = (int)(c0 - pix0 * A.K);
+  const int pp0 = (int)(pix0 % HW);
+  SlotIn<InT> nxt;
+  int32_t nfid = -1;
+  int noff = 0;
+  if (lane < n) {
+    noff = qo[lane];
+    nfid = qf[lane];
+    load_slot(A, c0 + noff, nfid, nxt);
+  }
+  for (int q0 = 0; q0 < n; q0 += 32) {
+    const SlotIn<InT> cur = nxt;
+    const int32_t my_fid = nfid;
+    const int off = noff;
+    nfid = -1;
+    if (q0 + 32 + lane < n) {
+      noff = qo[q0 + 32 + lane];
+      nfid = qf[q0 + 32 + lane];
+      load_slot(A, c0 + noff, nfid, nxt);
+    }
+    V2 p{0.0, 0.0};
+    if (my_fid >= 0) {
+      uint32_t pp = (uint32_t)pp0 + A.divK.div((uint32_t)(r0 + off));
+      if (pp >= (uint32_t)HW) pp %= (uint32_t)HW;  // the chunk crossed into the next image
+      const uint32_t i = A.divW.div(pp), j = pp - i * (uint32_t)A.W;
+      p = tab ? V2{pix_tab[j], pix_tab[A.W + i]} : V2{pixel_x(A.W, (int)j), pixel_y(A.H, (int)i)};  // MR:357
+    }
+    backward_batch(A, p, my_fid, cur, lane);
+  }
+}
+
+#if DR_BWD_V2
+// CTA = DR_BWD_CHUNKS_PER_CTA consecutive chunks; its warps take chunks from a shared counter (so they finish
+// together and the CTA's registers are released without idle warps holding them). While a warp computes chunk
+// c, the pix_to_face words of its next chunk stream into shared memory with cp.async (no registers held);
+// the chunk is then compacted (occupied slots -> queue of 16-bit offsets + face ids) straight from shared memory.
+template <typename InT>
+__global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdArgs<InT> A) {
+  constexpr int NWB = kBwdThreads / 32;
+  __shared__ __align__(16) int64_t stage[NWB][kBwdChunk];
+  __shared__ int32_t q_fid[NWB][kBwdChunk];
+  __shared__ uint16_t q_off[NWB][kBwdChunk];
+  __shared__ double pix_tab[kPixTab];  // pixel_x(W, j) for j < W, then pixel_y(H, i) (camera.cpp:100-102)
+  __shared__ int next_chunk;
+  const bool tab = A.W + A.H <= kPixTab;
+  if (threadIdx.x == 0) next_chunk = NWB;  // chunk w is warp w's first
+  if (tab)
+    for (int t = threadIdx.x; t < A.W + A.H; t += kBwdThreads)
+      pix_tab[t] = t < A.W ? pixel_x(A.W, t) : pixel_y(A.H, t - A.W);
+  __syncthreads();
+  constexpr int kSteps = kBwdChunk / 32;
+  // chunk k of this CTA starts at slot chunk0(k); valid while k < DR_BWD_CHUNKS_PER_CTA and it starts before S
+  // (only k is carried across the chunk's compute: everything else is recomputed, to stay spill-free)
+  auto chunk0 = [&](int k) {
+    return ((int64_t)blockIdx.x * DR_BWD_CHUNKS_PER_CTA + k) * kBwdChunk;
+  };
+  auto valid = [&](int k) { return k < DR_BWD_CHUNKS_PER_CTA && chunk0(k) < A.S; };
+  auto issue = [&](int k) {  // start the copy of chunk k's pix_to_face words (slots past S are not copied)
+    const int lane = threadIdx.x & 31;
+    const int64_t c0 = chunk0(k);
+    int64_t* stg = stage[threadIdx.x >> 5];
+#pragma unroll
+    for (int t = 0; t < kSteps; ++t) {
+      const int64_t slot = c0 + t * 32 + lane;
+      if (slot < A.S) cp_async8(stg + t * 32 + lane, A.p2f + slot);
+    }
+    cp_async_commit();
+  };
+  int k = threadIdx.x >> 5;
+  if (valid(k)) issue(k);
+  while (valid(k)) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c0 = chunk0(k);
+    const int64_t* stg = stage[wid];
+    uint16_t* qo = q_off[wid];
+    int32_t* qf = q_fid[wid];
+    cp_async_wait_all();
+    __syncwarp();
+    int n = 0;
+#pragma unroll 4
+    for (int t = 0; t < kSteps; ++t) {
+      const int64_t slot = c0 + t * 32 + lane;
+      const int64_t f = slot < A.S ? stg[t * 32 + lane] : -1;
+      const bool occ = f >= 0 && f < A.F;
+      const unsigned m = __ballot_sync(0xffffffffu, occ);
+      if (occ) {
+        const int pos = n + __popc(m & ((1u << lane) - 1u));
+        qo[pos] = (uint16_t)(t * 32 + lane);
+        qf[pos] = (int32_t)f;
+      }
+      n += __popc(m);
+    }
+    __syncwarp();
+    int kn = 0;
+    if (lane == 0) kn = atomicAdd(&next_chunk, 1);
+    kn = __shfl_sync(0xffffffffu, kn, 0);
+    if (valid(kn)) issue(kn);  // overlaps this chunk's compute
+    backward_chunk(A, c0, n, qo, qf, pix_tab, A.W + A.H <= kPixTab, lane);
+    __syncwarp();
+    k = kn;
+  }
+}
+#else
 template <typename InT>
 __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdArgs<InT> A) {
   __shared__ int32_t q_off[kBwdThreads / 32][kBwdChunk];
@@ -320,6 +444,8 @@ __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdA
     __syncwarp();
   }
 }
+
+#endif
 
 // ------------------------------------------------------------------------------------------------
 // Fused silhouette backward: silhouette_blend_backward (shading.cpp:93-121) feeding rasterize_backward
@@ -742,7 +868,11 @@ static cudaError_t launch_backward_t(const BwdArgs<InT>& A, cudaStream_t st) {
   // many short-lived CTAs (~DR_BWD_CHUNKS_PER_WARP chunks per warp) instead of one persistent wave: the block
   // scheduler then balances the uneven per-chunk work (occupied-slot density varies across the image); a single
   // wave measured 10.8 of 16 achievable warps per SM on C4
+#if DR_BWD_V2
+  const int64_t per_cta = (int64_t)kBwdChunk * DR_BWD_CHUNKS_PER_CTA;
+#else
   const int64_t per_cta = (int64_t)(kBwdThreads / 32) * kBwdChunk * DR_BWD_CHUNKS_PER_WARP;
+#endif
   const int64_t blocks = std::min<int64_t>((A.S + per_cta - 1) / per_cta, INT32_MAX);
   k_backward<InT><<<(unsigned)blocks, kBwdThreads, 0, st>>>(A);
   return cudaGetLastError();
