@@ -185,6 +185,17 @@ int dr_rasterize_silhouette_bwd(const double* face_verts, const int64_t* mesh_to
                                 const int64_t* num_faces_per_mesh, int64_t N, int64_t F, const dr_raster_settings* s,
                                 double sigma, const int64_t* pix_to_face, const float* grad_alpha,
                                 double* grad_face_verts, dr_stream_t stream);
+/* fp64 alpha / fp64 cotangent variants (the fit loop, pipeline.cpp:100-205, where Adam's per-coordinate
+ * normalisation amplifies fp32 rounding in near-zero gradients): alpha matches silhouette_blend of the fp64
+ * MeshFragments to a few ulps; the backward evaluates the sigmoid in fp64. */
+int dr_rasterize_silhouette_fwd_f64(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                                    const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
+                                    const dr_raster_settings* s, double sigma, int64_t* pix_to_face, double* alpha,
+                                    void* workspace, size_t workspace_bytes, dr_stream_t stream);
+int dr_rasterize_silhouette_bwd_f64(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                                    const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
+                                    const dr_raster_settings* s, double sigma, const int64_t* pix_to_face,
+                                    const double* grad_alpha, double* grad_face_verts, dr_stream_t stream);
 
 /* ---- fused fragment consumer: softmax render ----
  * The reference's differentiable softmax render (grad.cpp:177-209): rasterize_meshes -> interpolate_face_attributes

@@ -235,6 +235,9 @@ class RefLib:
         L.ref_barycentric.argtypes = [_dp] * 5
         L.ref_clamp_barycentric.argtypes = [_dp, _dp]
         L.ref_point_triangle_dist2_backward.argtypes = [_dp, _dp, _dp, _dp, C.c_double, _dp]
+        L.ref_fit_silhouette.argtypes = [C.c_char_p, _i32p, _dp, _dp, _dp, _dp, C.c_int64, _i64p]
+        L.ref_mesh_losses.argtypes = [C.c_void_p, _dp, _dp, _dp]
+        L.ref_silhouette_iou.argtypes = [_dp, _dp, C.c_int64, C.c_double, _dp, _dp]
 
     def set_num_threads(self, n: int):
         self.lib.ref_set_num_threads(n)
@@ -378,3 +381,40 @@ class RefLib:
                                                   _p(out, _dp)):
             raise RuntimeError(self.lib.ref_last_error().decode())
         return out
+
+    # fit_silhouette (pipeline.cpp:100-205) and its losses (geometry.cpp:556-682)
+    def fit_silhouette(self, cfg):
+        """cfg: any object with the FitConfig fields (pipeline.hpp:56-78). Returns (trace [iters,5], final loss,
+        fitted verts [V,3])."""
+        ci = np.array([cfg.template_level, cfg.num_views, cfg.iterations, cfg.image_size, cfg.faces_per_pixel],
+                      np.int32)
+        cd = np.array([cfg.target_scale, cfg.step_size, cfg.lambda_laplacian, cfg.lambda_edge, cfg.coarse_blur_radius,
+                       cfg.coarse_sigma, cfg.coarse_fraction, cfg.blur_radius, cfg.sigma, cfg.camera_distance,
+                       cfg.focal_length], np.float64)
+        trace = np.zeros((max(cfg.iterations, 0), 5), np.float64)
+        vcap = 10 * 4 ** (max(cfg.template_level, 0) + 1) + 2  # ico_sphere(l): 20 * 4^(l+1) faces
+        verts = np.zeros((vcap, 3), np.float64)
+        fl = np.zeros(1, np.float64)
+        nv = np.zeros(1, np.int64)
+        if self.lib.ref_fit_silhouette(cfg.target_spec.encode(), _p(ci, _i32p), _p(cd, _dp), _p(trace, _dp),
+                                       _p(fl, _dp), _p(verts, _dp), vcap, _p(nv, _i64p)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return trace, float(fl[0]), verts[: int(nv[0])]
+
+    def mesh_losses(self, batch: RefBatch, n_verts: int):
+        """(edge_length_loss mean, laplacian_loss mean, d_edge [V,3], d_lap [V,3]) for d_mean = 1."""
+        out = np.zeros(2)
+        de = np.zeros((n_verts, 3))
+        dl = np.zeros((n_verts, 3))
+        if self.lib.ref_mesh_losses(batch.h, _p(out, _dp), _p(de, _dp), _p(dl, _dp)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return float(out[0]), float(out[1]), de, dl
+
+    def silhouette_iou(self, pred, gt, d_loss=1.0):
+        p = np.ascontiguousarray(pred, np.float64).reshape(-1)
+        g = np.ascontiguousarray(gt, np.float64).reshape(-1)
+        loss = np.zeros(1)
+        grad = np.zeros_like(p)
+        if self.lib.ref_silhouette_iou(_p(p, _dp), _p(g, _dp), p.size, d_loss, _p(loss, _dp), _p(grad, _dp)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return float(loss[0]), grad

@@ -11,6 +11,8 @@
 //   dr::silhouette_blend / silhouette_blend_backward (shading.hpp:37-41)
 //   the softmax render op of grad.cpp:177-209 (interpolate_face_attributes + softmax_blend and their backwards)
 //   dr::rasterize_points / _naive, splat_position_backward (point_render.hpp:33-36, 66-68)
+//   dr::fit_silhouette (pipeline.hpp:91-95, pipeline.cpp:100-205) and its regularizers / loss
+//   (geometry.hpp:96-107)
 // Errors are caught and reported through ref_last_error() (the reference throws).
 #include <cstdint>
 #include <cstring>
@@ -21,7 +23,9 @@
 #include "dr/batching.hpp"
 #include "dr/camera.hpp"
 #include "dr/core.hpp"
+#include "dr/geometry.hpp"
 #include "dr/mesh_raster.hpp"
+#include "dr/pipeline.hpp"
 #include "dr/point_render.hpp"
 #include "dr/shading.hpp"
 #include "dr/templates.hpp"
@@ -387,4 +391,83 @@ void ref_point_triangle_dist2_backward(const double* p, const double* a, const d
                                     dc);
   g6[0] = da.x; g6[1] = da.y; g6[2] = db.x; g6[3] = db.y; g6[4] = dc.x; g6[5] = dc.y;
 }
+// ---- fit_silhouette (pipeline.cpp:100-205) ----
+// cfg_i: [template_level, num_views, iterations, image_size, faces_per_pixel]
+// cfg_d: [target_scale, step_size, lambda_laplacian, lambda_edge, coarse_blur_radius, coarse_sigma,
+//         coarse_fraction, blur_radius, sigma, camera_distance, focal_length]
+// trace: [iterations, 5] (iter, l_s, l_l, l_e, total); verts_out: the fitted packed verts [V,3] (V <= vcap)
+int ref_fit_silhouette(const char* target_spec, const int32_t* ci, const double* cd, double* trace, double* final_loss,
+                       double* verts_out, int64_t vcap, int64_t* nverts) {
+  return guarded([&] {
+    dr::FitConfig c;
+    c.target_spec = target_spec;
+    c.template_level = ci[0];
+    c.num_views = ci[1];
+    c.iterations = ci[2];
+    c.image_size = ci[3];
+    c.faces_per_pixel = ci[4];
+    c.target_scale = cd[0];
+    c.step_size = cd[1];
+    c.lambda_laplacian = cd[2];
+    c.lambda_edge = cd[3];
+    c.coarse_blur_radius = cd[4];
+    c.coarse_sigma = cd[5];
+    c.coarse_fraction = cd[6];
+    c.blur_radius = cd[7];
+    c.sigma = cd[8];
+    c.camera_distance = cd[9];
+    c.focal_length = cd[10];
+    dr::FitResult r = dr::fit_silhouette(c);
+    for (size_t i = 0; i < r.trace.size(); ++i) {
+      const auto& t = r.trace[i];
+      trace[5 * i] = t.iter;
+      trace[5 * i + 1] = t.l_s;
+      trace[5 * i + 2] = t.l_l;
+      trace[5 * i + 3] = t.l_e;
+      trace[5 * i + 4] = t.total;
+    }
+    *final_loss = r.final_silhouette_loss;
+    const auto& v = r.mesh.verts_packed().data;
+    *nverts = int64_t(v.size());
+    for (size_t i = 0; i < v.size() && int64_t(i) < vcap; ++i) {
+      verts_out[3 * i] = v[i].x;
+      verts_out[3 * i + 1] = v[i].y;
+      verts_out[3 * i + 2] = v[i].z;
+    }
+  });
+}
+
+// mesh regularizers of a batch: out2 = [edge_length_loss mean, laplacian_loss mean]; d_edge / d_lap [V,3] for
+// d_mean = 1 (geometry.cpp:556-649)
+int ref_mesh_losses(void* h, double* out2, double* d_edge, double* d_lap) {
+  return guarded([&] {
+    const auto& m = *static_cast<dr::MeshBatch*>(h);
+    out2[0] = dr::edge_length_loss(m).mean;
+    out2[1] = dr::laplacian_loss(m).mean;
+    std::vector<dr::Vec3> g;
+    dr::edge_length_loss_backward(m, 1.0, g);
+    for (size_t i = 0; i < g.size(); ++i) {
+      d_edge[3 * i] = g[i].x;
+      d_edge[3 * i + 1] = g[i].y;
+      d_edge[3 * i + 2] = g[i].z;
+    }
+    dr::laplacian_loss_backward(m, 1.0, g);
+    for (size_t i = 0; i < g.size(); ++i) {
+      d_lap[3 * i] = g[i].x;
+      d_lap[3 * i + 1] = g[i].y;
+      d_lap[3 * i + 2] = g[i].z;
+    }
+  });
+}
+
+// silhouette_iou_loss and its backward (geometry.cpp:651-682)
+int ref_silhouette_iou(const double* pred, const double* gt, int64_t n, double d_loss, double* loss, double* grad) {
+  return guarded([&] {
+    std::vector<double> p(pred, pred + n), g(gt, gt + n);
+    *loss = dr::silhouette_iou_loss(p, g);
+    std::vector<double> d = dr::silhouette_iou_loss_backward(p, g, d_loss);
+    std::memcpy(grad, d.data(), sizeof(double) * size_t(n));
+  });
+}
+
 }  // extern "C"

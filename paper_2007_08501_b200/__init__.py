@@ -5,6 +5,7 @@ Public surface (mirrors /root/reference/proj/include/dr/mesh_raster.hpp on the n
     rasterize_silhouette, rasterize_silhouette_backward, RasterizeSilhouette (fused silhouette_blend, shading.cpp)
     rasterize_softmax, rasterize_softmax_backward, RasterizeSoftmax, BlendParams (fused softmax render, grad.cpp)
     rasterize_points, rasterize_points_naive, rasterize_points_backward, PointRasterSettings (point_render.cpp)
+    fit_silhouette, FitConfig (pipeline.cpp:100-205 on the GPU path; ``fit``)
 Input generators and the host camera transform live in ``scenes``; mesh sharding across GPUs in ``shard``.
 """
 from .raster import (  # noqa: F401
@@ -44,3 +45,4 @@ from .points import (  # noqa: F401
     splat_position_backward,
     world_to_points_ndc,
 )
+from .fit import FitConfig, FitResult, FitTraceRow, NonFiniteError, fit_silhouette  # noqa: F401,E402

@@ -26,6 +26,8 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_meshes_bwd_hr",
     "dr_rasterize_silhouette_fwd",
     "dr_rasterize_silhouette_bwd",
+    "dr_rasterize_silhouette_fwd_f64",
+    "dr_rasterize_silhouette_bwd_f64",
     "dr_rasterize_softmax_fwd",
     "dr_rasterize_softmax_bwd",
     "dr_point_raster_settings_default",
@@ -133,10 +135,10 @@ def load() -> C.CDLL:
     L.dr_profile_read.argtypes = [C.POINTER(C.c_int), C.POINTER(C.c_float), C.c_int]
     L.dr_profile_kernel_name.argtypes = [C.c_int]
     L.dr_profile_kernel_name.restype = C.c_char_p
-    L.dr_rasterize_silhouette_fwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp,
-                                              C.c_size_t, _vp]
-    L.dr_rasterize_silhouette_bwd.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp,
-                                              _vp]
+    for fn in ("dr_rasterize_silhouette_fwd", "dr_rasterize_silhouette_fwd_f64"):
+        getattr(L, fn).argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp, C.c_size_t, _vp]
+    for fn in ("dr_rasterize_silhouette_bwd", "dr_rasterize_silhouette_bwd_f64"):
+        getattr(L, fn).argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp, _vp]
     L.dr_selftest_division.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
     L.dr_selftest_division.restype = C.c_int
     bpp = C.POINTER(DrBlendParams)
@@ -159,7 +161,8 @@ def load() -> C.CDLL:
     for fn in ("dr_rasterize_points_fwd", "dr_rasterize_points_fwd_f64", "dr_rasterize_points_bwd",
                "dr_rasterize_points_bwd_f64", "dr_world_to_points_ndc", "dr_points_ndc_backward"):
         getattr(L, fn).restype = C.c_int
-    for fn in ("dr_rasterize_silhouette_fwd", "dr_rasterize_silhouette_bwd", "dr_rasterize_meshes_fwd",
+    for fn in ("dr_rasterize_silhouette_fwd", "dr_rasterize_silhouette_bwd", "dr_rasterize_silhouette_fwd_f64",
+               "dr_rasterize_silhouette_bwd_f64", "dr_rasterize_meshes_fwd",
                "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
                "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_fwd_hr", "dr_rasterize_meshes_bwd_hr",
                "dr_rasterize_meshes_bin_stats"):

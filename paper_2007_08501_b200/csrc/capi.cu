@@ -373,11 +373,11 @@ int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
 
 int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
                  const dr_raster_settings* s, double sigma, const int64_t* p2f, const float* d_alpha, double* grad,
-                 cudaStream_t st) {
+                 cudaStream_t st, const double* d_alpha64 = nullptr) {
   Plan p;
   int rc = make_plan(N, F, s, p);
   if (rc) return rc;
-  if (!first || !num || !p2f || !d_alpha || (F > 0 && (!fv || !grad)))
+  if (!first || !num || !p2f || (!d_alpha && !d_alpha64) || (F > 0 && (!fv || !grad)))
     return fail(DR_ERR_USAGE, "null input/output pointer");
   if (!(sigma > 0.0)) return fail(DR_ERR_RANGE, "silhouette sigma must be > 0 (got %g)", sigma);
   int64_t mx;
@@ -395,6 +395,7 @@ int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int
   A.fv = fv;
   A.p2f = p2f;
   A.d_alpha = d_alpha;
+  A.d_alpha64 = d_alpha64;
   A.grad = grad;
   A.npix = N * (int64_t)p.H * p.W;
   A.F = F;
@@ -724,6 +725,21 @@ int dr_rasterize_silhouette_bwd(const double* fv, const int64_t* first, const in
                                 const dr_raster_settings* s, double sigma, const int64_t* p2f, const float* d_alpha,
                                 double* grad, dr_stream_t stream) {
   return sil_bwd_impl(fv, first, num, N, F, s, sigma, p2f, d_alpha, grad, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dr_rasterize_silhouette_fwd_f64(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                                    const dr_raster_settings* s, double sigma, int64_t* p2f, double* alpha, void* ws,
+                                    size_t ws_bytes, dr_stream_t stream) {
+  if (!alpha) return fail(DR_ERR_USAGE, "alpha is null");
+  return fwd_impl<double>(fv, first, num, N, F, s, p2f, nullptr, nullptr, nullptr, ws, ws_bytes,
+                          reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, alpha, sigma);
+}
+
+int dr_rasterize_silhouette_bwd_f64(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
+                                    const dr_raster_settings* s, double sigma, const int64_t* p2f,
+                                    const double* d_alpha, double* grad, dr_stream_t stream) {
+  return sil_bwd_impl(fv, first, num, N, F, s, sigma, p2f, nullptr, grad, reinterpret_cast<cudaStream_t>(stream),
+                      d_alpha);
 }
 
 void dr_raster_settings_default(dr_raster_settings* s) {

@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
   const int64_t HW = (int64_t)A.H * A.W;
   for (int64_t base = warp * 32; base < A.npix; base += nwarps * 32) {
     const int64_t pix = base + lane;
-    const double da = pix < A.npix ? (double)A.d_alpha[pix] : 0.0;
+    const double da = pix < A.npix ? (A.d_alpha64 ? A.d_alpha64[pix] : (double)A.d_alpha[pix]) : 0.0;
     const bool act = da != 0.0;  // shading.cpp:102: pixels with d_alpha == 0 contribute nothing
     if (!__any_sync(0xffffffffu, act)) continue;
     const int rem = act ? (int)(pix % HW) : 0;
@@ -553,8 +553,10 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
           int be;
           V2 qq;
           silhouette_envelope(v, p, dist, be, bt, qq, sign);
-          // sigmoid(-dist / sigma) (shading.cpp:9, 82); fp32 exp: the value enters gradients within tolerance
-          prob = 1.0 / (1.0 + (double)expf((float)(dist / A.sigma)));
+          // sigmoid(-dist / sigma) (shading.cpp:9, 82); fp32 exp for the fp32 cotangent (the value enters the
+          // gradients within tolerance), fp64 exp for the fp64 one
+          prob = A.d_alpha64 ? 1.0 / (1.0 + exp(dist / A.sigma))
+                             : 1.0 / (1.0 + (double)expf((float)(dist / A.sigma)));
           if constexpr (kStore) {
             EX[s * 32 + lane] = (qq.x - p.x) * (2.0 * sign);
             EY[s * 32 + lane] = (qq.y - p.y) * (2.0 * sign);

@@ -1214,14 +1214,14 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
   auto by_k = [&](auto nw_c) -> cudaError_t {
     constexpr int NW = decltype(nw_c)::value;
     // register-resident merge for small K, shared-memory shifting loop otherwise
-    if (A.alpha || A.image) {
-      if constexpr (std::is_same<OutT, float>::value) {  // the fused consumers write fp32 images only
-        if (A.alpha) {
-          if (A.K == 1) return go(k_fine<OutT, NW, 1, 1>);
-          if (A.K <= 4) return go(k_fine<OutT, NW, 4, 1>);
-          if (A.K <= 8) return go(k_fine<OutT, NW, 8, 1>);
-          return go(k_fine<OutT, NW, 0, 1>);
-        }
+    if (A.alpha) {  // fused silhouette: fp32 alpha, or fp64 for the fit loop (fit.py)
+      if (A.K == 1) return go(k_fine<OutT, NW, 1, 1>);
+      if (A.K <= 4) return go(k_fine<OutT, NW, 4, 1>);
+      if (A.K <= 8) return go(k_fine<OutT, NW, 8, 1>);
+      return go(k_fine<OutT, NW, 0, 1>);
+    }
+    if (A.image) {
+      if constexpr (std::is_same<OutT, float>::value) {  // the fused softmax render writes an fp32 image only
         if (A.K == 1) return go(k_fine<OutT, NW, 1, 2>);
         if (A.K <= 4) return go(k_fine<OutT, NW, 4, 2>);
         if (A.K <= 8) return go(k_fine<OutT, NW, 8, 2>);

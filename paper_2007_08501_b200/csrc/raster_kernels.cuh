@@ -88,6 +88,7 @@ struct SilBwdArgs {
   const double* fv;
   const int64_t* p2f;     // [N,H,W,K]
   const float* d_alpha;   // [N,H,W]
+  const double* d_alpha64;  // [N,H,W] fp64 cotangent (used instead of d_alpha when non-null; exact exp)
   double* grad;           // [F,3,3]
   int64_t npix;           // N*H*W
   int64_t F;

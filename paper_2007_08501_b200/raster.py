@@ -246,10 +246,12 @@ def rasterize_meshes_backward(face_verts, mesh_to_face_first_idx, num_faces_per_
 
 
 def rasterize_silhouette(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
-                         sigma: float = 1e-4, want_pix_to_face: bool = True, workspace=None):
+                         sigma: float = 1e-4, want_pix_to_face: bool = True, workspace=None, out_dtype=torch.float32):
     """Fused ``silhouette_blend(rasterize_meshes(...), sigma)`` (shading.cpp:75-91 over mesh_raster.cpp:234):
-    returns (pix_to_face int64 [N,H,W,K] or None, alpha float32 [N,H,W]). zbuf / bary / dists are never
-    materialised; pix_to_face is what the fused backward needs."""
+    returns (pix_to_face int64 [N,H,W,K] or None, alpha [N,H,W] in ``out_dtype``, float32 or float64). zbuf /
+    bary / dists are never materialised; pix_to_face is what the fused backward needs."""
+    if out_dtype not in (torch.float32, torch.float64):
+        raise UsageError("out_dtype must be float32 or float64")
     L = _lib.load()
     fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
     N, F = int(first.numel()), int(fv.shape[0])
@@ -263,9 +265,10 @@ def rasterize_silhouette(face_verts, mesh_to_face_first_idx, num_faces_per_mesh,
     if workspace is None or workspace.numel() < ws_n:
         workspace = torch.empty(ws_n, dtype=torch.uint8, device=dev)
     p2f = torch.empty((N, H, W, K), dtype=torch.int64, device=dev) if want_pix_to_face else None
-    alpha = torch.empty((N, H, W), dtype=torch.float32, device=dev)
+    alpha = torch.empty((N, H, W), dtype=out_dtype, device=dev)
+    fn = L.dr_rasterize_silhouette_fwd if out_dtype == torch.float32 else L.dr_rasterize_silhouette_fwd_f64
     with torch.cuda.device(dev):
-        rc = L.dr_rasterize_silhouette_fwd(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma),
+        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma),
                                            _ptr(p2f), _ptr(alpha), _ptr(workspace), workspace.numel(), _stream(dev))
     _check(rc, "rasterize_silhouette")
     return p2f, alpha
@@ -275,7 +278,8 @@ def rasterize_silhouette_backward(face_verts, mesh_to_face_first_idx, num_faces_
                                   sigma: float, pix_to_face, grad_alpha):
     """Fused ``rasterize_backward(..., 0, 0, silhouette_blend_backward(frag, sigma, grad_alpha))``
     (shading.cpp:93-121 + mesh_raster.cpp:329-403, the reference fit loop pipeline.cpp:153-162): returns
-    grad_face_verts [F,3,3] f64 (z components are zero: only the distance envelope carries gradient)."""
+    grad_face_verts [F,3,3] f64 (z components are zero: only the distance envelope carries gradient). A float64
+    grad_alpha selects the fp64 entry point (fp64 sigmoid), anything else is read as float32."""
     L = _lib.load()
     fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
     N, F = int(first.numel()), int(fv.shape[0])
@@ -285,11 +289,13 @@ def rasterize_silhouette_backward(face_verts, mesh_to_face_first_idx, num_faces_
         raise ShapeError(f"rasterize_silhouette_backward: pix_to_face {tuple(pix_to_face.shape)} / grad_alpha "
                          f"{tuple(grad_alpha.shape)} do not match [N,H,W,K] / [N,H,W] = {(N, H, W, K)}")
     p2f = pix_to_face.to(torch.int64).contiguous()
-    ga = grad_alpha.to(torch.float32).contiguous()
+    f64 = grad_alpha.dtype == torch.float64
+    ga = grad_alpha.to(torch.float64 if f64 else torch.float32).contiguous()
     grad = torch.zeros((F, 3, 3), dtype=torch.float64, device=fv.device)
     s = settings.to_c()
+    fn = L.dr_rasterize_silhouette_bwd_f64 if f64 else L.dr_rasterize_silhouette_bwd
     with torch.cuda.device(fv.device):
-        rc = L.dr_rasterize_silhouette_bwd(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma),
+        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma),
                                            _ptr(p2f), _ptr(ga), _ptr(grad), _stream(fv.device))
     _check(rc, "rasterize_silhouette_backward")
     return grad

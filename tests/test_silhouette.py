@@ -129,3 +129,29 @@ def test_fused_silhouette_autograd_and_errors(cuda):
     _, a1 = rasterize_silhouette(torch.as_tensor(fv, device=cuda), first, num, rs, SIGMA, want_pix_to_face=False)
     _, a2 = rasterize_silhouette(torch.as_tensor(fv, device=cuda), first, num, rs, SIGMA)
     assert torch.equal(a1, a2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,blur,sigma", [(8, 1e-4, SIGMA), (24, 4e-3, 2e-3)])
+def test_fused_silhouette_f64_vs_reference(reflib, cuda, K, blur, sigma):
+    """fp64 entry points (the fit loop's): alpha to a few ulps of silhouette_blend over the reference's fp64
+    MeshFragments, world-space gradients to 1e-10 of the reference chain."""
+    from paper_2007_08501_b200 import rasterize_silhouette, rasterize_silhouette_backward
+
+    m, cam = S.config_meshes("C2"), S.bench_camera()
+    H = 96
+    rb, frags = _ref_fragments(reflib, m, cam, H, K, blur)
+    a_ref = reflib.silhouette_blend(frags[0], frags[3], sigma)
+    da = a_ref - 0.5
+    dd = reflib.silhouette_blend_backward(frags[0], frags[3], sigma, da)
+    d_ref = reflib.rasterize_backward(rb, cam.packed(), H, H, K, blur, frags, np.zeros_like(frags[1]),
+                                      np.zeros_like(frags[2]), dd)
+    fv, first, num = boundary(m, cam)
+    rs = raster_settings(H, K, blur, cam)
+    fvt, ft, nt = (torch.as_tensor(x, device=cuda) for x in (fv, first, num))
+    p2f, alpha = rasterize_silhouette(fvt, ft, nt, rs, sigma, out_dtype=torch.float64)
+    assert alpha.dtype == torch.float64
+    assert np.array_equal(p2f.cpu().numpy(), frags[0])
+    np.testing.assert_allclose(alpha.cpu().numpy(), a_ref, rtol=1e-13, atol=1e-15)
+    g = rasterize_silhouette_backward(fvt, ft, nt, rs, sigma, p2f, torch.as_tensor(da, device=cuda)).cpu().numpy()
+    assert rel_err(S.scatter_face_grads(m, cam, g), d_ref) < 1e-10
