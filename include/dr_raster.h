@@ -149,6 +149,11 @@ typedef struct dr_camera {
  * Out-of-range vertex indices -> DR_ERR_INDEX (synchronises the stream to report it). */
 int dr_world_to_face_verts(const double* verts, int64_t V, const int64_t* faces, int64_t F, const dr_camera* cam,
                            double* face_verts, dr_stream_t stream);
+/* Same without the synchronising index check: a face with a vertex index outside [0, V) sets *bad_index = 1
+ * (device int, may be NULL) and that vertex's face_verts entries are NaN (the face is culled downstream). For callers that validated the topology
+ * once (a fit loop) and for CUDA-graph capture. */
+int dr_world_to_face_verts_async(const double* verts, int64_t V, const int64_t* faces, int64_t F,
+                                 const dr_camera* cam, double* face_verts, int* bad_index, dr_stream_t stream);
 
 /* Reverse of the above (mesh_raster.cpp:380-401): grad_face_verts [F,3,3] scattered to vertices and pulled
  * through world_to_ndc_backward (camera.cpp:72-85) -> grad_verts [V,3] world space (overwritten). */
@@ -196,6 +201,18 @@ int dr_rasterize_silhouette_bwd_f64(const double* face_verts, const int64_t* mes
                                     const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
                                     const dr_raster_settings* s, double sigma, const int64_t* pix_to_face,
                                     const double* grad_alpha, double* grad_face_verts, dr_stream_t stream);
+/* Asynchronous fp64 silhouette (host copies of the mesh ranges, as dr_rasterize_meshes_fwd_hr): no call
+ * synchronises or allocates, so a whole fit iteration can be captured into one CUDA graph (fit.py). */
+int dr_rasterize_silhouette_fwd_f64_hr(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                                       const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
+                                       const dr_raster_settings* s, double sigma, int64_t* pix_to_face,
+                                       double* alpha, void* workspace, size_t workspace_bytes, dr_stream_t stream,
+                                       const int64_t* host_first, const int64_t* host_num);
+int dr_rasterize_silhouette_bwd_f64_hr(const double* face_verts, const int64_t* mesh_to_face_first_idx,
+                                       const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
+                                       const dr_raster_settings* s, double sigma, const int64_t* pix_to_face,
+                                       const double* grad_alpha, double* grad_face_verts, dr_stream_t stream,
+                                       const int64_t* host_first, const int64_t* host_num);
 
 /* ---- fused fragment consumer: softmax render ----
  * The reference's differentiable softmax render (grad.cpp:177-209): rasterize_meshes -> interpolate_face_attributes

@@ -28,6 +28,9 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_silhouette_bwd",
     "dr_rasterize_silhouette_fwd_f64",
     "dr_rasterize_silhouette_bwd_f64",
+    "dr_rasterize_silhouette_fwd_f64_hr",
+    "dr_rasterize_silhouette_bwd_f64_hr",
+    "dr_world_to_face_verts_async",
     "dr_rasterize_softmax_fwd",
     "dr_rasterize_softmax_bwd",
     "dr_point_raster_settings_default",
@@ -139,6 +142,11 @@ def load() -> C.CDLL:
         getattr(L, fn).argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp, C.c_size_t, _vp]
     for fn in ("dr_rasterize_silhouette_bwd", "dr_rasterize_silhouette_bwd_f64"):
         getattr(L, fn).argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp, _vp, _vp]
+    L.dr_rasterize_silhouette_fwd_f64_hr.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp,
+                                                     _vp, C.c_size_t, _vp, _vp, _vp]
+    L.dr_rasterize_silhouette_bwd_f64_hr.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp,
+                                                     _vp, _vp, _vp, _vp]
+    L.dr_world_to_face_verts_async.argtypes = [_vp, C.c_int64, _vp, C.c_int64, C.POINTER(DrCamera), _vp, _vp, _vp]
     L.dr_selftest_division.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
     L.dr_selftest_division.restype = C.c_int
     bpp = C.POINTER(DrBlendParams)
@@ -162,7 +170,8 @@ def load() -> C.CDLL:
                "dr_rasterize_points_bwd_f64", "dr_world_to_points_ndc", "dr_points_ndc_backward"):
         getattr(L, fn).restype = C.c_int
     for fn in ("dr_rasterize_silhouette_fwd", "dr_rasterize_silhouette_bwd", "dr_rasterize_silhouette_fwd_f64",
-               "dr_rasterize_silhouette_bwd_f64", "dr_rasterize_meshes_fwd",
+               "dr_rasterize_silhouette_bwd_f64", "dr_rasterize_silhouette_fwd_f64_hr",
+               "dr_rasterize_silhouette_bwd_f64_hr", "dr_world_to_face_verts_async", "dr_rasterize_meshes_fwd",
                "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
                "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_fwd_hr", "dr_rasterize_meshes_bwd_hr",
                "dr_rasterize_meshes_bin_stats"):

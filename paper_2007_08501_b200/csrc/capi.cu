@@ -373,7 +373,8 @@ int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
 
 int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
                  const dr_raster_settings* s, double sigma, const int64_t* p2f, const float* d_alpha, double* grad,
-                 cudaStream_t st, const double* d_alpha64 = nullptr) {
+                 cudaStream_t st, const double* d_alpha64 = nullptr, const int64_t* host_first = nullptr,
+                 const int64_t* host_num = nullptr) {
   Plan p;
   int rc = make_plan(N, F, s, p);
   if (rc) return rc;
@@ -382,7 +383,7 @@ int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int
   if (!(sigma > 0.0)) return fail(DR_ERR_RANGE, "silhouette sigma must be > 0 (got %g)", sigma);
   int64_t mx;
   std::vector<int64_t> ranges;
-  rc = read_ranges(first, num, N, F, st, &mx, &ranges);
+  rc = read_ranges(first, num, N, F, st, &mx, &ranges, host_first, host_num);
   if (rc) return rc;
   if (F == 0) return DR_OK;
   cudaError_t e;
@@ -742,6 +743,25 @@ int dr_rasterize_silhouette_bwd_f64(const double* fv, const int64_t* first, cons
                       d_alpha);
 }
 
+int dr_rasterize_silhouette_fwd_f64_hr(const double* fv, const int64_t* first, const int64_t* num, int64_t N,
+                                       int64_t F, const dr_raster_settings* s, double sigma, int64_t* p2f,
+                                       double* alpha, void* ws, size_t ws_bytes, dr_stream_t stream,
+                                       const int64_t* host_first, const int64_t* host_num) {
+  if (!alpha) return fail(DR_ERR_USAGE, "alpha is null");
+  if (!host_first || !host_num) return fail(DR_ERR_USAGE, "host ranges are null");
+  return fwd_impl<double>(fv, first, num, N, F, s, p2f, nullptr, nullptr, nullptr, ws, ws_bytes,
+                          reinterpret_cast<cudaStream_t>(stream), host_first, host_num, alpha, sigma);
+}
+
+int dr_rasterize_silhouette_bwd_f64_hr(const double* fv, const int64_t* first, const int64_t* num, int64_t N,
+                                       int64_t F, const dr_raster_settings* s, double sigma, const int64_t* p2f,
+                                       const double* d_alpha, double* grad, dr_stream_t stream,
+                                       const int64_t* host_first, const int64_t* host_num) {
+  if (!host_first || !host_num) return fail(DR_ERR_USAGE, "host ranges are null");
+  return sil_bwd_impl(fv, first, num, N, F, s, sigma, p2f, nullptr, grad, reinterpret_cast<cudaStream_t>(stream),
+                      d_alpha, host_first, host_num);
+}
+
 void dr_raster_settings_default(dr_raster_settings* s) {
   if (!s) return;
   std::memset(s, 0, sizeof(*s));
@@ -840,6 +860,21 @@ int dr_world_to_face_verts(const double* verts, int64_t V, const int64_t* faces,
   if (e != cudaSuccess) return cuda_fail(e, "world_to_face_verts");
   if (bad) return fail(DR_ERR_INDEX, "face vertex index out of range [0, %lld)", (long long)V);
   return DR_OK;
+}
+
+int dr_world_to_face_verts_async(const double* verts, int64_t V, const int64_t* faces, int64_t F,
+                                 const dr_camera* cam, double* face_verts, int* bad_index, dr_stream_t stream) {
+  if (!cam) return fail(DR_ERR_USAGE, "camera pointer is null");
+  if (V < 0 || F < 0) return fail(DR_ERR_SHAPE, "negative vertex/face count");
+  if (F == 0) return DR_OK;
+  if (!verts || !faces || !face_verts) return fail(DR_ERR_USAGE, "null input/output pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  {
+    ProfScope ps(st, KN_CAMERA);
+    e = drb::launch_world_to_face_verts(verts, V, faces, F, camera_args(cam), face_verts, bad_index, st);
+  }
+  return e == cudaSuccess ? DR_OK : cuda_fail(e, "world_to_face_verts");
 }
 
 int dr_face_verts_backward(const double* verts, int64_t V, const int64_t* faces, int64_t F, const dr_camera* cam,

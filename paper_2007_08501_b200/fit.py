@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from .raster import (RasterSettings, UsageError, face_verts_backward, rasterize_silhouette,
-                     rasterize_silhouette_backward, world_to_face_verts)
+                     rasterize_silhouette_backward, workspace_bytes, world_to_face_verts)
 from .scenes import Camera, Meshes, axis_angle, cube, ico_sphere
 
 
@@ -211,39 +211,81 @@ def silhouette_iou_loss_backward(pred, gt, d_loss=1.0):
 
 
 class _Views:
-    """The fixed cameras + raster settings of one fit; silhouettes of packed verts on the GPU."""
+    """The fixed cameras + raster settings of one fit; silhouettes of packed verts on the GPU. Every call is
+    non-synchronising (host copies of the mesh ranges, the unchecked projection after a one-time index check,
+    a preallocated workspace), so an iteration can be captured into a CUDA graph."""
 
-    def __init__(self, cfg: FitConfig, faces_global: torch.Tensor, first, num):
+    def __init__(self, cfg: FitConfig, m: Meshes, dev):
         self.cams = [view_camera(cfg.camera_distance, cfg.focal_length, True,
                                  2.0 * 3.14159265358979323846 * v / cfg.num_views) for v in range(cfg.num_views)]
-        self.faces, self.first, self.num = faces_global, first, num
+        self.faces = torch.as_tensor(m.faces_packed(), dtype=torch.int64, device=dev)
+        self.host = (m.mesh_to_face_first_idx(), m.num_faces_per_mesh())
+        self.first, self.num = (torch.as_tensor(x, device=dev) for x in self.host)
+        self.V = int(m.num_verts_per_mesh().sum())
+        if len(self.faces) and (int(self.faces.min()) < 0 or int(self.faces.max()) >= self.V):
+            raise UsageError("face vertex index out of range")
         self.rs = RasterSettings(image_size=cfg.image_size, faces_per_pixel=cfg.faces_per_pixel)
-        self.ws = None
+        self.ws = torch.empty(workspace_bytes(len(m), len(self.faces), self.rs), dtype=torch.uint8, device=dev)
 
     def set_blur(self, blur: float):
         self.rs = RasterSettings(image_size=self.rs.image_size, faces_per_pixel=self.rs.faces_per_pixel,
                                  blur_radius=blur, znear=self.cams[0].znear)
+        need = workspace_bytes(len(self.host[0]), len(self.faces), self.rs)
+        if need > self.ws.numel():
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.ws.device)
 
     def alpha(self, verts, v: int, sigma: float, want_p2f: bool):
-        fv = world_to_face_verts(verts, self.faces, self.cams[v])
+        fv = world_to_face_verts(verts, self.faces, self.cams[v], check=False)
         p2f, a = rasterize_silhouette(fv, self.first, self.num, self.rs, sigma, want_pix_to_face=want_p2f,
-                                      workspace=self.ws, out_dtype=torch.float64)
+                                      workspace=self.ws, out_dtype=torch.float64, host_ranges=self.host)
         return fv, p2f, a
 
     def grad(self, verts, v: int, fv, sigma: float, p2f, d_alpha):
-        g_fv = rasterize_silhouette_backward(fv, self.first, self.num, self.rs, sigma, p2f, d_alpha)
+        g_fv = rasterize_silhouette_backward(fv, self.first, self.num, self.rs, sigma, p2f, d_alpha,
+                                             host_ranges=self.host)
         return face_verts_backward(verts, self.faces, self.cams[v], g_fv)
 
 
-def _batch_tensors(m: Meshes, dev):
-    faces = torch.as_tensor(m.faces_packed(), dtype=torch.int64, device=dev)
-    first = torch.as_tensor(m.mesh_to_face_first_idx(), device=dev)
-    num = torch.as_tensor(m.num_faces_per_mesh(), device=dev)
-    return faces, first, num
+class _Step:
+    """One fit iteration (pipeline.cpp:146-190) on static tensors: reads verts / Adam state / the bias
+    corrections c1, c2 (device scalars) / the band's targets, updates verts and the Adam state in place and
+    writes (l_s / views, l_l, l_e, total) into ``row``. Device work only, so it can be replayed as a graph."""
+
+    def __init__(self, cfg: FitConfig, views: _Views, reg: MeshRegularizers, verts, targets, sigma):
+        self.cfg, self.views, self.reg, self.verts, self.targets, self.sigma = cfg, views, reg, verts, targets, sigma
+        dev = verts.device
+        self.m = torch.zeros_like(verts)
+        self.v = torch.zeros_like(verts)
+        self.c1 = torch.ones((), dtype=torch.float64, device=dev)
+        self.c2 = torch.ones((), dtype=torch.float64, device=dev)
+        self.row = torch.zeros(4, dtype=torch.float64, device=dev)
+
+    def __call__(self):
+        cfg, views, reg, verts = self.cfg, self.views, self.reg, self.verts
+        b1, b2, adam_eps = 0.9, 0.999, 1e-8
+        grad = torch.zeros_like(verts)
+        l_s = torch.zeros((), dtype=torch.float64, device=verts.device)
+        for v in range(cfg.num_views):
+            fv, p2f, alpha = views.alpha(verts, v, self.sigma, True)
+            tgt = self.targets[v]
+            l_s = l_s + silhouette_iou_loss(alpha, tgt)
+            d_alpha = silhouette_iou_loss_backward(alpha, tgt, 1.0)
+            grad += views.grad(verts, v, fv, self.sigma, p2f, d_alpha)
+        _, l_l = reg.laplacian_loss(verts)
+        _, l_e = reg.edge_length_loss(verts)
+        total = l_s + cfg.lambda_laplacian * l_l + cfg.lambda_edge * l_e
+        grad += reg.laplacian_loss_backward(verts, cfg.lambda_laplacian)
+        grad += reg.edge_length_loss_backward(verts, cfg.lambda_edge)
+        self.row.copy_(torch.stack([l_s / cfg.num_views, l_l, l_e, total]))
+        # pipeline.cpp:182-186, same operation order
+        self.m.copy_(b1 * self.m + (1 - b1) * grad)
+        self.v.copy_(b2 * self.v + (1 - b2) * grad * grad)
+        verts -= cfg.step_size * (self.m / self.c1) / (torch.sqrt(self.v / self.c2) + adam_eps)
 
 
-def fit_silhouette(cfg: FitConfig, device="cuda") -> FitResult:
-    """dr::fit_silhouette (pipeline.cpp:100-205) on the B200 path."""
+def fit_silhouette(cfg: FitConfig, device="cuda", graph: bool = True) -> FitResult:
+    """dr::fit_silhouette (pipeline.cpp:100-205) on the B200 path. ``graph``: each band's iteration is captured
+    once into a CUDA graph and replayed (one launch per iteration instead of ~150 kernel launches + host work)."""
     if cfg.num_views < 2:
         raise UsageError("fit requires at least 2 views")
     dev = torch.device(device)
@@ -251,65 +293,51 @@ def fit_silhouette(cfg: FitConfig, device="cuda") -> FitResult:
     tverts = torch.as_tensor(target.verts_packed(), device=dev)
     if cfg.target_scale != 1.0:
         tverts = tverts * cfg.target_scale  # scale_mesh, pipeline.cpp:29-33
-    tv = _Views(cfg, *_batch_tensors(target, dev))
-
+    tv = _Views(cfg, target, dev)
+    mesh = ico_sphere(cfg.template_level)
+    views = _Views(cfg, mesh, dev)
+    reg = MeshRegularizers(mesh, dev)
+    verts = torch.as_tensor(mesh.verts_packed(), device=dev).clone()
     coarse_iters = int(cfg.coarse_fraction * cfg.iterations)
-    state = {}
-
-    def set_band(sigma, blur):  # pipeline.cpp:119-125: target silhouettes re-rendered per band
-        state["sigma"] = sigma
+    bands = [(0, coarse_iters, cfg.coarse_sigma, cfg.coarse_blur_radius)] if coarse_iters > 0 else []
+    bands.append((coarse_iters if coarse_iters > 0 else 0, cfg.iterations, cfg.sigma, cfg.blur_radius))
+    trace = torch.zeros((max(cfg.iterations, 0), 4), dtype=torch.float64, device=dev)
+    b1, b2 = 0.9, 0.999
+    step = None
+    for lo, hi, sigma, blur in bands:
+        # pipeline.cpp:119-125 / 167-172: target silhouettes re-rendered per band, Adam restarted
         tv.set_blur(blur)
         views.set_blur(blur)
-        state["target"] = [tv.alpha(tverts, v, sigma, False)[2] for v in range(cfg.num_views)]
+        targets = [tv.alpha(tverts, v, sigma, False)[2] for v in range(cfg.num_views)]
+        step = _Step(cfg, views, reg, verts, targets, sigma)
+        run = step
+        if graph and dev.type == "cuda" and hi > lo:
+            # warm up on a side stream (library loads, allocator), restoring the state it touched
+            saved = verts.clone()
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                step()
+            torch.cuda.current_stream(dev).wait_stream(side)
+            verts.copy_(saved)
+            step.m.zero_()
+            step.v.zero_()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            run = g.replay
+        for k, it in enumerate(range(lo, hi)):
+            step.c1.fill_(1.0 - math.pow(b1, k + 1))
+            step.c2.fill_(1.0 - math.pow(b2, k + 1))
+            run()
+            trace[it].copy_(step.row)
 
-    mesh = ico_sphere(cfg.template_level)
-    views = _Views(cfg, *_batch_tensors(mesh, dev))
-    reg = MeshRegularizers(mesh, dev)
-    set_band(cfg.coarse_sigma if coarse_iters > 0 else cfg.sigma,
-             cfg.coarse_blur_radius if coarse_iters > 0 else cfg.blur_radius)
-
-    verts = torch.as_tensor(mesh.verts_packed(), device=dev).clone()
-    adam_m = torch.zeros_like(verts)
-    adam_v = torch.zeros_like(verts)
-    b1, b2, adam_eps = 0.9, 0.999, 1e-8
-    steps_in_phase = 0
-    rows = []
-    for it in range(cfg.iterations):
-        if it == coarse_iters and coarse_iters > 0:
-            set_band(cfg.sigma, cfg.blur_radius)
-            adam_m.zero_()
-            adam_v.zero_()
-            steps_in_phase = 0
-        sigma = state["sigma"]
-        grad = torch.zeros_like(verts)
-        l_s = torch.zeros((), dtype=torch.float64, device=dev)
-        for v in range(cfg.num_views):
-            fv, p2f, alpha = views.alpha(verts, v, sigma, True)
-            tgt = state["target"][v]
-            l_s = l_s + silhouette_iou_loss(alpha, tgt)
-            d_alpha = silhouette_iou_loss_backward(alpha, tgt, 1.0)
-            grad += views.grad(verts, v, fv, sigma, p2f, d_alpha)
-        _, l_l = reg.laplacian_loss(verts)
-        _, l_e = reg.edge_length_loss(verts)
-        total = l_s + cfg.lambda_laplacian * l_l + cfg.lambda_edge * l_e
-        grad += reg.laplacian_loss_backward(verts, cfg.lambda_laplacian)
-        grad += reg.edge_length_loss_backward(verts, cfg.lambda_edge)
-        rows.append(torch.stack([l_s / cfg.num_views, l_l, l_e, total]))
-        steps_in_phase += 1
-        c1 = 1.0 - math.pow(b1, steps_in_phase)
-        c2 = 1.0 - math.pow(b2, steps_in_phase)
-        # pipeline.cpp:182-186, same operation order
-        adam_m.copy_(b1 * adam_m + (1 - b1) * grad)
-        adam_v.copy_(b2 * adam_v + (1 - b2) * grad * grad)
-        verts -= cfg.step_size * (adam_m / c1) / (torch.sqrt(adam_v / c2) + adam_eps)
-
-    trace_np = torch.stack(rows).cpu().numpy() if rows else np.zeros((0, 4))
-    bad = np.nonzero(~np.isfinite(trace_np[:, 3]))[0] if len(trace_np) else []
+    trace_np = trace.cpu().numpy()
+    bad = np.nonzero(~np.isfinite(trace_np[:, 3]))[0]
     if len(bad):
         raise NonFiniteError(f"fit diverged at iteration {int(bad[0])}")
-    sigma = state["sigma"]
-    l_s = sum(float(silhouette_iou_loss(views.alpha(verts, v, sigma, False)[2], state["target"][v]))
-              for v in range(cfg.num_views))
-    trace = [FitTraceRow(i, *map(float, r)) for i, r in enumerate(trace_np)]
-    return FitResult(verts=verts, faces=mesh.faces_local_packed(), trace=trace,
+    l_s = sum(float(silhouette_iou_loss(views.alpha(verts, v, step.sigma, False)[2], step.targets[v]))
+              for v in range(cfg.num_views)) if step is not None else 0.0
+    rows = [FitTraceRow(i, *map(float, r)) for i, r in enumerate(trace_np)]
+    return FitResult(verts=verts, faces=mesh.faces_local_packed(), trace=rows,
                      final_silhouette_loss=l_s / cfg.num_views)

@@ -188,6 +188,13 @@ def rasterize_meshes_naive(face_verts, mesh_to_face_first_idx, num_faces_per_mes
     return rasterize_meshes(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings, out_dtype=out_dtype)
 
 
+def _host_ranges(host_ranges) -> tuple:
+    """(first, num) host copies as contiguous int64 arrays (kept alive by the caller for the call), or ()."""
+    if host_ranges is None:
+        return ()
+    return tuple(np.ascontiguousarray(x, dtype=np.int64) for x in host_ranges)
+
+
 def _covers(host_ranges, F: int) -> bool:
     """True when the meshes' face ranges cover [0, F) (the backward then overwrites every row of its output)."""
     first, num = (np.asarray(x, dtype=np.int64) for x in host_ranges)
@@ -246,12 +253,17 @@ def rasterize_meshes_backward(face_verts, mesh_to_face_first_idx, num_faces_per_
 
 
 def rasterize_silhouette(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
-                         sigma: float = 1e-4, want_pix_to_face: bool = True, workspace=None, out_dtype=torch.float32):
+                         sigma: float = 1e-4, want_pix_to_face: bool = True, workspace=None, out_dtype=torch.float32,
+                         host_ranges=None):
     """Fused ``silhouette_blend(rasterize_meshes(...), sigma)`` (shading.cpp:75-91 over mesh_raster.cpp:234):
     returns (pix_to_face int64 [N,H,W,K] or None, alpha [N,H,W] in ``out_dtype``, float32 or float64). zbuf /
-    bary / dists are never materialised; pix_to_face is what the fused backward needs."""
+    bary / dists are never materialised; pix_to_face is what the fused backward needs. ``host_ranges`` =
+    (first, num) as host int64 arrays with the device values (float64 only): the call then never synchronises
+    (dr_rasterize_silhouette_fwd_f64_hr), e.g. inside a CUDA graph."""
     if out_dtype not in (torch.float32, torch.float64):
         raise UsageError("out_dtype must be float32 or float64")
+    if host_ranges is not None and out_dtype != torch.float64:
+        raise UsageError("host_ranges needs out_dtype=float64")
     L = _lib.load()
     fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
     N, F = int(first.numel()), int(fv.shape[0])
@@ -267,19 +279,24 @@ def rasterize_silhouette(face_verts, mesh_to_face_first_idx, num_faces_per_mesh,
     p2f = torch.empty((N, H, W, K), dtype=torch.int64, device=dev) if want_pix_to_face else None
     alpha = torch.empty((N, H, W), dtype=out_dtype, device=dev)
     fn = L.dr_rasterize_silhouette_fwd if out_dtype == torch.float32 else L.dr_rasterize_silhouette_fwd_f64
+    hr = _host_ranges(host_ranges)
+    if hr:
+        fn = L.dr_rasterize_silhouette_fwd_f64_hr
     with torch.cuda.device(dev):
-        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma),
-                                           _ptr(p2f), _ptr(alpha), _ptr(workspace), workspace.numel(), _stream(dev))
+        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma), _ptr(p2f), _ptr(alpha),
+                _ptr(workspace), workspace.numel(), _stream(dev), *[a.ctypes.data_as(C.c_void_p) for a in hr])
     _check(rc, "rasterize_silhouette")
     return p2f, alpha
 
 
 def rasterize_silhouette_backward(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
-                                  sigma: float, pix_to_face, grad_alpha):
+                                  sigma: float, pix_to_face, grad_alpha, host_ranges=None, out=None):
     """Fused ``rasterize_backward(..., 0, 0, silhouette_blend_backward(frag, sigma, grad_alpha))``
     (shading.cpp:93-121 + mesh_raster.cpp:329-403, the reference fit loop pipeline.cpp:153-162): returns
     grad_face_verts [F,3,3] f64 (z components are zero: only the distance envelope carries gradient). A float64
-    grad_alpha selects the fp64 entry point (fp64 sigmoid), anything else is read as float32."""
+    grad_alpha selects the fp64 entry point (fp64 sigmoid), anything else is read as float32. ``host_ranges``
+    (float64 only) makes the call non-synchronising; ``out`` receives grad_face_verts (overwritten on the batch's
+    face ranges)."""
     L = _lib.load()
     fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
     N, F = int(first.numel()), int(fv.shape[0])
@@ -290,13 +307,18 @@ def rasterize_silhouette_backward(face_verts, mesh_to_face_first_idx, num_faces_
                          f"{tuple(grad_alpha.shape)} do not match [N,H,W,K] / [N,H,W] = {(N, H, W, K)}")
     p2f = pix_to_face.to(torch.int64).contiguous()
     f64 = grad_alpha.dtype == torch.float64
+    if host_ranges is not None and not f64:
+        raise UsageError("host_ranges needs a float64 grad_alpha")
     ga = grad_alpha.to(torch.float64 if f64 else torch.float32).contiguous()
-    grad = torch.zeros((F, 3, 3), dtype=torch.float64, device=fv.device)
+    grad = out if out is not None else torch.zeros((F, 3, 3), dtype=torch.float64, device=fv.device)
     s = settings.to_c()
     fn = L.dr_rasterize_silhouette_bwd_f64 if f64 else L.dr_rasterize_silhouette_bwd
+    hr = _host_ranges(host_ranges)
+    if hr:
+        fn = L.dr_rasterize_silhouette_bwd_f64_hr
     with torch.cuda.device(fv.device):
-        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma),
-                                           _ptr(p2f), _ptr(ga), _ptr(grad), _stream(fv.device))
+        rc = fn(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), float(sigma), _ptr(p2f), _ptr(ga), _ptr(grad),
+                _stream(fv.device), *[a.ctypes.data_as(C.c_void_p) for a in hr])
     _check(rc, "rasterize_silhouette_backward")
     return grad
 
@@ -469,7 +491,8 @@ def _camera_c(cam) -> _lib.DrCamera:
     return c
 
 
-def world_to_face_verts(verts: torch.Tensor, faces: torch.Tensor, camera) -> torch.Tensor:
+def world_to_face_verts(verts: torch.Tensor, faces: torch.Tensor, camera, check: bool = True,
+                        bad_index: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
     """world_to_ndc (camera.cpp:36-70) + per-face gather on the GPU: verts [V,3] f64 world space, faces [F,3] packed
     global vertex ids -> face_verts [F,3,3] (x_ndc, y_ndc, z_view), bit-identical to the reference."""
     L = _lib.load()
@@ -477,11 +500,16 @@ def world_to_face_verts(verts: torch.Tensor, faces: torch.Tensor, camera) -> tor
         raise UsageError("verts must be a CUDA tensor (there is no CPU path)")
     v = verts.detach().to(torch.float64).contiguous()
     f = faces.to(device=v.device, dtype=torch.int64).contiguous()
-    out = torch.empty((f.shape[0], 3, 3), dtype=torch.float64, device=v.device)
+    if out is None:
+        out = torch.empty((f.shape[0], 3, 3), dtype=torch.float64, device=v.device)
     cam = _camera_c(camera)
     with torch.cuda.device(v.device):
-        rc = L.dr_world_to_face_verts(_ptr(v), v.shape[0], _ptr(f), f.shape[0], C.byref(cam), _ptr(out),
-                                      _stream(v.device))
+        if check:  # validates the vertex indices (one synchronisation)
+            rc = L.dr_world_to_face_verts(_ptr(v), v.shape[0], _ptr(f), f.shape[0], C.byref(cam), _ptr(out),
+                                          _stream(v.device))
+        else:  # no synchronisation (CUDA-graph capturable); bad indices flag `bad_index` (device int32)
+            rc = L.dr_world_to_face_verts_async(_ptr(v), v.shape[0], _ptr(f), f.shape[0], C.byref(cam), _ptr(out),
+                                                _ptr(bad_index), _stream(v.device))
     _check(rc, "world_to_face_verts")
     return out
 

@@ -80,8 +80,8 @@ FIT_CASES = [
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", FIT_CASES)
-def test_fit_matches_reference(reflib, cuda, case):
+@pytest.mark.parametrize("case,graph", [(c, True) for c in FIT_CASES] + [(FIT_CASES[0], False)])
+def test_fit_matches_reference(reflib, cuda, case, graph):
     target, scale, level, views, iters, image, K = case
     cfg = FitConfig(target_spec=target, target_scale=scale, template_level=level, num_views=views,
                     iterations=iters, image_size=image, faces_per_pixel=K)
@@ -94,7 +94,7 @@ def test_fit_matches_reference(reflib, cuda, case):
 
     tr_p, final_p, verts_p = reflib.fit_silhouette(replace(cfg, target_scale=scale * (1 + 1e-12)))
     self_dev = np.abs(tr_p[:, 1:] - tr_ref[:, 1:]).max(0)
-    res = fit_silhouette(cfg, device=cuda)
+    res = fit_silhouette(cfg, device=cuda, graph=graph)
     tr = np.array([[r.iter, r.l_s, r.l_l, r.l_e, r.total] for r in res.trace])
     assert tr.shape == tr_ref.shape
     assert np.array_equal(tr[:, 0], tr_ref[:, 0])
