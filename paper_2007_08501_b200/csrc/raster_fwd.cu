@@ -487,6 +487,15 @@ struct WarpSmem {
   double* pxy;      // [12] pixel-centre NDC coordinates of the micro-tile: x of its 8 columns, y of its 4 rows
   uint32_t* pairq;  // [kPairQ] queued (ring slot << 5 | pixel) pairs awaiting evaluation
   int32_t* tcnt;    // [32] entries held by each pixel's list (shared-memory list path, KMAX == 0)
+  int ls;           // pixel-major list stride K + 1
+
+  // element (slot s, pixel p) of the top-K lists. kPM: pixel-major rows padded to K + 1 entries, so both the
+  // owner-lane accesses (32 pixels, same s) and the transposed emit (consecutive s of a few pixels) hit distinct
+  // banks; otherwise slot-major [K][32] (shift-and-add indexing; the emit's same-column reads conflict 8-way).
+  // Measured: pixel-major pays for the shared-memory lists (K > 8, C5 k_fine 6.84 -> 6.73 ms) but not for the
+  // register-merge path (C4 6.18 -> 6.21 ms), so it is used where KMAX == 0 only.
+  template <bool kPM>
+  __device__ __forceinline__ int li(int s, int p) const { return kPM ? p * ls + s : s * 32 + p; }
 
   __device__ __forceinline__ double get(int f, int k) const { return d[f * kRing + k]; }
   __device__ __forceinline__ void put(int f, int k, double v) const { d[f * kRing + k] = v; }
@@ -544,8 +553,9 @@ constexpr int kBuf = DR_KBUF;  // buffered candidates per pixel before the owner
 // per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt | pairq |
 // tcnt
 __host__ __device__ constexpr size_t warp_smem_bytes(int K) {
-  return (size_t)kNF * kRing * sizeof(double) + (size_t)K * 32 * sizeof(double) + (size_t)kBuf * 32 * sizeof(double) +
-         12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) + (size_t)K * 32 * sizeof(int32_t) +
+  return (size_t)kNF * kRing * sizeof(double) + (size_t)(K + 1) * 32 * sizeof(double) +
+         (size_t)kBuf * 32 * sizeof(double) + 12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) +
+         (size_t)(K + 1) * 32 * sizeof(int32_t) +
          (size_t)kBuf * 32 * sizeof(int32_t) + (size_t)kRing * (sizeof(uint32_t) + sizeof(float)) +
          32 * sizeof(int32_t) + kPairQ * sizeof(uint32_t) + 32 * sizeof(int32_t) +
          8;  // + pad keeps the next warp's base 8-byte aligned
@@ -642,19 +652,20 @@ __device__ __forceinline__ void softmax_slot(const FineArgs<OutT>& A, const doub
 template <bool kCounted>
 __device__ __forceinline__ void list_insert(const WarpSmem& ws, int K, int p, double zc, int32_t f) {
   const int n = kCounted ? ws.tcnt[p] : K;
-  if (n < K || cand_less(zc, f, ws.tz[(K - 1) * 32 + p], ws.tid[(K - 1) * 32 + p])) {
+  const int tail = ws.li<kCounted>(K - 1, p);
+  if (n < K || cand_less(zc, f, ws.tz[tail], ws.tid[tail])) {
     int s = n < K ? n : K - 1;
     if (kCounted && n < K) ws.tcnt[p] = n + 1;
     while (s > 0) {
-      const double zp = ws.tz[(s - 1) * 32 + p];
-      const int32_t ip = ws.tid[(s - 1) * 32 + p];
+      const double zp = ws.tz[ws.li<kCounted>(s - 1, p)];
+      const int32_t ip = ws.tid[ws.li<kCounted>(s - 1, p)];
       if (!cand_less(zc, f, zp, ip)) break;
-      ws.tz[s * 32 + p] = zp;
-      ws.tid[s * 32 + p] = ip;
+      ws.tz[ws.li<kCounted>(s, p)] = zp;
+      ws.tid[ws.li<kCounted>(s, p)] = ip;
       --s;
     }
-    ws.tz[s * 32 + p] = zc;
-    ws.tid[s * 32 + p] = f;
+    ws.tz[ws.li<kCounted>(s, p)] = zc;
+    ws.tid[ws.li<kCounted>(s, p)] = f;
   }
 }
 
@@ -681,8 +692,8 @@ __device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane)
       int32_t id[KMAX];
 #pragma unroll
       for (int s = 0; s < KMAX; ++s) {
-        z[s] = s < K ? ws.tz[s * 32 + lane] : pos_inf();
-        id[s] = s < K ? ws.tid[s * 32 + lane] : INT_MAX;
+        z[s] = s < K ? ws.tz[ws.li<(KMAX == 0)>(s, lane)] : pos_inf();
+        id[s] = s < K ? ws.tid[ws.li<(KMAX == 0)>(s, lane)] : INT_MAX;
       }
       for (int c = 0; c < n; ++c) {
         const double zc = ws.bz[c * 32 + lane];
@@ -705,8 +716,8 @@ __device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane)
 #pragma unroll
       for (int s = 0; s < KMAX; ++s) {
         if (s < K) {
-          ws.tz[s * 32 + lane] = z[s];
-          ws.tid[s * 32 + lane] = id[s];
+          ws.tz[ws.li<(KMAX == 0)>(s, lane)] = z[s];
+          ws.tid[ws.li<(KMAX == 0)>(s, lane)] = id[s];
         }
       }
     }
@@ -832,7 +843,7 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
         const int k = (head + lo) % kRing;
         // K-th-depth cull: every z this face can produce is > its key; if the key already exceeds the pixel's
         // current K-th candidate the face cannot enter the pixel's list (strict (z, id) order, MR:138-140)
-        keep = !A.zsort || !((double)ws.fkey[k] > ws.tz[(K - 1) * 32 + p]);
+        keep = !A.zsort || !((double)ws.fkey[k] > ws.tz[ws.li<(KMAX == 0)>(K - 1, p)]);
         entry = ((uint32_t)k << 5) | (uint32_t)p;
       }
       STAT_ADD(2, __popc(__ballot_sync(0xffffffffu, act)));
@@ -879,11 +890,12 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(K);
     ws.d = reinterpret_cast<double*>(base);
     ws.tz = ws.d + kNF * kRing;
-    ws.bz = ws.tz + K * 32;
+    ws.bz = ws.tz + (K + 1) * 32;
+    ws.ls = K + 1;
     ws.pxy = ws.bz + kBuf * 32;
     ws.fid = reinterpret_cast<int32_t*>(ws.pxy + 12);
     ws.tid = ws.fid + kRing;
-    ws.bid = ws.tid + K * 32;
+    ws.bid = ws.tid + (K + 1) * 32;
     ws.rect = reinterpret_cast<uint32_t*>(ws.bid + kBuf * 32);
     ws.fkey = reinterpret_cast<float*>(ws.rect + kRing);
     ws.bcnt = reinterpret_cast<int32_t*>(ws.fkey + kRing);
@@ -929,8 +941,8 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       }
     }
     for (int s = 0; s < K; ++s) {
-      ws.tz[s * 32 + lane] = pos_inf();
-      ws.tid[s * 32 + lane] = INT_MAX;
+      ws.tz[ws.li<(KMAX == 0)>(s, lane)] = pos_inf();
+      ws.tid[ws.li<(KMAX == 0)>(s, lane)] = INT_MAX;
     }
     ws.bcnt[lane] = 0;
     ws.tcnt[lane] = 0;
@@ -1011,7 +1023,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
             __syncwarp();
           }
           if (A.zsort) {  // max of the K-th depths (the list tails alone are a valid, looser threshold)
-            double t = valid_px ? ws.tz[(K - 1) * 32 + lane] : -pos_inf();
+            double t = valid_px ? ws.tz[ws.li<(KMAX == 0)>(K - 1, lane)] : -pos_inf();
 #pragma unroll
             for (int d = 16; d >= 1; d >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, d));
             T = t;
@@ -1044,8 +1056,8 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
         const int row = pix >> 3, col = pix & 7;
         if (row >= vh || col >= vw) return;
         slot = (((int64_t)b * A.H + mi0 + row) * A.W + mj0 + col) * K + s;
-        f = ws.tid[s * 32 + pix];
-        z = ws.tz[s * 32 + pix];
+        f = ws.tid[ws.li<(KMAX == 0)>(s, pix)];
+        z = ws.tz[ws.li<(KMAX == 0)>(s, pix)];
         qx = ws.pxy[col];
         qy = ws.pxy[8 + row];
         if (f != INT_MAX) {
@@ -1079,7 +1091,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       const double px = pixel_x(A.W, pj), py = pixel_y(A.H, pi);
       const int64_t slot0 = (((int64_t)b * A.H + pi) * A.W + pj) * K;
       double vnext[9];
-      int32_t fnext = ws.tid[lane];
+      int32_t fnext = ws.tid[ws.li<(KMAX == 0)>(0, lane)];
       if (fnext != INT_MAX) {
 #pragma unroll
         for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
@@ -1090,9 +1102,9 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       bool any = false;
       if constexpr (kMode == 2) {
         for (int s = 0; s < K; ++s) {
-          if (ws.tid[s * 32 + lane] == INT_MAX) continue;
+          if (ws.tid[ws.li<(KMAX == 0)>(s, lane)] == INT_MAX) continue;
           any = true;
-          const double zi = blend_zinv(ws.tz[s * 32 + lane], A.blend);
+          const double zi = blend_zinv(ws.tz[ws.li<(KMAX == 0)>(s, lane)], A.blend);
           zinv_max = zinv_max < zi ? zi : zinv_max;  // std::max(zinv_max, zinv)
         }
       }
@@ -1101,7 +1113,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
         double v[9];
 #pragma unroll
         for (int t = 0; t < 9; ++t) v[t] = vnext[t];
-        fnext = s + 1 < K ? ws.tid[(s + 1) * 32 + lane] : INT_MAX;
+        fnext = s + 1 < K ? ws.tid[ws.li<(KMAX == 0)>(s + 1, lane)] : INT_MAX;
         if (fnext != INT_MAX) {
 #pragma unroll
           for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
@@ -1114,7 +1126,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
           if (f != INT_MAX) {
             double c[3], prob;
             softmax_slot(A, v, f, px, py, c, prob);
-            const double zi = blend_zinv(ws.tz[s * 32 + lane], A.blend);
+            const double zi = blend_zinv(ws.tz[ws.li<(KMAX == 0)>(s, lane)], A.blend);
             const double w = prob * exp((zi - zinv_max) / A.blend.gamma);
             wsum += w;
             acc[0] += c[0] * w;  // Vec3 += Vec3 * double
@@ -1122,7 +1134,7 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
             acc[2] += c[2] * w;
           }
         } else {
-          emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[s * 32 + lane], f, v, px, py);
+          emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[ws.li<(KMAX == 0)>(s, lane)], f, v, px, py);
         }
       }
       if constexpr (kMode == 1) A.alpha[((int64_t)b * A.H + pi) * A.W + pj] = (OutT)(1.0 - keep);  // shading.cpp:86
