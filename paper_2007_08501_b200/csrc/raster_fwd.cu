@@ -474,6 +474,14 @@ enum : int {
 };
 
 // one warp's shared memory: staged-face ring (SoA) + top-K lists of its 32 pixels
+#ifndef DR_KBUF
+#define DR_KBUF 8
+#endif
+constexpr int kBuf = DR_KBUF;  // buffered candidates per pixel before the owner lane merges them into its list
+
+#ifndef DR_BUF_PM
+#define DR_BUF_PM 0  // measured: the conflict-free layout is 0.4 % slower (index math > the conflicts it removes)
+#endif
 struct WarpSmem {
   double* d;        // [kNF][kRing]
   int32_t* fid;     // [kRing]
@@ -496,6 +504,10 @@ struct WarpSmem {
   // register-merge path (C4 6.18 -> 6.21 ms), so it is used where KMAX == 0 only.
   template <bool kPM>
   __device__ __forceinline__ int li(int s, int p) const { return kPM ? p * ls + s : s * 32 + p; }
+  // element c of pixel p's candidate buffer. DR_BUF_PM: pixel-major rows of kBuf + 1 (lanes appending to the
+  // same pixel write consecutive words, the owner-lane merge reads at stride kBuf + 1: both conflict-free);
+  // otherwise [kBuf][32] (same-pixel appends all hit one bank)
+  __device__ __forceinline__ int bi(int c, int p) const { return DR_BUF_PM ? p * (kBuf + 1) + c : c * 32 + p; }
 
   __device__ __forceinline__ double get(int f, int k) const { return d[f * kRing + k]; }
   __device__ __forceinline__ void put(int f, int k, double v) const { d[f * kRing + k] = v; }
@@ -545,18 +557,13 @@ struct WarpSmem {
   }
 };
 
-#ifndef DR_KBUF
-#define DR_KBUF 8
-#endif
-constexpr int kBuf = DR_KBUF;  // buffered candidates per pixel before the owner lane merges them into its list
-
 // per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt | pairq |
 // tcnt
 __host__ __device__ constexpr size_t warp_smem_bytes(int K) {
   return (size_t)kNF * kRing * sizeof(double) + (size_t)(K + 1) * 32 * sizeof(double) +
-         (size_t)kBuf * 32 * sizeof(double) + 12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) +
+         (size_t)(kBuf + 1) * 32 * sizeof(double) + 12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) +
          (size_t)(K + 1) * 32 * sizeof(int32_t) +
-         (size_t)kBuf * 32 * sizeof(int32_t) + (size_t)kRing * (sizeof(uint32_t) + sizeof(float)) +
+         (size_t)(kBuf + 1) * 32 * sizeof(int32_t) + (size_t)kRing * (sizeof(uint32_t) + sizeof(float)) +
          32 * sizeof(int32_t) + kPairQ * sizeof(uint32_t) + 32 * sizeof(int32_t) +
          8;  // + pad keeps the next warp's base 8-byte aligned
 }
@@ -686,7 +693,7 @@ __device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane)
   const int n = ws.bcnt[lane];
   if (n > 0) {
     if constexpr (KMAX == 0) {
-      for (int c = 0; c < n; ++c) list_insert<true>(ws, K, lane, ws.bz[c * 32 + lane], ws.bid[c * 32 + lane]);
+      for (int c = 0; c < n; ++c) list_insert<true>(ws, K, lane, ws.bz[ws.bi(c, lane)], ws.bid[ws.bi(c, lane)]);
     } else {
       double z[KMAX];
       int32_t id[KMAX];
@@ -696,8 +703,8 @@ __device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane)
         id[s] = s < K ? ws.tid[ws.li<(KMAX == 0)>(s, lane)] : INT_MAX;
       }
       for (int c = 0; c < n; ++c) {
-        const double zc = ws.bz[c * 32 + lane];
-        const int32_t ic = ws.bid[c * 32 + lane];
+        const double zc = ws.bz[ws.bi(c, lane)];
+        const int32_t ic = ws.bid[ws.bi(c, lane)];
         if (!cand_less(zc, ic, z[KMAX - 1], id[KMAX - 1])) continue;  // not below the list tail
 #pragma unroll
         for (int s = KMAX - 1; s >= 0; --s) {
@@ -756,8 +763,8 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
     }
     if (pass) {
       if (rank < kBuf) {
-        ws.bz[(base + rank) * 32 + p] = z;
-        ws.bid[(base + rank) * 32 + p] = f;
+        ws.bz[ws.bi(base + rank, p)] = z;
+        ws.bid[ws.bi(base + rank, p)] = f;
       }
       if (rank == 0) ws.bcnt[p] = base + min(n_same, kBuf);
     }
@@ -892,11 +899,11 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     ws.tz = ws.d + kNF * kRing;
     ws.bz = ws.tz + (K + 1) * 32;
     ws.ls = K + 1;
-    ws.pxy = ws.bz + kBuf * 32;
+    ws.pxy = ws.bz + (kBuf + 1) * 32;
     ws.fid = reinterpret_cast<int32_t*>(ws.pxy + 12);
     ws.tid = ws.fid + kRing;
     ws.bid = ws.tid + (K + 1) * 32;
-    ws.rect = reinterpret_cast<uint32_t*>(ws.bid + kBuf * 32);
+    ws.rect = reinterpret_cast<uint32_t*>(ws.bid + (kBuf + 1) * 32);
     ws.fkey = reinterpret_cast<float*>(ws.rect + kRing);
     ws.bcnt = reinterpret_cast<int32_t*>(ws.fkey + kRing);
     ws.pairq = reinterpret_cast<uint32_t*>(ws.bcnt + 32);
