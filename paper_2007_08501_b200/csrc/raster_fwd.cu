@@ -475,12 +475,21 @@ enum : int {
 
 // one warp's shared memory: staged-face ring (SoA) + top-K lists of its 32 pixels
 #ifndef DR_KBUF
-#define DR_KBUF 8
+#define DR_KBUF 8  // shared-memory list path (K > 8)
 #endif
-constexpr int kBuf = DR_KBUF;  // buffered candidates per pixel before the owner lane merges them into its list
+#ifndef DR_KBUF_REG
+#define DR_KBUF_REG 12  // register-merge path (K <= 8)
+#endif
+// buffered candidates per pixel before the owner lane merges them into its list. Measured: 12 instead of 8 on the
+// register path (C4 k_fine 6.16 -> 6.00 ms: fewer overflow merges); on the shared-memory list path 12 costs
+// shared memory per warp (C5 6.70 -> 8.52 ms) and 6 is no better (6.74), so 8 there
+constexpr int kBufSmem = DR_KBUF, kBufReg = DR_KBUF_REG;
+__host__ __device__ constexpr int buf_cap(int K) { return K <= 8 ? kBufReg : kBufSmem; }
+template <int KMAX>
+constexpr int kBufT = KMAX == 0 ? kBufSmem : kBufReg;
 
-#ifndef DR_BUF_PM
-#define DR_BUF_PM 0  // measured: the conflict-free layout is 0.4 % slower (index math > the conflicts it removes)
+#ifndef DR_EMIT_UNROLL2
+#define DR_EMIT_UNROLL2 0
 #endif
 struct WarpSmem {
   double* d;        // [kNF][kRing]
@@ -489,8 +498,8 @@ struct WarpSmem {
   float* fkey;      // [kRing] depth key (zkey) of the staged face
   double* tz;       // [K][32]      sorted top-K lists, column p = pixel p of the micro-tile
   int32_t* tid;     // [K][32]
-  double* bz;       // [kBuf][32]   unsorted per-pixel candidate buffers (merged by the owner lane)
-  int32_t* bid;     // [kBuf][32]
+  double* bz;       // [buf_cap(K)][32]   unsorted per-pixel candidate buffers (merged by the owner lane)
+  int32_t* bid;     // [buf_cap(K)][32]
   int32_t* bcnt;    // [32]
   double* pxy;      // [12] pixel-centre NDC coordinates of the micro-tile: x of its 8 columns, y of its 4 rows
   uint32_t* pairq;  // [kPairQ] queued (ring slot << 5 | pixel) pairs awaiting evaluation
@@ -504,10 +513,9 @@ struct WarpSmem {
   // register-merge path (C4 6.18 -> 6.21 ms), so it is used where KMAX == 0 only.
   template <bool kPM>
   __device__ __forceinline__ int li(int s, int p) const { return kPM ? p * ls + s : s * 32 + p; }
-  // element c of pixel p's candidate buffer. DR_BUF_PM: pixel-major rows of kBuf + 1 (lanes appending to the
-  // same pixel write consecutive words, the owner-lane merge reads at stride kBuf + 1: both conflict-free);
-  // otherwise [kBuf][32] (same-pixel appends all hit one bank)
-  __device__ __forceinline__ int bi(int c, int p) const { return DR_BUF_PM ? p * (kBuf + 1) + c : c * 32 + p; }
+  // element c of pixel p's candidate buffer, [cap][32] (a pixel-major, conflict-free layout measured 0.4 %
+  // slower: the index math costs more than the conflicts of same-pixel appends)
+  __device__ __forceinline__ int bi(int c, int p) const { return c * 32 + p; }
 
   __device__ __forceinline__ double get(int f, int k) const { return d[f * kRing + k]; }
   __device__ __forceinline__ void put(int f, int k, double v) const { d[f * kRing + k] = v; }
@@ -559,13 +567,18 @@ struct WarpSmem {
 
 // per-warp layout, 8-byte aligned pieces first: d | tz | bz | pxy | fid | tid | bid | rect | fkey | bcnt | pairq |
 // tcnt
-__host__ __device__ constexpr size_t warp_smem_bytes(int K) {
+template <int CAP>
+__host__ __device__ constexpr size_t warp_smem_bytes_cap(int K) {
   return (size_t)kNF * kRing * sizeof(double) + (size_t)(K + 1) * 32 * sizeof(double) +
-         (size_t)(kBuf + 1) * 32 * sizeof(double) + 12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) +
-         (size_t)(K + 1) * 32 * sizeof(int32_t) +
-         (size_t)(kBuf + 1) * 32 * sizeof(int32_t) + (size_t)kRing * (sizeof(uint32_t) + sizeof(float)) +
-         32 * sizeof(int32_t) + kPairQ * sizeof(uint32_t) + 32 * sizeof(int32_t) +
-         8;  // + pad keeps the next warp's base 8-byte aligned
+         (size_t)CAP * 32 * sizeof(double) + 12 * sizeof(double) + (size_t)kRing * sizeof(int32_t) +
+         (size_t)(K + 1) * 32 * sizeof(int32_t) + (size_t)CAP * 32 * sizeof(int32_t) +
+         (size_t)kRing * (sizeof(uint32_t) + sizeof(float)) + 32 * sizeof(int32_t) + kPairQ * sizeof(uint32_t) +
+         32 * sizeof(int32_t) + 8;  // + pad keeps the next warp's base 8-byte aligned
+}
+// (the kernel uses the compile-time-capacity form: a runtime select in the warp's base offset cost ptxas ~20
+// registers and spills)
+__host__ __device__ constexpr size_t warp_smem_bytes(int K) {
+  return K <= 8 ? warp_smem_bytes_cap<kBufReg>(K) : warp_smem_bytes_cap<kBufSmem>(K);
 }
 
 // Rectangle of the micro-tile (rows i0..i0+3, cols j0..j0+7, limited to vh x vw existing pixels) covered by
@@ -751,7 +764,7 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
     const int rank = __popc(peers & ((1u << lane) - 1u));
     const int n_same = __popc(peers);
     int base = pass ? ws.bcnt[p] : 0;
-    if (__any_sync(0xffffffffu, pass && base + n_same > kBuf)) {
+    if (__any_sync(0xffffffffu, pass && base + n_same > kBufT<KMAX>)) {
       __syncwarp();
 #if DR_OVF_NOINLINE
       merge_buffers_ool<KMAX>(ws, K, lane);
@@ -762,17 +775,17 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
       base = 0;
     }
     if (pass) {
-      if (rank < kBuf) {
+      if (rank < kBufT<KMAX>) {
         ws.bz[ws.bi(base + rank, p)] = z;
         ws.bid[ws.bi(base + rank, p)] = f;
       }
-      if (rank == 0) ws.bcnt[p] = base + min(n_same, kBuf);
+      if (rank == 0) ws.bcnt[p] = base + min(n_same, kBufT<KMAX>);
     }
     __syncwarp();
-    // more than kBuf candidates for one pixel in one step (rare): insert the excess directly, one at a time
-    const int extra = __reduce_max_sync(0xffffffffu, pass ? n_same - kBuf : 0);
+    // more than kBufT<KMAX> candidates for one pixel in one step (rare): insert the excess directly, one at a time
+    const int extra = __reduce_max_sync(0xffffffffu, pass ? n_same - kBufT<KMAX> : 0);
     for (int rr = 0; rr < extra; ++rr) {
-      if (pass && rank == kBuf + rr) list_insert<KMAX == 0>(ws, K, p, z, f);
+      if (pass && rank == kBufT<KMAX> + rr) list_insert<KMAX == 0>(ws, K, p, z, f);
       __syncwarp();
     }
   }
@@ -894,16 +907,16 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
   const int K = A.K;
   WarpSmem ws;
   {
-    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(K);
+    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes_cap<kBufT<KMAX>>(K);
     ws.d = reinterpret_cast<double*>(base);
     ws.tz = ws.d + kNF * kRing;
     ws.bz = ws.tz + (K + 1) * 32;
     ws.ls = K + 1;
-    ws.pxy = ws.bz + (kBuf + 1) * 32;
+    ws.pxy = ws.bz + kBufT<KMAX> * 32;  // == buf_cap(K): KMAX == 0 exactly when K > 8
     ws.fid = reinterpret_cast<int32_t*>(ws.pxy + 12);
     ws.tid = ws.fid + kRing;
     ws.bid = ws.tid + (K + 1) * 32;
-    ws.rect = reinterpret_cast<uint32_t*>(ws.bid + (kBuf + 1) * 32);
+    ws.rect = reinterpret_cast<uint32_t*>(ws.bid + kBufT<KMAX> * 32);
     ws.fkey = reinterpret_cast<float*>(ws.rect + kRing);
     ws.bcnt = reinterpret_cast<int32_t*>(ws.fkey + kRing);
     ws.pairq = reinterpret_cast<uint32_t*>(ws.bcnt + 32);
@@ -1076,6 +1089,9 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       double vn[9], zn = 0.0, xn = 0.0, yn = 0.0;
       int64_t sn;
       fetch(lane, fn, vn, sn, zn, xn, yn);
+#if DR_EMIT_UNROLL2
+#pragma unroll 2
+#endif
       for (int q0 = 0; q0 < 32 * K; q0 += 32) {
         const int32_t f = fn;
         const int64_t slot = sn;
