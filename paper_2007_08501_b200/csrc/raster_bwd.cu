@@ -622,8 +622,203 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
   }
 }
 
+// Slot-compacted variant (K <= kSilQMaxK): the warp's 32 pixels x K slots are compacted to their occupied
+// slots, and the two geometry passes run lane-per-SLOT, 32 occupied slots per step (as K3), instead of
+// lane-per-pixel walks where a pixel with few candidates idles its lane while a busy neighbour works:
+//   A  pix_to_face block + d_alpha + pixel centres -> shared memory; the occupied slots of active pixels -> queue
+//   B  per queued slot: distance envelope + prob = sigmoid(-dist / sigma)          (lane per slot)
+//   C  per pixel: suffix products, then coefficient da * prefix * suffix * dprob   (lane per pixel, K steps)
+//   D  per queued slot: the envelope gradient, reduce_by_face, fp64 atomics       (lane per slot)
+constexpr int kSilQMaxK = 16;
+#ifndef DR_SILQ_WARPS
+#define DR_SILQ_WARPS 1  // one-warp CTAs: 14 resident per SM by shared memory (C4: 4 warps 3.65 ms, 2 3.11, 1 2.87)
+#endif
+constexpr int kSilQWarps = DR_SILQ_WARPS;
+
+__host__ __device__ __forceinline__ size_t silq_warp_bytes(int K) {
+  const size_t n = (size_t)32 * K;
+  return n * (5 * sizeof(double) + sizeof(int64_t) + sizeof(int32_t) + sizeof(int32_t) + sizeof(uint16_t)) +
+         32 * 4 * sizeof(double) + 8;
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBwdArgs A) {
+  extern __shared__ double silq_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int K = A.K;
+  const int n = 32 * K;
+  unsigned char* wb = reinterpret_cast<unsigned char*>(silq_smem) + (size_t)wid * silq_warp_bytes(K);
+  double* PR = reinterpret_cast<double*>(wb);  // [n] prob (-1: empty / inactive)
+  double* EX = PR + n;                          // [n] (qq - p).x * 2 sign
+  double* EY = EX + n;                          // [n] (qq - p).y * 2 sign
+  double* BT = EY + n;                          // [n] t on the nearest edge
+  double* CO = BT + n;                          // [n] suffix products, then the d_dist coefficient
+  double* PXY = CO + n;                         // [32][2] pixel centres
+  double* DAS = PXY + 64;                       // [32] staged d_alpha of the next chunk (fp32 or fp64 bits)
+  int64_t* STG = reinterpret_cast<int64_t*>(DAS + 32);  // [n] staged pix_to_face of the next chunk
+  int32_t* FID = reinterpret_cast<int32_t*>(STG + n);   // [n] face id per slot (-1: empty)
+  int32_t* BE = FID + n;                                // [n] nearest edge
+  uint16_t* Q = reinterpret_cast<uint16_t*>(BE + n);    // [n] queued slot offsets
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t HW = (int64_t)A.H * A.W;
+  // the next chunk's pix_to_face block and d_alpha stream into shared memory (cp.async) while this one computes
+  auto issue = [&](int64_t b0) {
+    const int64_t pix = b0 + lane;
+    if (pix < A.npix) {
+      if (A.d_alpha64) cp_async8(DAS + lane, A.d_alpha64 + pix);
+      else cp_async4(reinterpret_cast<float*>(DAS) + lane, A.d_alpha + pix);
+    }
+    const int64_t ns = (A.npix - b0 < 32 ? A.npix - b0 : 32) * K;
+    for (int t = lane; t < ns; t += 32) cp_async8(STG + t, A.p2f + b0 * K + t);
+    cp_async_commit();
+  };
+  if (warp * 32 < A.npix) issue(warp * 32);
+  for (int64_t base = warp * 32; base < A.npix; base += nwarps * 32) {
+    cp_async_wait_all();
+    __syncwarp();
+    // A: this lane's pixel
+    const int64_t pix = base + lane;
+    const double da = pix < A.npix ? (A.d_alpha64 ? DAS[lane] : (double)reinterpret_cast<const float*>(DAS)[lane])
+                                   : 0.0;
+    const bool act = da != 0.0;  // shading.cpp:102: pixels with d_alpha == 0 contribute nothing
+    const unsigned act_mask = __ballot_sync(0xffffffffu, act);
+    const int64_t nslots = (A.npix - base < 32 ? A.npix - base : 32) * K;
+    int q = 0;
+    if (act_mask) {
+      const int rem = act ? (int)(pix % HW) : 0;
+      const int i = rem / A.W, j = rem - i * A.W;
+      PXY[2 * lane] = pixel_x(A.W, j);  // MR:357
+      PXY[2 * lane + 1] = pixel_y(A.H, i);
+      for (int t0 = 0; t0 < n; t0 += 32) {  // compacted in slot order
+        const int t = t0 + lane;
+        const int64_t f = t < nslots ? STG[t] : -1;
+        const bool occ = f >= 0 && f < A.F && ((act_mask >> (t / K)) & 1u);
+        FID[t] = occ ? (int32_t)f : -1;
+        PR[t] = -1.0;
+        const unsigned m = __ballot_sync(0xffffffffu, occ);
+        if (occ) Q[q + __popc(m & ((1u << lane) - 1u))] = (uint16_t)t;
+        q += __popc(m);
+      }
+    }
+    __syncwarp();
+    if (base + nwarps * 32 < A.npix) issue(base + nwarps * 32);  // the staging buffers are free again
+    if (!act_mask) continue;
+    // B: envelope + prob per queued slot (next batch's face_verts prefetched)
+    {
+      double vn[9];
+      int tn = lane < q ? Q[lane] : -1;
+      int32_t fn = tn >= 0 ? FID[tn] : -1;
+      if (fn >= 0) {
+#pragma unroll
+        for (int u = 0; u < 9; ++u) vn[u] = __ldg(A.fv + 9 * (int64_t)fn + u);
+      }
+      for (int q0 = 0; q0 < q; q0 += 32) {
+        const int t = tn;
+        double v[9];
+#pragma unroll
+        for (int u = 0; u < 9; ++u) v[u] = vn[u];
+        tn = q0 + 32 + lane < q ? Q[q0 + 32 + lane] : -1;
+        fn = tn >= 0 ? FID[tn] : -1;
+        if (fn >= 0) {
+#pragma unroll
+          for (int u = 0; u < 9; ++u) vn[u] = __ldg(A.fv + 9 * (int64_t)fn + u);
+        }
+        if (t >= 0) {
+          const int pl = t / K;
+          const V2 p{PXY[2 * pl], PXY[2 * pl + 1]};
+          double dist, bt, sign;
+          int be;
+          V2 qq;
+          silhouette_envelope(v, p, dist, be, bt, qq, sign);
+          // sigmoid(-dist / sigma) (shading.cpp:9, 82): fp32 exp for the fp32 cotangent, fp64 for the fp64 one
+          PR[t] = A.d_alpha64 ? 1.0 / (1.0 + exp(dist / A.sigma))
+                              : 1.0 / (1.0 + (double)expf((float)(dist / A.sigma)));
+          EX[t] = (qq.x - p.x) * (2.0 * sign);
+          EY[t] = (qq.y - p.y) * (2.0 * sign);
+          BT[t] = bt;
+          BE[t] = be;
+        }
+      }
+    }
+    __syncwarp();
+    // C: per pixel, d_dists (shading.cpp:115-117) = da * prod_{other occupied} (1 - prob) * (-prob (1 - prob) / sigma)
+    if (act) {
+      const int r = lane * K;
+      double suf = 1.0;
+      for (int s = K - 1; s >= 0; --s) {
+        CO[r + s] = suf;
+        const double pr = PR[r + s];
+        if (pr >= 0.0) suf *= 1.0 - pr;
+      }
+      double pre = 1.0;
+      for (int s = 0; s < K; ++s) {
+        const double pr = PR[r + s];
+        if (pr >= 0.0) {
+          CO[r + s] = da * (pre * CO[r + s]) * (-pr * (1.0 - pr) / A.sigma);
+          pre *= 1.0 - pr;
+        }
+      }
+    }
+    __syncwarp();
+    // D: the frozen-edge envelope gradient (MR:46-69) per queued slot, summed per face across the warp
+    for (int q0 = 0; q0 < q; q0 += 32) {
+      const int t = q0 + lane < q ? Q[q0 + lane] : -1;
+      int32_t fid = -1;
+      double g[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (t >= 0) {
+        fid = FID[t];
+        const double d_out = CO[t];
+        const double bt = BT[t];
+        const int be = BE[t];
+        const V2 gg{EX[t] * d_out, EY[t] * d_out};  // (qq - p) * (2 sign d_out): the same single rounding
+        const V2 g_first = gg * (1.0 - bt), g_second = gg * bt;
+        const int v1 = be == 2 ? 0 : be + 1;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {  // vertex be gets g_first, the next one g_second (selects, no local array)
+          g[2 * k] = be == k ? g_first.x : (v1 == k ? g_second.x : 0.0);
+          g[2 * k + 1] = be == k ? g_first.y : (v1 == k ? g_second.y : 0.0);
+        }
+      }
+      if (reduce_by_face<6>(fid, lane, g)) {
+        double* out = A.grad + 9 * (int64_t)fid;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          atomicAdd(out + 3 * k, g[2 * k]);
+          atomicAdd(out + 3 * k + 1, g[2 * k + 1]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+#ifndef DR_SIL_Q
+#define DR_SIL_Q 1
+#endif
 cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
+  if (DR_SIL_Q && A.K <= kSilQMaxK) {
+    const size_t smem = (size_t)kSilQWarps * silq_warp_bytes(A.K);
+    cudaError_t e = cudaFuncSetAttribute(k_silhouette_backward_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 48 * 1024));
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_silhouette_backward_q, kSilQWarps * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int64_t need = (A.npix + kSilQWarps * 32 - 1) / (kSilQWarps * 32);
+    if (blocks > need) blocks = need;
+    k_silhouette_backward_q<<<(unsigned)blocks, kSilQWarps * 32, smem, st>>>(A);
+    return cudaGetLastError();
+  }
   const bool store = A.K <= kSilStoreMaxK;
   const size_t per_warp = (size_t)A.K * 32 * (store ? 5 * sizeof(double) : 2 * sizeof(double)) +
                           (size_t)A.K * 16 * sizeof(double) * (store ? 2 : 1);  // + edge ids + the p2f block

@@ -120,6 +120,19 @@ def main():
            "fragments_ms": timed(fragments, a.steps, a.warmup), "fused_vs_unfused_grad_rel_err": err,
            "softmax_fused_ms": timed(soft_fused, a.steps, a.warmup),
            "softmax_unfused_ms": timed(soft_unfused, a.steps, a.warmup), "softmax_grad_rel_err": serr}
+    from paper_2007_08501_b200 import KernelTimer
+
+    for name, fn in (("fused_kernels_ms", fused), ("softmax_fused_kernels_ms", soft_fused),
+                     ("fragments_kernels_ms", fragments)):
+        torch.cuda.synchronize()
+        with KernelTimer() as kt:
+            for _ in range(a.steps):
+                fn()
+            torch.cuda.synchronize()
+        per = {}
+        for k, ms in kt.records:
+            per[k] = per.get(k, 0.0) + ms / a.steps
+        out[name] = per
     out["speedup"] = out["unfused_ms"] / out["fused_ms"]
     out["softmax_speedup"] = out["softmax_unfused_ms"] / out["softmax_fused_ms"]
     print(json.dumps(out))
