@@ -629,14 +629,19 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
 //   B  per queued slot: distance envelope + prob = sigmoid(-dist / sigma)          (lane per slot)
 //   C  per pixel: suffix products, then coefficient da * prefix * suffix * dprob   (lane per pixel, K steps)
 //   D  per queued slot: the envelope gradient, reduce_by_face, fp64 atomics       (lane per slot)
-constexpr int kSilQMaxK = 16;
+#ifndef DR_SILQ_MAXK
+#define DR_SILQ_MAXK 64
+#endif
+constexpr int kSilQMaxK = DR_SILQ_MAXK;
 #ifndef DR_SILQ_WARPS
 #define DR_SILQ_WARPS 1  // one-warp CTAs: 14 resident per SM by shared memory (C4: 4 warps 3.65 ms, 2 3.11, 1 2.87)
 #endif
 constexpr int kSilQWarps = DR_SILQ_WARPS;
 
+// pixels per chunk: 32, or fewer for large K so a chunk stays <= 512 slots
+__host__ __device__ __forceinline__ int silq_pixels(int K) { return K >= 512 ? 1 : min(32, 512 / K); }
 __host__ __device__ __forceinline__ size_t silq_warp_bytes(int K) {
-  const size_t n = (size_t)32 * K;
+  const size_t n = (size_t)silq_pixels(K) * K;
   return n * (5 * sizeof(double) + sizeof(int64_t) + sizeof(int32_t) + sizeof(int32_t) + sizeof(uint16_t)) +
          32 * 4 * sizeof(double) + 8;
 }
@@ -650,7 +655,9 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
   extern __shared__ double silq_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
-  const int n = 32 * K;
+  const int KS = K;  // per-pixel row stride (K + 1, conflict-free for the lane-per-pixel pass, measured slower)
+  const int P = silq_pixels(K);
+  const int n = P * KS;
   unsigned char* wb = reinterpret_cast<unsigned char*>(silq_smem) + (size_t)wid * silq_warp_bytes(K);
   double* PR = reinterpret_cast<double*>(wb);  // [n] prob (-1: empty / inactive)
   double* EX = PR + n;                          // [n] (qq - p).x * 2 sign
@@ -669,44 +676,47 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
   // the next chunk's pix_to_face block and d_alpha stream into shared memory (cp.async) while this one computes
   auto issue = [&](int64_t b0) {
     const int64_t pix = b0 + lane;
-    if (pix < A.npix) {
+    if (lane < P && pix < A.npix) {
       if (A.d_alpha64) cp_async8(DAS + lane, A.d_alpha64 + pix);
       else cp_async4(reinterpret_cast<float*>(DAS) + lane, A.d_alpha + pix);
     }
-    const int64_t ns = (A.npix - b0 < 32 ? A.npix - b0 : 32) * K;
+    const int64_t ns = (A.npix - b0 < P ? A.npix - b0 : P) * K;
     for (int t = lane; t < ns; t += 32) cp_async8(STG + t, A.p2f + b0 * K + t);
     cp_async_commit();
   };
-  if (warp * 32 < A.npix) issue(warp * 32);
-  for (int64_t base = warp * 32; base < A.npix; base += nwarps * 32) {
+  if (warp * P < A.npix) issue(warp * P);
+  for (int64_t base = warp * P; base < A.npix; base += nwarps * P) {
     cp_async_wait_all();
     __syncwarp();
     // A: this lane's pixel
     const int64_t pix = base + lane;
-    const double da = pix < A.npix ? (A.d_alpha64 ? DAS[lane] : (double)reinterpret_cast<const float*>(DAS)[lane])
+    const double da = lane < P && pix < A.npix ? (A.d_alpha64 ? DAS[lane] : (double)reinterpret_cast<const float*>(DAS)[lane])
                                    : 0.0;
     const bool act = da != 0.0;  // shading.cpp:102: pixels with d_alpha == 0 contribute nothing
     const unsigned act_mask = __ballot_sync(0xffffffffu, act);
-    const int64_t nslots = (A.npix - base < 32 ? A.npix - base : 32) * K;
+    const int64_t nslots = (A.npix - base < P ? A.npix - base : P) * K;
     int q = 0;
     if (act_mask) {
       const int rem = act ? (int)(pix % HW) : 0;
       const int i = rem / A.W, j = rem - i * A.W;
       PXY[2 * lane] = pixel_x(A.W, j);  // MR:357
       PXY[2 * lane + 1] = pixel_y(A.H, i);
-      for (int t0 = 0; t0 < n; t0 += 32) {  // compacted in slot order
+      for (int t0 = 0; t0 < P * K; t0 += 32) {  // compacted in slot order
         const int t = t0 + lane;
+        const int tp = t;
         const int64_t f = t < nslots ? STG[t] : -1;
-        const bool occ = f >= 0 && f < A.F && ((act_mask >> (t / K)) & 1u);
-        FID[t] = occ ? (int32_t)f : -1;
-        PR[t] = -1.0;
+        const bool occ = t < P * K && f >= 0 && f < A.F && ((act_mask >> (t / K)) & 1u);
+        if (t < P * K) {
+          FID[tp] = occ ? (int32_t)f : -1;
+          PR[tp] = -1.0;
+        }
         const unsigned m = __ballot_sync(0xffffffffu, occ);
-        if (occ) Q[q + __popc(m & ((1u << lane) - 1u))] = (uint16_t)t;
+        if (occ) Q[q + __popc(m & ((1u << lane) - 1u))] = (uint16_t)tp;
         q += __popc(m);
       }
     }
     __syncwarp();
-    if (base + nwarps * 32 < A.npix) issue(base + nwarps * 32);  // the staging buffers are free again
+    if (base + nwarps * P < A.npix) issue(base + nwarps * P);  // the staging buffers are free again
     if (!act_mask) continue;
     // B: envelope + prob per queued slot (next batch's face_verts prefetched)
     {
@@ -729,7 +739,7 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
           for (int u = 0; u < 9; ++u) vn[u] = __ldg(A.fv + 9 * (int64_t)fn + u);
         }
         if (t >= 0) {
-          const int pl = t / K;
+          const int pl = t / KS;
           const V2 p{PXY[2 * pl], PXY[2 * pl + 1]};
           double dist, bt, sign;
           int be;
@@ -748,7 +758,7 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
     __syncwarp();
     // C: per pixel, d_dists (shading.cpp:115-117) = da * prod_{other occupied} (1 - prob) * (-prob (1 - prob) / sigma)
     if (act) {
-      const int r = lane * K;
+      const int r = lane * KS;
       double suf = 1.0;
       for (int s = K - 1; s >= 0; --s) {
         CO[r + s] = suf;
@@ -802,7 +812,7 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
 #endif
 cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
-  if (DR_SIL_Q && A.K <= kSilQMaxK) {
+  if (DR_SIL_Q && A.K <= kSilQMaxK) {  // (any K: chunks shrink to 512 / K pixels)
     const size_t smem = (size_t)kSilQWarps * silq_warp_bytes(A.K);
     cudaError_t e = cudaFuncSetAttribute(k_silhouette_backward_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
@@ -814,7 +824,7 @@ cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = (int64_t)sms * per_sm;
-    const int64_t need = (A.npix + kSilQWarps * 32 - 1) / (kSilQWarps * 32);
+    const int64_t need = (A.npix + (int64_t)kSilQWarps * silq_pixels(A.K) - 1) / ((int64_t)kSilQWarps * silq_pixels(A.K));
     if (blocks > need) blocks = need;
     k_silhouette_backward_q<<<(unsigned)blocks, kSilQWarps * 32, smem, st>>>(A);
     return cudaGetLastError();
@@ -1037,9 +1047,257 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
   }
 }
 
+// Slot-compacted variant: a warp takes P = min(32, 512 / K) consecutive pixels; their occupied slots are queued
+// and the two geometry-heavy passes run lane-per-slot, 32 occupied slots per step:
+//   B  per slot: exact-sequence re-evaluation (fast divisions), inverse depth, opacity, interpolated colour
+//   C  per pixel (lane < P): zinv_max (the first occupied slot, see above), weights, the mean term, d_zinv_max,
+//      then per slot what = w / wsum, d_dists and d_zbuf (same operation order as the per-pixel kernel)
+//   D  per slot: d_bary from the vertex colours, the K3 chain, the colour cotangent, one 18-value reduce-by-face
+constexpr int kSoftQSlots = 512;
+
+__host__ __device__ __forceinline__ int softq_pixels(int K) { return K >= kSoftQSlots ? 1 : min(32, kSoftQSlots / K); }
+__host__ __device__ __forceinline__ size_t softq_warp_bytes(int K) {
+  const size_t n = (size_t)softq_pixels(K) * K;
+  return n * (6 * sizeof(double) + sizeof(int32_t) + sizeof(uint16_t)) + 32 * 5 * sizeof(double) + 16;
+}
+
+__global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
+  extern __shared__ double softq_smem[];
+  const int lane = threadIdx.x & 31;
+  const int K = A.K;
+  const int P = softq_pixels(K);
+  const int KS = K;  // per-pixel row stride (K + 1, conflict-free for the lane-per-pixel pass, measured slower)
+  const int n = P * KS;
+  double* ZI = softq_smem;  // [n] zinv (-1: empty; +2: clamped), then d_zbuf
+  double* PR = ZI + n;      // [n] prob, then d_dists
+  double* WT = PR + n;      // [n] weight, then what = w / wsum
+  double* C0 = WT + n;      // [n] interpolated colour
+  double* C1 = C0 + n;
+  double* C2 = C1 + n;
+  double* PXY = C2 + n;     // [32][2] pixel centres
+  double* DIM = PXY + 64;   // [32][3] d_image
+  int32_t* FID = reinterpret_cast<int32_t*>(DIM + 96);  // [n]
+  uint16_t* Q = reinterpret_cast<uint16_t*>(FID + n);   // [n]
+  BwdArgs<double> BA;
+  BA.persp = A.persp;
+  BA.clip = A.clip;
+  const int64_t HW = (int64_t)A.H * A.W;
+  const double zrange = A.blend.zfar - A.blend.znear;
+  for (int64_t base = (int64_t)blockIdx.x * P; base < A.npix; base += (int64_t)gridDim.x * P) {
+    const int np = (int)(A.npix - base < P ? A.npix - base : P);
+    if (lane < np) {
+      const int64_t pix = base + lane;
+      const int rem = (int)(pix % HW);
+      const int i = rem / A.W, j = rem - i * A.W;
+      PXY[2 * lane] = pixel_x(A.W, j);  // MR:357
+      PXY[2 * lane + 1] = pixel_y(A.H, i);
+      DIM[3 * lane] = (double)A.d_image[3 * pix];
+      DIM[3 * lane + 1] = (double)A.d_image[3 * pix + 1];
+      DIM[3 * lane + 2] = (double)A.d_image[3 * pix + 2];
+    }
+    // A: pix_to_face block -> queue of occupied slots (slot order; a (rank, pixel) order that groups shared
+    // faces for reduce_by_face measured slower: C4 15.1 -> 16.8 ms)
+    const int ns = np * K;
+    const int64_t* src = A.p2f + base * K;
+    int q = 0;
+    for (int t0 = 0; t0 < P * K; t0 += 32) {
+      const int t = t0 + lane;
+      const int tp = t;
+      const int64_t f = t < ns ? __ldcs(src + t) : -1;
+      const bool occ = f >= 0 && f < A.F;
+      if (t < P * K) {
+        FID[tp] = occ ? (int32_t)f : -1;
+        ZI[tp] = -1.0;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, occ);
+      if (occ) Q[q + __popc(m & ((1u << lane) - 1u))] = (uint16_t)tp;
+      q += __popc(m);
+    }
+    __syncwarp();
+    // B: per occupied slot
+    {
+      double vn[9];
+      int tn = lane < q ? Q[lane] : -1;
+      int32_t fn = tn >= 0 ? FID[tn] : -1;
+      if (fn >= 0) {
+#pragma unroll
+        for (int u = 0; u < 9; ++u) vn[u] = __ldg(A.fv + 9 * (int64_t)fn + u);
+      }
+      for (int q0 = 0; q0 < q; q0 += 32) {
+        const int t = tn;
+        const int32_t f = fn;
+        double v[9];
+#pragma unroll
+        for (int u = 0; u < 9; ++u) v[u] = vn[u];
+        tn = q0 + 32 + lane < q ? Q[q0 + 32 + lane] : -1;
+        fn = tn >= 0 ? FID[tn] : -1;
+        if (fn >= 0) {
+#pragma unroll
+          for (int u = 0; u < 9; ++u) vn[u] = __ldg(A.fv + 9 * (int64_t)fn + u);
+        }
+        if (t >= 0) {
+          const int pl = t / KS;
+          const V2 p{PXY[2 * pl], PXY[2 * pl + 1]};
+          const FaceGeom g = make_face_geom(v);
+          PixelFaceResult r;
+          eval_pixel_face<true, false>(p, g, A.blur, A.znear, A.persp, A.clip, r);
+          bool clamped;
+          double zi = blend_zinv_b(r.z, A.blend, clamped);
+          double c[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+          for (int qq = 0; qq < 3; ++qq) {  // interpolate_face_attributes (shading.cpp:21-29)
+            const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)f + qq];
+            c[0] += r.bary[qq] * __ldg(a);
+            c[1] += r.bary[qq] * __ldg(a + 1);
+            c[2] += r.bary[qq] * __ldg(a + 2);
+          }
+          C0[t] = c[0];
+          C1[t] = c[1];
+          C2[t] = c[2];
+          PR[t] = 1.0 / (1.0 + exp(r.dist / A.blend.sigma));  // sigmoid(-dists / sigma)
+          if (clamped) zi += 2.0;
+          ZI[t] = zi;
+        }
+      }
+    }
+    __syncwarp();
+    // C: per pixel (shading.cpp:185-228)
+    if (lane < np) {
+      const int r0 = lane * KS;
+      const double dimg[3] = {DIM[3 * lane], DIM[3 * lane + 1], DIM[3 * lane + 2]};
+      double zinv_max = -1.0;
+      int argmax = -1;
+      for (int s = 0; s < K; ++s) {
+        double zi = ZI[r0 + s];
+        if (zi < -0.5) continue;
+        if (zi > 1.5) zi -= 2.0;
+        if (argmax < 0) {
+          zinv_max = zi;
+          argmax = s;
+        }
+      }
+      double wsum = 0.0;
+      for (int s = 0; s < K; ++s) {
+        double zi = ZI[r0 + s];
+        if (zi < -0.5) continue;
+        if (zi > 1.5) zi -= 2.0;
+        const double w = PR[r0 + s] * exp((zi - zinv_max) / A.blend.gamma);
+        WT[r0 + s] = w;
+        wsum += w;
+      }
+      double mean_term = 0.0;
+      for (int s = 0; s < K; ++s) {
+        if (ZI[r0 + s] < -0.5) continue;
+        const double dc = dimg[0] * C0[r0 + s] + dimg[1] * C1[r0 + s] + dimg[2] * C2[r0 + s];
+        mean_term += dc * (WT[r0 + s] / wsum);
+      }
+      double d_zinv_max = 0.0;
+      for (int s = 0; s < K; ++s) {
+        if (ZI[r0 + s] < -0.5) continue;
+        const double w = WT[r0 + s];
+        const double d_what = dimg[0] * C0[r0 + s] + dimg[1] * C1[r0 + s] + dimg[2] * C2[r0 + s];
+        const double d_w = (d_what - mean_term) / wsum;
+        d_zinv_max += -d_w * w / A.blend.gamma;
+      }
+      for (int s = 0; s < K; ++s) {
+        const double zis = ZI[r0 + s];
+        if (zis < -0.5) continue;
+        const bool clamped = zis > 1.5;
+        const double w = WT[r0 + s], pr = PR[r0 + s];
+        const double what = w / wsum;
+        const double d_what = dimg[0] * C0[r0 + s] + dimg[1] * C1[r0 + s] + dimg[2] * C2[r0 + s];
+        const double d_w = (d_what - mean_term) / wsum;
+        const double d_prob = d_w * w / pr;
+        const double d_zinv = d_w * w / A.blend.gamma;
+        const double d_dists = d_prob * (-pr * (1.0 - pr) / A.blend.sigma);
+        double d_zbuf = clamped ? 0.0 : d_zinv * (-1.0 / zrange);
+        if (s == argmax && !clamped) d_zbuf += d_zinv_max * (-1.0 / zrange);
+        WT[r0 + s] = what;
+        PR[r0 + s] = d_dists;
+        ZI[r0 + s] = d_zbuf;
+      }
+    }
+    __syncwarp();
+    // D: per occupied slot
+    for (int q0 = 0; q0 < q; q0 += 32) {
+      const int t = q0 + lane < q ? Q[q0 + lane] : -1;
+      int32_t fid = -1;
+      double gg[18];
+#pragma unroll
+      for (int k = 0; k < 18; ++k) gg[k] = 0.0;
+      if (t >= 0) {
+        fid = FID[t];
+        const int pl = t / KS;
+        const V2 p{PXY[2 * pl], PXY[2 * pl + 1]};
+        const double what = WT[t];
+        const double d_col[3] = {DIM[3 * pl] * what, DIM[3 * pl + 1] * what, DIM[3 * pl + 2] * what};
+        SlotIn<double> in;
+#pragma unroll
+        for (int qq = 0; qq < 3; ++qq) {  // interpolate_face_attributes_backward (shading.cpp:46-72)
+          const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)fid + qq];
+          in.db[qq] = d_col[0] * __ldg(a) + d_col[1] * __ldg(a + 1) + d_col[2] * __ldg(a + 2);
+          in.w[qq] = 0.0;
+        }
+        in.dz = ZI[t];
+        in.dd = PR[t];
+#if DR_BWD_PREFETCH_FV
+#pragma unroll
+        for (int u = 0; u < 9; ++u) in.v[u] = __ldg(A.fv + 9 * (int64_t)fid + u);
+#endif
+        double g[9], wh[3];
+        slot_backward<double, true>(BA, p, fid, in, g, wh);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) gg[k] = g[k];
+#pragma unroll
+        for (int qq = 0; qq < 3; ++qq) {
+          gg[9 + 3 * qq + 0] = wh[qq] * d_col[0];
+          gg[9 + 3 * qq + 1] = wh[qq] * d_col[1];
+          gg[9 + 3 * qq + 2] = wh[qq] * d_col[2];
+        }
+      }
+      if (reduce_by_face<18>(fid, lane, gg)) {
+        double* out = A.grad + 9 * (int64_t)fid;
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+          if (gg[k] != 0.0) atomicAdd(out + k, gg[k]);
+#pragma unroll
+        for (int qq = 0; qq < 3; ++qq) {
+          double* oc = A.grad_colors + 3 * A.blend.faces[3 * (int64_t)fid + qq];
+          for (int d = 0; d < 3; ++d)
+            if (gg[9 + 3 * qq + d] != 0.0) atomicAdd(oc + d, gg[9 + 3 * qq + d]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+#ifndef DR_SOFT_Q
+#define DR_SOFT_Q 1
+#endif
 cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
   if (A.K > kSoftMaxK) return cudaErrorInvalidConfiguration;
+  // measured (C4 K=8 / C5 K=50): per-pixel kernel 10.9 / 39.1 ms, slot-compacted 15.1 / 16.1 ms — the
+  // compaction pays once a pixel's K slots are unevenly filled (large K)
+  if (DR_SOFT_Q && A.K > 16) {
+    const size_t smem = softq_warp_bytes(A.K);
+    cudaError_t e = cudaFuncSetAttribute(k_softmax_backward_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 48 * 1024));
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_softmax_backward_q, 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int P = softq_pixels(A.K);
+    const int64_t need = (A.npix + P - 1) / P;
+    if (blocks > need) blocks = need;
+    k_softmax_backward_q<<<(unsigned)blocks, 32, smem, st>>>(A);
+    return cudaGetLastError();
+  }
   const size_t per_warp = ((size_t)A.K * 32 * 6 + (size_t)A.K * 16) * sizeof(double);
   const int warps = (int)std::min<size_t>(kSoftThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));
   const size_t smem = per_warp * warps;
