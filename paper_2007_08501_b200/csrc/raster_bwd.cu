@@ -252,6 +252,9 @@ constexpr int kPixTab = 2048;  // pixel-centre tables in shared memory when H + 
 #ifndef DR_BWD_V2
 #define DR_BWD_V2 1
 #endif
+#ifndef DR_BWD_RANKMAJOR
+#define DR_BWD_RANKMAJOR 0  // measured slower (C4 2.48 -> 3.05 ms): longer reductions, scattered input loads
+#endif
 #ifndef DR_BWD_CHUNKS_PER_CTA
 #define DR_BWD_CHUNKS_PER_CTA 32
 #endif
@@ -348,15 +351,21 @@ __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdA
     cp_async_wait_all();
     __syncwarp();
     int n = 0;
+    // DR_BWD_RANKMAJOR (K divides the chunk): queue the chunk's slots rank-major — a step's lanes are neighbouring
+    // pixels at the same list rank, which mostly hold the same face, so reduce_by_face merges them before the atomics
+    const bool rank_major = DR_BWD_RANKMAJOR && kBwdChunk % A.K == 0;
+    const int ppc = kBwdChunk / A.K;  // pixels per chunk (rank-major)
 #pragma unroll 4
     for (int t = 0; t < kSteps; ++t) {
-      const int64_t slot = c0 + t * 32 + lane;
-      const int64_t f = slot < A.S ? stg[t * 32 + lane] : -1;
+      const int u = t * 32 + lane;
+      const int o = rank_major ? (u % ppc) * A.K + u / ppc : u;
+      const int64_t slot = c0 + o;
+      const int64_t f = slot < A.S ? stg[o] : -1;
       const bool occ = f >= 0 && f < A.F;
       const unsigned m = __ballot_sync(0xffffffffu, occ);
       if (occ) {
         const int pos = n + __popc(m & ((1u << lane) - 1u));
-        qo[pos] = (uint16_t)(t * 32 + lane);
+        qo[pos] = (uint16_t)o;
         qf[pos] = (int32_t)f;
       }
       n += __popc(m);
