@@ -1070,6 +1070,9 @@ __host__ __device__ __forceinline__ size_t softq_warp_bytes(int K) {
   return n * (6 * sizeof(double) + sizeof(int32_t) + sizeof(uint16_t)) + 32 * 5 * sizeof(double) + 16;
 }
 
+// kPhase: 0 = all phases in one kernel; 1 = A-C, the per-slot coefficients (what, d_dists, d_zbuf) go to
+// A.coef [S][3]; 2 = A + D reading them back (two smaller kernels: the one-kernel form is instruction-cache bound)
+template <int kPhase>
 __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
   extern __shared__ double softq_smem[];
   const int lane = threadIdx.x & 31;
@@ -1123,6 +1126,7 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
       q += __popc(m);
     }
     __syncwarp();
+    if constexpr (kPhase != 2) {
     // B: per occupied slot
     {
       double vn[9];
@@ -1227,6 +1231,32 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
       }
     }
     __syncwarp();
+    if constexpr (kPhase == 1) {  // park the coefficients of the occupied slots
+      for (int q0 = 0; q0 < q; q0 += 32) {
+        const int t = q0 + lane < q ? Q[q0 + lane] : -1;
+        if (t >= 0) {
+          double* c = A.coef + 3 * (base * K + t);
+          c[0] = WT[t];
+          c[1] = PR[t];
+          c[2] = ZI[t];
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    }  // kPhase != 2
+    if constexpr (kPhase == 2) {  // the coefficients from the first kernel
+      for (int q0 = 0; q0 < q; q0 += 32) {
+        const int t = q0 + lane < q ? Q[q0 + lane] : -1;
+        if (t >= 0) {
+          const double* c = A.coef + 3 * (base * K + t);
+          WT[t] = c[0];
+          PR[t] = c[1];
+          ZI[t] = c[2];
+        }
+      }
+      __syncwarp();
+    }
     // D: per occupied slot
     for (int q0 = 0; q0 < q; q0 += 32) {
       const int t = q0 + lane < q ? Q[q0 + lane] : -1;
@@ -1284,28 +1314,52 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
 #ifndef DR_SOFT_Q
 #define DR_SOFT_Q 1
 #endif
+#ifndef DR_SOFT_SPLIT
+#define DR_SOFT_SPLIT 0  // two-kernel form for K <= 16: measured 11.6 vs 10.9 ms per-pixel (C4)
+#endif
 cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
   if (A.K > kSoftMaxK) return cudaErrorInvalidConfiguration;
   // measured (C4 K=8 / C5 K=50): per-pixel kernel 10.9 / 39.1 ms, slot-compacted 15.1 / 16.1 ms — the
   // compaction pays once a pixel's K slots are unevenly filled (large K)
-  if (DR_SOFT_Q && A.K > 16) {
-    const size_t smem = softq_warp_bytes(A.K);
-    cudaError_t e = cudaFuncSetAttribute(k_softmax_backward_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto go_q = [&](auto kern, const SoftBwdArgs& args) -> cudaError_t {
+    const size_t smem = softq_warp_bytes(args.K);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_softmax_backward_q, 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = (int64_t)sms * per_sm;
-    const int P = softq_pixels(A.K);
-    const int64_t need = (A.npix + P - 1) / P;
+    const int P = softq_pixels(args.K);
+    const int64_t need = (args.npix + P - 1) / P;
     if (blocks > need) blocks = need;
-    k_softmax_backward_q<<<(unsigned)blocks, 32, smem, st>>>(A);
+    kern<<<(unsigned)blocks, 32, smem, st>>>(args);
     return cudaGetLastError();
+  };
+  if (DR_SOFT_Q && A.K > 16) return go_q(k_softmax_backward_q<0>, A);
+  if (DR_SOFT_SPLIT) {  // two kernels through a [S][3] fp64 coefficient scratch (stream-ordered allocation)
+    SoftBwdArgs B = A;
+    const size_t bytes = sizeof(double) * 3 * (size_t)A.npix * A.K;
+    {  // keep the scratch in the device's default pool between calls (the default threshold returns it to the
+       // driver at every synchronisation, and a multi-GB cudaMalloc per call costs more than the kernels)
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    }
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&B.coef), bytes, st);
+    if (e != cudaSuccess) return e;
+    e = go_q(k_softmax_backward_q<1>, B);
+    if (e == cudaSuccess) e = go_q(k_softmax_backward_q<2>, B);
+    cudaError_t e2 = cudaFreeAsync(B.coef, st);
+    return e != cudaSuccess ? e : e2;
   }
   const size_t per_warp = ((size_t)A.K * 32 * 6 + (size_t)A.K * 16) * sizeof(double);
   const int warps = (int)std::min<size_t>(kSoftThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));

@@ -140,6 +140,7 @@ struct SoftBwdArgs {
   bool persp, clip;
   double blur, znear;      // raster settings (exact re-evaluation of each slot)
   BlendArgs blend;
+  double* coef = nullptr;  // [S][3] per-slot (what, d_dists, d_zbuf) scratch of the two-kernel form
 };
 cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st);
 
