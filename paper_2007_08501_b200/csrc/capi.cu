@@ -335,6 +335,16 @@ int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   if (rc) return rc;
   if (!first || !num || !p2f || !bary || !dz || !db || !dd || (F > 0 && (!fv || !grad)))
     return fail(DR_ERR_USAGE, "null input/output pointer");
+  // the cotangents may live in page-locked HOST memory (read in place over PCIe through the unified address
+  // space: only occupied slots are touched, so a host caller skips copying the empty slots' cotangents);
+  // pageable host memory is rejected instead of faulting in the kernel
+  for (const void* ptr : {static_cast<const void*>(dz), static_cast<const void*>(db), static_cast<const void*>(dd)}) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess || at.type == cudaMemoryTypeUnregistered) {
+      cudaGetLastError();
+      return fail(DR_ERR_USAGE, "cotangent pointer is neither device nor page-locked host memory");
+    }
+  }
   int64_t mx;
   std::vector<int64_t> ranges;
   rc = read_ranges(first, num, N, F, st, &mx, &ranges, host_first, host_num);

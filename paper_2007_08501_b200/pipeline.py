@@ -54,7 +54,7 @@ class HostPipeline:
     """Streams forward (+ backward) of a fixed batch layout between pinned host buffers and the GPU."""
 
     def __init__(self, first, num, settings: RasterSettings, num_faces: int, device, n_groups: int = 8,
-                 backward: bool = True, ramp: int = 2, lookahead: int = 3):
+                 backward: bool = True, ramp: int = 2, lookahead: int = 3, zero_copy: bool = False):
         self.first = np.asarray(first, dtype=np.int64)
         self.num = np.asarray(num, dtype=np.int64)
         order = np.argsort(self.first, kind="stable")
@@ -66,6 +66,9 @@ class HostPipeline:
         self.dev = torch.device(device)
         self.backward = backward
         self.lookahead = int(lookahead)  # 0: every H2D enqueued at once
+        # zero_copy: the backward reads the (page-locked) host cotangents in place, only at occupied slots,
+        # instead of an H2D copy of every slot's cotangents
+        self.zero_copy = bool(zero_copy)
         H, W = settings.hw
         K = settings.faces_per_pixel
         # groups balance PCIe bytes (the e2e bound), not faces: a mesh's slots cost as much as ~0.5M faces
@@ -77,9 +80,10 @@ class HostPipeline:
         self.bary = torch.empty((self.N, H, W, K, 3), dtype=torch.float32, device=d)
         self.dists = torch.empty((self.N, H, W, K), dtype=torch.float32, device=d)
         if backward:
-            self.dz = torch.empty_like(self.zbuf)
-            self.db = torch.empty_like(self.bary)
-            self.dd = torch.empty_like(self.dists)
+            if not zero_copy:
+                self.dz = torch.empty_like(self.zbuf)
+                self.db = torch.empty_like(self.bary)
+                self.dd = torch.empty_like(self.dists)
             self.grad = torch.zeros((self.F, 3, 3), dtype=torch.float64, device=d)
         ws = max(workspace_bytes(g1 - g0, self.F, settings) for g0, g1 in self.groups)
         self.ws = torch.empty(ws, dtype=torch.uint8, device=d)
@@ -111,7 +115,7 @@ class HostPipeline:
                 self.h2d.wait_event(ev_d2h[gi - self.lookahead])
             with torch.cuda.stream(self.h2d):
                 self.fv[lo:hi].copy_(fv_h[lo:hi], non_blocking=True)
-                if self.backward:
+                if self.backward and not self.zero_copy:
                     for d, h in zip((self.dz, self.db, self.dd), cot_h):
                         d[g0:g1].copy_(h[g0:g1], non_blocking=True)
                 ev_in = torch.cuda.Event()
@@ -124,9 +128,10 @@ class HostPipeline:
                 ev_fwd = torch.cuda.Event()
                 ev_fwd.record(self.comp)
                 if self.backward:
+                    cz, cb, cd = ((c[g0:g1] for c in cot_h) if self.zero_copy
+                                  else (self.dz[g0:g1], self.db[g0:g1], self.dd[g0:g1]))
                     rasterize_meshes_backward(self.fv, self.g_first[gi], self.g_num[gi], self.s, outs[0], outs[2],
-                                              self.dz[g0:g1], self.db[g0:g1], self.dd[g0:g1], out=self.grad,
-                                              host_ranges=self.g_host[gi])
+                                              cz, cb, cd, out=self.grad, host_ranges=self.g_host[gi])
                 ev_out = torch.cuda.Event()
                 ev_out.record(self.comp)
             self.d2h.wait_event(ev_fwd)
