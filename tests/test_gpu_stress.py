@@ -42,8 +42,11 @@ def _tie_scene(seed: int) -> S.Meshes:
     return m
 
 
+# DR_STRESS_SEEDS widens the sweep for a long soak run (default 36 keeps the suite to seconds)
+import os  # noqa: E402
+
 CASES = []
-for seed in range(36):
+for seed in range(int(os.environ.get("DR_STRESS_SEEDS", "36"))):
     persp = seed % 3 != 2
     CASES.append((seed, persp, [1, 3, 8, 17, 64][seed % 5], [0.0, 1e-4, 3e-3][seed % 3],
                   bool(seed & 1), bool(seed & 2), bool(seed & 4), [8, 16, 0, 32][seed % 4]))
