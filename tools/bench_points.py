@@ -77,6 +77,17 @@ def main():
                                     "threads": ref.num_threads()}
     except Exception as e:  # noqa: BLE001
         out["cpu_reference_fwd"] = {"unavailable": str(e)}
+    from paper_2007_08501_b200 import KernelTimer
+
+    torch.cuda.synchronize()
+    with KernelTimer() as kt:
+        for _ in range(5):
+            step()
+        torch.cuda.synchronize()
+    per = {}
+    for k, t in kt.records:
+        per[k] = round(per.get(k, 0.0) + t / 5, 4)
+    out["kernels_ms"] = per
     print(json.dumps(out))
 
 
