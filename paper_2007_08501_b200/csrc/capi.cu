@@ -305,6 +305,11 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
     }
   }
   if (nw == 0) return fail(DR_ERR_RANGE, "faces_per_pixel=%d too large for the shared-memory top-K", p.K);
+  static const int nw_env = [] {  // DR_FINE_NW=2|8: force the CTA size (A/B of the occupancy choice)
+    const char* e = std::getenv("DR_FINE_NW");
+    return e ? std::atoi(e) : 0;
+  }();
+  if ((nw_env == 2 || nw_env == 8) && (size_t)nw_env * per_warp <= 227 * 1024) nw = nw_env;
   A.N = (int)N;
   A.work_counter = reinterpret_cast<unsigned long long*>(base + p.off_counter);
   A.p2f = p2f;
