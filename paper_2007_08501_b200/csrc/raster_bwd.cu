@@ -209,7 +209,10 @@ __device__ __forceinline__ bool reduce_by_face(int32_t fid, int lane, double g[N
 // Persistent warps walk the slots in chunks of kChunk consecutive slots. Occupied slots (pix_to_face >= 0;
 // typically 40-70 % of them) are compacted with ballot + popc into a warp-private queue and processed 32 at
 // a time, so every lane of a batch does a full per-slot backward.
-constexpr int kBwdChunk = 32 * 16;
+#ifndef DR_BWD_CHUNK_STEPS
+#define DR_BWD_CHUNK_STEPS 16
+#endif
+constexpr int kBwdChunk = 32 * DR_BWD_CHUNK_STEPS;
 
 #ifndef DR_BWD_THREADS
 #define DR_BWD_THREADS 128
