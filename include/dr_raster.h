@@ -169,6 +169,12 @@ int dr_packed_to_padded(const void* packed, const int64_t* first, const int64_t*
 /* packed[first[b] + j, :] = padded[b, j, :] for j < num[b]. */
 int dr_padded_to_packed(const void* padded, const int64_t* first, const int64_t* num, int64_t N, int64_t max_count,
                         int64_t row_bytes, void* packed, dr_stream_t stream);
+/* Host pipeline helper: copy the backward's cotangents (fp32; grad_bary [S,3]) from page-locked host (or
+ * device) arrays to device arrays at the occupied slots only (pix_to_face >= 0) — the slots
+ * dr_rasterize_meshes_bwd reads; the other destination slots are left untouched. */
+int dr_gather_occupied_cotangents(const int64_t* pix_to_face, int64_t S, const float* grad_zbuf_src,
+                                  const float* grad_bary_src, const float* grad_dists_src, float* grad_zbuf,
+                                  float* grad_bary, float* grad_dists, dr_stream_t stream);
 /* out[i] = the batch element owning packed row i (PackedView::item_to_element), -1 for rows in no range. */
 int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
                               dr_stream_t stream);

@@ -972,6 +972,27 @@ int dr_padded_to_packed(const void* padded, const int64_t* first, const int64_t*
   return e == cudaSuccess ? DR_OK : cuda_fail(e, "padded_to_packed");
 }
 
+int dr_gather_occupied_cotangents(const int64_t* pix_to_face, int64_t S, const float* grad_zbuf_src,
+                                  const float* grad_bary_src, const float* grad_dists_src, float* grad_zbuf,
+                                  float* grad_bary, float* grad_dists, dr_stream_t stream) {
+  if (S < 0) return fail(DR_ERR_SHAPE, "negative slot count");
+  if (S == 0) return DR_OK;
+  if (!pix_to_face || !grad_zbuf_src || !grad_bary_src || !grad_dists_src || !grad_zbuf || !grad_bary || !grad_dists)
+    return fail(DR_ERR_USAGE, "null pointer");
+  for (const void* ptr : {static_cast<const void*>(grad_zbuf_src), static_cast<const void*>(grad_bary_src),
+                          static_cast<const void*>(grad_dists_src)}) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess || at.type == cudaMemoryTypeUnregistered) {
+      cudaGetLastError();
+      return fail(DR_ERR_USAGE, "source pointer is neither device nor page-locked host memory");
+    }
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = drb::launch_gather_occupied(pix_to_face, S, grad_zbuf_src, grad_bary_src, grad_dists_src, grad_zbuf,
+                                              grad_bary, grad_dists, st);
+  return e == cudaSuccess ? DR_OK : cuda_fail(e, "gather_occupied_cotangents");
+}
+
 int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
                               dr_stream_t stream) {
   if (N < 0 || total < 0) return fail(DR_ERR_SHAPE, "item_to_element: bad sizes");

@@ -172,6 +172,8 @@ cudaError_t launch_packed_to_padded(const void* packed, const int64_t* first, co
                                     cudaStream_t st);
 cudaError_t launch_padded_to_packed(const void* padded, const int64_t* first, const int64_t* num, int64_t N,
                                     int64_t max_count, int64_t row_bytes, void* packed, cudaStream_t st);
+cudaError_t launch_gather_occupied(const int64_t* p2f, int64_t S, const float* dz_src, const float* db_src,
+                                   const float* dd_src, float* dz, float* db, float* dd, cudaStream_t st);
 cudaError_t launch_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
                                    cudaStream_t st);
 

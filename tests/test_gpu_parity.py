@@ -378,8 +378,8 @@ def test_div_free_paths_and_rerun_backward_tolerance(cuda, oracle):
     assert rel_err(got, want) < 1e-12
 
 
-@pytest.mark.parametrize("zero_copy", [False, True])
-def test_host_pipeline_matches_device_calls(cuda, zero_copy):
+@pytest.mark.parametrize("zero_copy,gather", [(False, False), (True, False), (False, True)])
+def test_host_pipeline_matches_device_calls(cuda, zero_copy, gather):
     """HostPipeline (pinned host in/out, mesh groups streamed over 3 CUDA streams) == plain device calls; with
     zero_copy the backward reads the pinned host cotangents in place."""
     from paper_2007_08501_b200 import rasterize_meshes, rasterize_meshes_backward
@@ -392,7 +392,7 @@ def test_host_pipeline_matches_device_calls(cuda, zero_copy):
     g = np.random.default_rng(3)
     cot = [torch.as_tensor(g.standard_normal(s), dtype=torch.float32) for s in
            ((N, 128, 128, 8), (N, 128, 128, 8, 3), (N, 128, 128, 8))]
-    pipe = HostPipeline(first, num, rs, F, cuda, n_groups=3, zero_copy=zero_copy)
+    pipe = HostPipeline(first, num, rs, F, cuda, n_groups=3, zero_copy=zero_copy, gather=gather)
     out_h = (torch.empty((N, 128, 128, 8), dtype=torch.int64).pin_memory(),
              torch.empty((N, 128, 128, 8), dtype=torch.float32).pin_memory(),
              torch.empty((N, 128, 128, 8, 3), dtype=torch.float32).pin_memory(),
