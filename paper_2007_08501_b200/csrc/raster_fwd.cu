@@ -453,6 +453,9 @@ constexpr int kPairQ = 64;  // < 32 pending + one enumeration step of 32
 #ifndef DR_EARLY_EXIT
 #define DR_EARLY_EXIT 0  // measured: the per-chunk exit test costs more than the chunks it skips
 #endif
+#if DR_EARLY_EXIT && DR_SORT_BUCKET
+#error "the sorted-list early exit needs an exact key order: build with -DDR_SORT_BUCKET=0 (bitonic bins)"
+#endif
 #ifndef DR_EMIT_T
 #define DR_EMIT_T 1  // fragment emit with lanes over (pixel, slot) pairs: coalesced payload stores
 #endif
