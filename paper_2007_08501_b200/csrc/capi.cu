@@ -533,7 +533,9 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   const bool sorted = p.binned && zsort_enabled();
   if (sorted) {
     ProfScope ps(st, KN_SORT);
-    e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, 0, st);
+    // exact (bitonic) order: the point fine stage stops streaming a bin at the first key above every pixel's
+    // K-th depth, which the mesh path's bucket order would not guarantee
+    e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, 0, st, true);
     if (e != cudaSuccess) return cuda_fail(e, "sorting point bins");
   }
   drb::PointFineArgs<OutT> A;

@@ -288,7 +288,7 @@ constexpr int kSortBpt = DR_SORT_BPT;                    // bucket counts per th
 constexpr int kSortBuckets = kSortThreads * kSortBpt;
 
 // MAXN = shared-memory capacity in entries; bins with (MINN, MAXN] entries are sorted by this instantiation
-template <int MAXN, int MINN, bool kDyn>
+template <int MAXN, int MINN, bool kDyn, bool kBucket>
 __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restrict__ counts,
                                                             const int64_t* __restrict__ off,
                                                             int4* __restrict__ entries,
@@ -296,8 +296,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
                                                             int64_t pool, int cap) {
   __shared__ unsigned long long s_static[kDyn ? 1 : MAXN];
   __shared__ unsigned sel_mask;
-#if DR_SORT_BUCKET
-  __shared__ unsigned hist[kSortBuckets];
+#if 1
+  __shared__ unsigned hist[kBucket ? kSortBuckets : 1];
   __shared__ unsigned wsum[kSortThreads / 32];
   __shared__ float red_lo[kSortThreads / 32], red_hi[kSortThreads / 32];
 #endif
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
     const int c = counts[bin];
     const int64_t o = off[bin];
     int4* L = entries + o;
-#if DR_SORT_BUCKET
+    if constexpr (kBucket) {
     // depth-bucket order: keys in smem, bin depth range, 256 linear buckets (histogram, scan, scatter). Order
     // inside a bucket is arbitrary (K2 is order-independent); one pass of O(c) instead of O(c log^2 c).
     float lo = __int_as_float(0x7f800000), hi = -lo;
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
       const int32_t f = (int32_t)(uint32_t)e;
       L[pos] = make_bin_entry(f, __uint_as_float((uint32_t)(e >> 32)), __ldg(ibbox + f));
     }
-#else
+    } else {
     int P = 1;
     while (P < c) P <<= 1;
     for (int i = threadIdx.x; i < P; i += kSortThreads) {
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
       const int32_t f = (int32_t)(uint32_t)e;
       L[i] = make_bin_entry(f, float_from_order_bits((uint32_t)(e >> 32)), __ldg(ibbox + f));
     }
-#endif
+    }
     __syncthreads();
   }
   }
@@ -1220,12 +1220,17 @@ void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* nu
 }
 
 cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entries, const int4* ibbox,
-                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st) {
+                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st, bool exact) {
   if (nbins_total <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nbins_total, 148 * 16);
-  k_sort_bins<kSortMax, 0, false><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total, pool,
-                                                                  cap);
-  auto big = k_sort_bins<kSortMaxBig, kSortMax, true>;
+  const bool bucket = DR_SORT_BUCKET && !exact;
+  if (bucket)
+    k_sort_bins<kSortMax, 0, false, true><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total,
+                                                                        pool, cap);
+  else
+    k_sort_bins<kSortMax, 0, false, false><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total,
+                                                                         pool, cap);
+  auto big = bucket ? k_sort_bins<kSortMaxBig, kSortMax, true, true> : k_sort_bins<kSortMaxBig, kSortMax, true, false>;
   const int smem = kSortMaxBig * (int)sizeof(unsigned long long);
   cudaError_t e = cudaFuncSetAttribute(big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

@@ -192,7 +192,8 @@ void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* nu
                       int bs, int nbx, int nby, const int* counts, const int64_t* off, int* cursor, int64_t pool,
                       const float* zkey, int4* entries, cudaStream_t st);
 cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entries, const int4* ibbox,
-                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st);
+                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st,
+                             bool exact = false);
 cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st);

@@ -100,6 +100,31 @@ def test_points_large_k_and_dense_cloud(oracle, cuda):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("K", [1, 4])
+def test_points_early_exit_needs_exact_bin_order(oracle, cuda, K):
+    """Bins of thousands of points whose depths all fall in a sliver (one depth bucket): the point fine stage stops
+    streaming a bin at the first key above every pixel's K-th depth, which is only valid on an exactly ordered bin
+    (a bucket order leaves nearer points after the first key of a chunk)."""
+    from paper_2007_08501_b200 import rasterize_points
+
+    rng = np.random.default_rng(11)
+    n = 6000  # a layer covering the whole image (ndc x = 2x/3 at depth 3): every pixel fills its K slots early
+    pts = np.stack([rng.uniform(-1.8, 1.8, n), rng.uniform(-1.8, 1.8, n), rng.uniform(0.0, 5e-3, n)], 1)
+    # far outliers stretch every bin's key range, so the whole dense layer lands in one of 1024 depth buckets
+    far = np.stack([rng.uniform(-1.5, 1.5, 64), rng.uniform(-1.5, 1.5, 64), np.full(64, 5.0)], 1)
+    pts = np.concatenate([pts, far])
+    n = len(pts)
+    cam = S.bench_camera()
+    ndc = S.points_ndc(pts, cam)
+    first, num = np.array([0]), np.array([n])
+    want = oracle.rasterize_points(ndc, first, num, 32, 32, K, 0.2, tile=16, znear=cam.znear)
+    got = rasterize_points(torch.as_tensor(ndc, device=cuda), first, num, _settings(32, K, 0.2, 16, cam),
+                           out_dtype=torch.float64)
+    for g, w in zip(got, want):
+        assert np.array_equal(g.cpu().numpy(), w)
+
+
+@pytest.mark.gpu
 def test_points_backward_vs_reference(reflib, oracle, cuda):
     """splat_opacity -> d_alpha -> splat_position_backward (world space) vs the GPU chain."""
     from paper_2007_08501_b200 import rasterize_points, rasterize_points_backward, splat_position_backward, \
