@@ -429,6 +429,14 @@ int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int
   return DR_OK;
 }
 
+bool point_exact_sort() {
+  static const bool v = [] {
+    const char* e = std::getenv("DR_POINT_EXACT_SORT");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 // ---- point rasterizer (point_render.cpp:105-155) ----
 struct PointPlan {
   int64_t N = 0, P = 0;
@@ -436,7 +444,7 @@ struct PointPlan {
   bool binned = false;
   int64_t nbins_total = 0, pool = 0;
   size_t off_ibbox = 0, off_zkey = 0, off_bounds = 0, off_counts = 0, off_cursor = 0, off_binoff = 0, off_lists = 0,
-         total = 0;
+         off_brange = 0, total = 0;
 };
 
 int make_point_plan(int64_t N, int64_t P, const dr_point_raster_settings* s, PointPlan& p) {
@@ -478,6 +486,8 @@ int make_point_plan(int64_t N, int64_t P, const dr_point_raster_settings* s, Poi
     off = align_up(off + sizeof(int64_t) * (size_t)p.nbins_total);
     p.off_lists = off;
     off = align_up(off + sizeof(int4) * (size_t)p.pool);
+    p.off_brange = off;
+    off = align_up(off + sizeof(float2) * (size_t)p.nbins_total);
   }
   p.total = off;
   return DR_OK;
@@ -511,6 +521,7 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   int* cursor = reinterpret_cast<int*>(base + p.off_cursor);
   int64_t* bin_off = reinterpret_cast<int64_t*>(base + p.off_binoff);
   int4* entries = reinterpret_cast<int4*>(base + p.off_lists);
+  float2* brange = reinterpret_cast<float2*>(base + p.off_brange);
   cudaError_t e;
   {
     ProfScope ps(st, KN_PT_SETUP);
@@ -533,9 +544,12 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   const bool sorted = p.binned && zsort_enabled();
   if (sorted) {
     ProfScope ps(st, KN_SORT);
-    // exact (bitonic) order: the point fine stage stops streaming a bin at the first key above every pixel's
-    // K-th depth, which the mesh path's bucket order would not guarantee
-    e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, 0, st, true);
+    // the point fine stage stops streaming a bin once a lower bound of its remaining keys exceeds every pixel's
+    // K-th depth: with the bucket order that bound comes from the bin's bucket map (brange), with the exact
+    // bitonic order (DR_POINT_EXACT_SORT=1) from the next key itself
+    e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, 0, st, point_exact_sort(),
+                              point_exact_sort() ? nullptr : brange);
+    // (bin_range is only written when the sort really ran in bucket mode)
     if (e != cudaSuccess) return cuda_fail(e, "sorting point bins");
   }
   drb::PointFineArgs<OutT> A;
@@ -552,6 +566,7 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   A.nbx = p.nbx;
   A.nby = p.nby;
   A.sorted = sorted ? 1 : 0;
+  A.brange = sorted && drb::sort_uses_buckets(point_exact_sort()) ? brange : nullptr;
   A.sub_x = (p.bs + 15) / 16;
   A.sub_y = (p.bs + 15) / 16;
   A.H = p.H;

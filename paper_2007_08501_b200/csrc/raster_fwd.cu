@@ -281,11 +281,9 @@ constexpr int kSortThreads = 256;
 #ifndef DR_SORT_BUCKET
 #define DR_SORT_BUCKET 1
 #endif
-#ifndef DR_SORT_BPT
-#define DR_SORT_BPT 4
-#endif
 constexpr int kSortBpt = DR_SORT_BPT;                    // bucket counts per thread in the scan
 constexpr int kSortBuckets = kSortThreads * kSortBpt;
+static_assert(kSortBuckets == kSortBucketsH, "bucket count shared with the point fine stage");
 
 // MAXN = shared-memory capacity in entries; bins with (MINN, MAXN] entries are sorted by this instantiation
 template <int MAXN, int MINN, bool kDyn, bool kBucket>
@@ -293,7 +291,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
                                                             const int64_t* __restrict__ off,
                                                             int4* __restrict__ entries,
                                                             const int4* __restrict__ ibbox, int64_t nbins_total,
-                                                            int64_t pool, int cap) {
+                                                            int64_t pool, int cap, float2* __restrict__ brange) {
   __shared__ unsigned long long s_static[kDyn ? 1 : MAXN];
   __shared__ unsigned sel_mask;
 #if 1
@@ -350,11 +348,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
     lo = red_lo[0]; hi = red_hi[0];
 #pragma unroll
     for (int w = 1; w < kSortThreads / 32; ++w) { lo = fminf(lo, red_lo[w]); hi = fmaxf(hi, red_hi[w]); }
-    const float scale = hi > lo ? (float)kSortBuckets * 0.99999f / (hi - lo) : 0.f;
-    auto bucket = [&](unsigned long long e) {
-      const float t = (__uint_as_float((uint32_t)(e >> 32)) - lo) * scale;  // NaN/inf range -> bucket 0
-      return min(kSortBuckets - 1, max(0, __float2int_rz(t)));
-    };
+    const float scale = sort_bucket_scale(lo, hi);
+    if (brange && threadIdx.x == 0) brange[bin] = make_float2(lo, scale);  // the bucket map, for an exit bound
+    auto bucket = [&](unsigned long long e) { return sort_bucket(__uint_as_float((uint32_t)(e >> 32)), lo, scale); };
     for (int i = threadIdx.x; i < c; i += kSortThreads) atomicAdd(&hist[bucket(s[i])], 1u);
     __syncthreads();
     {  // exclusive scan of the bucket counts (kSortBpt consecutive ones per thread)
@@ -1219,23 +1215,27 @@ void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* nu
                                                           const_cast<int*>(counts), off, cursor, pool, zkey, entries);
 }
 
+bool sort_uses_buckets(bool exact) { return DR_SORT_BUCKET && !exact; }
+
 cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entries, const int4* ibbox,
-                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st, bool exact) {
+                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st, bool exact,
+                             float2* bin_range) {
   if (nbins_total <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nbins_total, 148 * 16);
   const bool bucket = DR_SORT_BUCKET && !exact;
   if (bucket)
     k_sort_bins<kSortMax, 0, false, true><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total,
-                                                                        pool, cap);
+                                                                        pool, cap, bin_range);
   else
     k_sort_bins<kSortMax, 0, false, false><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total,
-                                                                         pool, cap);
+                                                                         pool, cap, nullptr);
   auto big = bucket ? k_sort_bins<kSortMaxBig, kSortMax, true, true> : k_sort_bins<kSortMaxBig, kSortMax, true, false>;
   const int smem = kSortMaxBig * (int)sizeof(unsigned long long);
   cudaError_t e = cudaFuncSetAttribute(big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   big<<<(unsigned)std::min<int64_t>(nbins_total, 148), kSortThreads, smem, st>>>(counts, off, entries, ibbox,
-                                                                                  nbins_total, pool, cap);
+                                                                                  nbins_total, pool, cap,
+                                                                                  bucket ? bin_range : nullptr);
   return cudaGetLastError();
 }
 

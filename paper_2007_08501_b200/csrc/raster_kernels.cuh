@@ -108,7 +108,8 @@ struct PointFineArgs {  // rasterize_points (point_render.cpp:105-155)
   const int4* bin_entries;
   int64_t pool;
   int binned, bs, nbx, nby, sub_x, sub_y;  // sub_x/sub_y: 16x16 blocks per bin row / column
-  int sorted;                              // bins sorted ascending by depth key (early exit)
+  int sorted;                              // bins depth-ordered (early exit)
+  const float2* brange = nullptr;          // bucket-ordered bins: per-bin (lo, scale) of the bucket map
   int H, W, K;
   double r2;
   int N;
@@ -191,9 +192,23 @@ void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cuda
 void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
                       int bs, int nbx, int nby, const int* counts, const int64_t* off, int* cursor, int64_t pool,
                       const float* zkey, int4* entries, cudaStream_t st);
+// Depth-bucket order of a bin (k_sort_bins, bucket mode): keys [lo, hi] map linearly onto kSortBucketsH buckets.
+// Shared with the point fine stage, which bounds the keys of the rest of a bin from the bucket of its next entry.
+#ifndef DR_SORT_BPT
+#define DR_SORT_BPT 4
+#endif
+constexpr int kSortBucketsH = 256 * DR_SORT_BPT;
+__device__ __forceinline__ float sort_bucket_scale(float lo, float hi) {
+  return hi > lo ? (float)kSortBucketsH * 0.99999f / (hi - lo) : 0.f;
+}
+__device__ __forceinline__ int sort_bucket(float key, float lo, float scale) {
+  return min(kSortBucketsH - 1, max(0, __float2int_rz((key - lo) * scale)));  // NaN/inf range -> bucket 0
+}
+
+bool sort_uses_buckets(bool exact);
 cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entries, const int4* ibbox,
                              int64_t nbins_total, int64_t pool, int cap, cudaStream_t st,
-                             bool exact = false);
+                             bool exact = false, float2* bin_range = nullptr);
 cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st);

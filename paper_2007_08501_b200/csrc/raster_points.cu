@@ -162,8 +162,10 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
       }
     }
     for (int64_t c0 = 0; c0 < nsrc; c0 += kPtThreads) {
-      // depth-ordered bin: once every pixel of the block holds K points nearer than the next point's depth key,
-      // no later point can enter any list (strict (z, id) order, PR:37)
+      // depth-ordered bin: once every pixel of the block holds K points nearer than a lower bound of every
+      // remaining depth key, no later point can enter any list (strict (z, id) order, PR:37). Exact order: the
+      // next key itself; bucket order: the lower edge of the bucket two below the next entry's (rounding in the
+      // float bucket map stays under one bucket width)
       if (sorted) {
         double kth = -__longlong_as_double(0x7ff0000000000000LL);
         if (valid) {
@@ -176,7 +178,15 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
         __syncthreads();
         double T = s_kth[0];
         for (int w = 1; w < kPtThreads / 32; ++w) T = fmax(T, s_kth[w]);
-        if ((double)__int_as_float(list[c0].y) > T) break;
+        const float key = __int_as_float(list[c0].y);
+        double bound = (double)key;
+        if (A.brange) {  // the sort's bucket map (lo, scale) of this bin, loaded here: nothing stays live
+          const float2 br = A.brange[(int64_t)b * nbins + bin];
+          const int bk = sort_bucket(key, br.x, br.y);
+          // lo + (bk - 2) / scale with both roundings downward: a lower bound of every key in buckets >= bk
+          bound = br.y > 0.f && bk >= 2 ? (double)__fadd_rd(br.x, __fdiv_rd((float)(bk - 2), br.y)) : (double)br.x;
+        }
+        if (bound > T) break;
       }
       __syncthreads();
       const int64_t ci = c0 + threadIdx.x;
