@@ -54,6 +54,12 @@ def parse():
     ap.add_argument("--e2e-ramp", type=int, default=2, help="smaller first/last pipeline groups (HostPipeline ramp)")
     ap.add_argument("--cpu-sample-faces", type=float, default=0.25,
                     help="fraction of the batch's faces the CPU sample covers")
+    ap.add_argument("--cpu-runs", type=int, default=3, help="CPU baseline runs (median reported)")
+    ap.add_argument("--cpu-sample-faces-1t", type=float, default=0.03,
+                    help="fraction of the batch's faces the 1-thread CPU figure covers")
+    ap.add_argument("--like-for-like", type=int, default=1,
+                    help="1: also time the GPU at reference semantics (flags off) on the whole batch and on the "
+                         "CPU sample")
     return ap.parse_args()
 
 
@@ -185,13 +191,14 @@ def ncu_traffic(cfg, kernel):
 # CPU arms
 
 
-def cpu_reference_run(meshes: S.Meshes, cfg, steps=1, warmup=0):
-    """Reference CPU path (oracle/_ref) fwd+bwd on `meshes`; falls back to the oracle port."""
+def cpu_reference_run(meshes: S.Meshes, cfg, steps=1, warmup=0, threads=None):
+    """Reference CPU path (oracle/_ref) fwd+bwd on `meshes` with `threads` host threads (default: all); falls back
+    to the oracle port (one thread). Returns (Mfaces·px/s of the median step, median s, kind, threads, all s)."""
     c = S.CONFIGS[cfg]
     H = W = c["image"]
     K, blur = c["K"], c["blur"]
     cam = S.bench_camera()
-    ncores = os.cpu_count() or 1
+    ncores = threads or os.cpu_count() or 1
     try:
         from oracle.oracle import RefLib
 
@@ -233,7 +240,7 @@ def cpu_reference_run(meshes: S.Meshes, cfg, steps=1, warmup=0):
         step()
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
-    return face_px(meshes, H, W) / t / 1e6, t, kind, ncores
+    return face_px(meshes, H, W) / t / 1e6, t, kind, ncores, times
 
 
 def cpu_sample(meshes: S.Meshes, frac: float):
@@ -246,6 +253,98 @@ def cpu_sample(meshes: S.Meshes, frac: float):
         if acc >= target:
             break
     return idx
+
+
+def like_for_like_leg(args, cfg, meshes_all, cam, dev):
+    """The GPU at the reference's own semantics (perspective_correct and cull_backfaces off: the reference has
+    neither, mesh_raster.cpp:234-285), on the whole batch and on exactly the CPU arm's mesh sample, device-resident
+    and end to end through HostPipeline — the like-for-like numbers beside the flagged headline."""
+    import torch
+
+    from paper_2007_08501_b200 import rasterize_meshes, rasterize_meshes_backward, workspace_bytes
+    from paper_2007_08501_b200.pipeline import HostPipeline
+
+    c = S.CONFIGS[cfg]
+    H = W = c["image"]
+    K = c["K"]
+    rs = config_settings(cfg)
+    rs.perspective_correct = False
+    rs.cull_backfaces = False
+    st = torch.cuda.current_stream()
+
+    def device_rate(meshes, steps):
+        fv_np = S.face_verts(meshes, cam)
+        first_np, num_np = meshes.mesh_to_face_first_idx(), meshes.num_faces_per_mesh()
+        N, F = len(num_np), len(fv_np)
+        fv, first, num = (torch.as_tensor(x, device=dev) for x in (fv_np, first_np, num_np))
+        ws = torch.empty(workspace_bytes(N, F, rs), dtype=torch.uint8, device=dev)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(99)
+        dz = torch.randn((N, H, W, K), generator=gen, device=dev)
+        db = torch.randn((N, H, W, K, 3), generator=gen, device=dev)
+        dd = torch.randn((N, H, W, K), generator=gen, device=dev)
+        hr = (first_np, num_np)
+
+        def step():
+            p2f, _, bary, _ = rasterize_meshes(fv, first, num, rs, workspace=ws, host_ranges=hr)
+            if c["backward"]:
+                rasterize_meshes_backward(fv, first, num, rs, p2f, bary, dz, db, dd, host_ranges=hr)
+
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        del ws, dz, db, dd, fv
+        torch.cuda.empty_cache()
+        return face_px(meshes, H, W) / (ms * 1e-3) / 1e6, ms
+
+    def e2e_rate(meshes, steps):
+        fv_np = S.face_verts(meshes, cam)
+        first_np, num_np = meshes.mesh_to_face_first_idx(), meshes.num_faces_per_mesh()
+        N, F = len(num_np), len(fv_np)
+        g = np.random.default_rng(5)
+        pipe = HostPipeline(first_np, num_np, rs, F, dev, n_groups=min(args.e2e_groups, N), backward=c["backward"],
+                            ramp=args.e2e_ramp, lookahead=args.e2e_lookahead)
+        h_fv = torch.from_numpy(fv_np).pin_memory()
+        cot = tuple(torch.from_numpy(g.standard_normal(s).astype(np.float32)).pin_memory()
+                    for s in ((N, H, W, K), (N, H, W, K, 3), (N, H, W, K))) if c["backward"] else None
+        out_h = (torch.empty((N, H, W, K), dtype=torch.int64).pin_memory(),
+                 torch.empty((N, H, W, K), dtype=torch.float32).pin_memory(),
+                 torch.empty((N, H, W, K, 3), dtype=torch.float32).pin_memory(),
+                 torch.empty((N, H, W, K), dtype=torch.float32).pin_memory())
+        grad_h = torch.empty((F, 3, 3), dtype=torch.float64).pin_memory() if c["backward"] else None
+        pipe.run(h_fv, out_h, cot, grad_h)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            pipe.run(h_fv, out_h, cot, grad_h)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        del pipe
+        torch.cuda.empty_cache()
+        return face_px(meshes, H, W) / (ms * 1e-3) / 1e6, ms
+
+    full_v, full_ms = device_rate(meshes_all, 5)
+    idx = cpu_sample(meshes_all, args.cpu_sample_faces)
+    sample = subset(meshes_all, idx)
+    s_v, s_ms = device_rate(sample, 5)
+    out = {"semantics": "reference (perspective_correct=0, cull_backfaces=0)",
+           "full": {"meshes": len(meshes_all.verts), "gpu_value": full_v, "gpu_ms_per_step": full_ms},
+           "sample": {"meshes": f"0..{len(idx) - 1}", "faces": int(sample.num_faces_per_mesh().sum()),
+                      "gpu_value": s_v, "gpu_ms_per_step": s_ms}}
+    if not args.no_e2e:
+        e_v, e_ms = e2e_rate(sample, 3)
+        out["sample"]["gpu_e2e"] = e_v
+        out["sample"]["gpu_e2e_ms_per_step"] = e_ms
+    return out
 
 
 # -------------------------------------------------------------------------------------------------
@@ -267,7 +366,7 @@ def main():
             return
         idx = cpu_sample(meshes_all, args.cpu_sample_faces)
         sample = subset(meshes_all, idx)
-        v, t, kind, cores = cpu_reference_run(sample, cfg, steps=max(1, min(args.steps, 3)), warmup=0)
+        v, t, kind, cores, _ = cpu_reference_run(sample, cfg, steps=max(1, min(args.steps, 3)), warmup=0)
         desc = (f"meshes 0..{len(idx) - 1} of {cfg} ({int(sample.num_faces_per_mesh().sum())} faces), fwd"
                 + ("+bwd" if c["backward"] else "") + ", reference semantics (no perspective_correct/cull)")
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
@@ -414,14 +513,31 @@ def main():
                "zero_copy_cotangents": bool(args.e2e_zero_copy), "gather_cotangents": bool(args.e2e_gather),
                "api": "paper_2007_08501_b200.pipeline.HostPipeline.run (pinned host in/out)"}
 
+    like = None
+    if rank == 0 and world == 1 and args.like_for_like and (rs.perspective_correct or rs.cull_backfaces):
+        like = like_for_like_leg(args, cfg, meshes_all, cam, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # median of >= 3 runs on all host threads, plus a 1-thread figure on a smaller sample
         idx = cpu_sample(meshes_all, args.cpu_sample_faces)
         sample = subset(meshes_all, idx)
-        v, t, kind, cores = cpu_reference_run(sample, cfg, steps=1)
+        v, t, kind, cores, times = cpu_reference_run(sample, cfg, steps=args.cpu_runs)
+        idx1 = cpu_sample(meshes_all, args.cpu_sample_faces_1t)
+        s1 = subset(meshes_all, idx1)
+        v1, t1, _, _, _ = cpu_reference_run(s1, cfg, steps=1, threads=1)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"meshes 0..{len(idx) - 1} of {cfg} ({int(sample.num_faces_per_mesh().sum())} faces), "
-                         f"fwd{'+bwd' if c['backward'] else ''}, {t:.2f} s, reference semantics"}
+                         f"fwd{'+bwd' if c['backward'] else ''}, median of {len(times)} runs "
+                         f"({', '.join(f'{x:.2f}' for x in times)} s), reference semantics",
+               "one_thread": {"value": v1, "unit": UNIT, "cores": 1, "seconds": t1,
+                              "sample": f"meshes 0..{len(idx1) - 1} ({int(s1.num_faces_per_mesh().sum())} faces)"}}
+        if like is not None:
+            like["sample"]["ref_value"] = v
+            like["sample"]["ratio"] = like["sample"]["gpu_value"] / v
+            if like["sample"].get("gpu_e2e") is not None:
+                like["sample"]["e2e_ratio"] = like["sample"]["gpu_e2e"] / v
+            like["full"]["ratio_vs_ref_rate"] = like["full"]["gpu_value"] / v
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -431,7 +547,8 @@ def main():
                           "faces": int(meshes_all.num_faces_per_mesh().sum()), "image": H, "K": K,
                           "blur_radius": c["blur"], "bin_size": c["bin_size"], "parallelism": f"mesh-shard{world}",
                           "l2": "inputs+outputs (GBs) exceed the 126 MB L2; no flush"},
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "like_for_like": like,
+               "gpu_launches": int(launches),
                "clocks": clk.summary()}
         print(json.dumps(out))
     if dist is not None:
