@@ -77,3 +77,21 @@ def fast_cotangents(S_: int, seed: int = 1):
 def rel_err(a, b, floor=1e-12):
     a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), floor)) if a.size else 0.0
+
+
+GRAD_RTOL, GRAD_ATOL_SCALE = 1e-4, 1e-8
+
+
+def grad_close(got, want, what="", rtol=GRAD_RTOL, atol_scale=GRAD_ATOL_SCALE):
+    """north_star "face_verts gradients within 1e-4 relative", element by element:
+    |got - want| <= rtol * |want| + atol_scale * max|want| (the absolute term only absorbs elements whose
+    contributions cancel to below atol_scale of the largest gradient). Returns the worst element's err / bound."""
+    got, want = np.asarray(got, np.float64).ravel(), np.asarray(want, np.float64).ravel()
+    assert got.shape == want.shape, what
+    if not want.size:
+        return 0.0
+    bound = rtol * np.abs(want) + atol_scale * float(np.abs(want).max())
+    ratio = np.abs(got - want) / np.maximum(bound, 1e-300)
+    i = int(np.argmax(ratio))
+    assert ratio[i] <= 1.0, f"{what}: element {i} got {got[i]!r} want {want[i]!r} (err/bound {ratio[i]:.3g})"
+    return float(ratio[i])

@@ -13,7 +13,7 @@ import pytest
 import torch
 
 from paper_2007_08501_b200 import scenes as S
-from tests._common import (acceptance_scenes, boundary, cotangents, fast_cotangents, orc_settings,
+from tests._common import (acceptance_scenes, boundary, cotangents, fast_cotangents, grad_close, orc_settings,
                            raster_settings, raster_test_scenes, rel_err)
 
 pytestmark = pytest.mark.gpu
@@ -175,6 +175,7 @@ def test_builder_defined_flags(persp, clip, cull, oracle, cuda):
     g_want = oracle.backward(fv, first, num, o, want[0], want[2], dz, db, dd)
     g_got = gpu_bwd(fv, first, num, rs, cuda, got[0], got[2], dz, db, dd, torch.float64)
     assert rel_err(g_got, g_want) < 1e-9
+    grad_close(g_got, g_want, f"flags {persp}{clip}{cull}")
 
 
 def test_forward_rerun_identical(cuda):
@@ -205,11 +206,13 @@ def test_c2_forward_backward(oracle, cuda):
                              dd32.astype(np.float64))
     g_got = gpu_bwd(fv, first, num, raster_settings(128, 8, 1e-4, cam), cuda, got[0], got[2], dz32, db32, dd32)
     assert rel_err(g_got, g_want) < GRAD_RTOL
+    grad_close(g_got, g_want, "C2 fp32")
     # fp64 variant: same inputs as the oracle, agreement to accumulation order
     g64 = gpu_bwd(fv, first, num, raster_settings(128, 8, 1e-4, cam), cuda, want[0], want[2], dz, db, dd,
                   torch.float64)
     g_w64 = oracle.backward(fv, first, num, o, want[0], want[2], dz, db, dd)
     assert rel_err(g64, g_w64) < 1e-12
+    grad_close(g64, g_w64, "C2 fp64")
 
 
 def test_backward_end_to_end_vs_reference(reflib, oracle, cuda):
@@ -224,6 +227,7 @@ def test_backward_end_to_end_vs_reference(reflib, oracle, cuda):
                 torch.float64)
     d_got = S.scatter_face_grads(m, cam, g)
     assert rel_err(d_got, d_ref) < 1e-10
+    grad_close(d_got, d_ref, "C2 world d_verts vs reference")
 
 
 def test_backward_finite_differences(cuda):
@@ -330,6 +334,7 @@ def test_full_config_properties_and_mesh_sample(cfg, oracle, cuda):
             g_g = gpu_bwd(fv, f_, n_, rs, cuda, got[0], got[2], dz, db, dd)
             sl = slice(int(f_[0]), int(f_[0] + n_[0]))
             assert rel_err(g_g[sl], g_w[sl]) < GRAD_RTOL
+            grad_close(g_g[sl], g_w[sl], f"{cfg} mesh 0")
 
 
 # -------------------------------------------------------------------------------------------------

@@ -11,7 +11,7 @@ import pytest
 import torch
 
 from paper_2007_08501_b200 import scenes as S
-from tests._common import boundary, orc_settings, raster_settings, rel_err
+from tests._common import boundary, grad_close, orc_settings, raster_settings, rel_err
 
 SIGMA = 1e-4
 GRAD_RTOL = 1e-4
@@ -82,6 +82,7 @@ def test_fused_silhouette_forward_and_backward(name, H, K, blur, flags, oracle, 
                                       torch.as_tensor(da, device=cuda)).cpu().numpy()
     assert np.abs(g_want).max() > 0
     assert rel_err(g, g_want) < GRAD_RTOL, f"{name}: grad rel err {rel_err(g, g_want):.2e}"
+    grad_close(g, g_want, name)
     assert np.all(g[..., 2] == 0.0)  # d_zbuf = d_bary = 0: no depth gradient
 
 

@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from paper_2007_08501_b200 import scenes as S
-from tests._common import boundary, raster_settings, rel_err
+from tests._common import boundary, grad_close, raster_settings, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -49,6 +49,7 @@ def test_softmax_render_vs_reference(name, H, K, blur, sigma, gamma, reflib, cud
     d_got = S.scatter_face_grads(m, cam, g_fv.cpu().numpy())
     assert np.abs(dv_ref).max() > 0 and np.abs(dc_ref).max() > 0
     assert rel_err(d_got, dv_ref) < 1e-4, f"{name}: d_verts rel err {rel_err(d_got, dv_ref):.2e}"
+    grad_close(d_got, dv_ref, name)
     assert rel_err(g_vc.cpu().numpy(), dc_ref) < 1e-6, f"{name}: d_colors rel err {rel_err(g_vc.cpu().numpy(), dc_ref):.2e}"
 
 

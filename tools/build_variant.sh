@@ -1,12 +1,15 @@
 #!/bin/bash
 # build_variant.sh NAME "EXTRA NVCC FLAGS" -> build/variants/NAME/libdr_raster_b200.so (A/B experiments only)
+# FMAD_FILES="raster_bwd ..." compiles those translation units with FMA contraction allowed (-fmad=true).
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
 out=build/variants/$name; mkdir -p $out
 SRCS=$(cd paper_2007_08501_b200/csrc && ls *.cu | sed 's/\.cu$//')
 for f in $SRCS; do
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v "$@" \
+  fmad=-fmad=false
+  for g in $FMAD_FILES; do [ "$g" = "$f" ] && fmad=-fmad=true; done
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 $fmad -Xcompiler -fPIC -Xptxas -v "$@" \
     -c paper_2007_08501_b200/csrc/$f.cu -o $out/$f.o 2> $out/$f.ptxas.txt &
 done
 wait
