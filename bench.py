@@ -47,10 +47,6 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-groups", type=int, default=24, help="mesh groups the host pipeline streams")
     ap.add_argument("--e2e-lookahead", type=int, default=3, help="H2D of group g waits for D2H of g - L (0: off)")
-    ap.add_argument("--e2e-zero-copy", type=int, default=0,
-                    help="1: the backward reads the pinned host cotangents in place (occupied slots only)")
-    ap.add_argument("--e2e-gather", type=int, default=0,
-                    help="1: a device kernel gathers only the occupied slots' cotangents from pinned host memory")
     ap.add_argument("--e2e-ramp", type=int, default=2, help="smaller first/last pipeline groups (HostPipeline ramp)")
     ap.add_argument("--cpu-sample-faces", type=float, default=0.25,
                     help="fraction of the batch's faces the CPU sample covers")
@@ -479,8 +475,7 @@ def main():
         del ws  # the pipeline owns its own device buffers
         torch.cuda.empty_cache()
         pipe = HostPipeline(first_np, num_np, rs, F, dev, n_groups=args.e2e_groups, backward=c["backward"],
-                            ramp=args.e2e_ramp, lookahead=args.e2e_lookahead,
-                            zero_copy=bool(args.e2e_zero_copy), gather=bool(args.e2e_gather))
+                            ramp=args.e2e_ramp, lookahead=args.e2e_lookahead)
         h_fv = torch.from_numpy(fv_np).pin_memory()
         cot_h = tuple(t.cpu().pin_memory() for t in (dz, db, dd)) if c["backward"] else None
         out_h = (torch.empty((N, H, W, K), dtype=torch.int64).pin_memory(),
@@ -492,11 +487,7 @@ def main():
         e2e_steps = max(1, min(args.steps, 5))
         pipe.run(h_fv, out_h, cot_h, grad_h)
         barrier()
-        if c["backward"] and (args.e2e_zero_copy or args.e2e_gather):
-            # only the occupied slots' cotangents cross PCIe (read in place by the backward): 20 B per slot
-            h2d = h_fv.numel() * 8 + int((out_h[0] >= 0).sum()) * 20
-        else:
-            h2d = h_fv.numel() * 8 + (sum(t.numel() for t in cot_h) * 4 if c["backward"] else 0)
+        h2d = h_fv.numel() * 8 + (sum(t.numel() for t in cot_h) * 4 if c["backward"] else 0)
         e0.record(st)
         for _ in range(e2e_steps):
             pipe.run(h_fv, out_h, cot_h, grad_h)
@@ -510,7 +501,6 @@ def main():
         e2e = {"value": total_fpx / (ems * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "pcie_gbs": (h2d + d2h) / (ems * 1e-3) / 1e9, "groups": len(pipe.groups), "ramp": args.e2e_ramp, "lookahead": args.e2e_lookahead,
-               "zero_copy_cotangents": bool(args.e2e_zero_copy), "gather_cotangents": bool(args.e2e_gather),
                "api": "paper_2007_08501_b200.pipeline.HostPipeline.run (pinned host in/out)"}
 
     like = None

@@ -100,7 +100,8 @@ int dr_rasterize_meshes_fwd_f64(const double* face_verts, const int64_t* mesh_to
  * untouched (so disjoint groups of meshes of one packed buffer can be processed by separate calls).
  * pix_to_face / bary_coords are the forward's outputs for the same batch (the reference reads frag.bary,
  * mesh_raster.cpp:359).
- * Accumulation uses fp64 atomics: the summation order is not fixed, results agree to ~1e-15 relative. */
+ * Accumulation uses fp64 atomics: the summation order is not fixed, results agree to ~1e-15 relative.
+ * The cotangents must be device memory (DR_ERR_USAGE otherwise, page-locked host memory included). */
 int dr_rasterize_meshes_bwd(const double* face_verts, const int64_t* mesh_to_face_first_idx,
                             const int64_t* num_faces_per_mesh, int64_t N, int64_t F,
                             const dr_raster_settings* s, const int64_t* pix_to_face, const float* bary_coords,
@@ -169,12 +170,6 @@ int dr_packed_to_padded(const void* packed, const int64_t* first, const int64_t*
 /* packed[first[b] + j, :] = padded[b, j, :] for j < num[b]. */
 int dr_padded_to_packed(const void* padded, const int64_t* first, const int64_t* num, int64_t N, int64_t max_count,
                         int64_t row_bytes, void* packed, dr_stream_t stream);
-/* Host pipeline helper: copy the backward's cotangents (fp32; grad_bary [S,3]) from page-locked host (or
- * device) arrays to device arrays at the occupied slots only (pix_to_face >= 0) — the slots
- * dr_rasterize_meshes_bwd reads; the other destination slots are left untouched. */
-int dr_gather_occupied_cotangents(const int64_t* pix_to_face, int64_t S, const float* grad_zbuf_src,
-                                  const float* grad_bary_src, const float* grad_dists_src, float* grad_zbuf,
-                                  float* grad_bary, float* grad_dists, dr_stream_t stream);
 /* out[i] = the batch element owning packed row i (PackedView::item_to_element), -1 for rows in no range. */
 int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
                               dr_stream_t stream);

@@ -31,7 +31,6 @@ EXPORTED_SYMBOLS = (
     "dr_rasterize_silhouette_fwd_f64_hr",
     "dr_rasterize_silhouette_bwd_f64_hr",
     "dr_world_to_face_verts_async",
-    "dr_gather_occupied_cotangents",
     "dr_rasterize_softmax_fwd",
     "dr_rasterize_softmax_bwd",
     "dr_point_raster_settings_default",
@@ -148,8 +147,6 @@ def load() -> C.CDLL:
     L.dr_rasterize_silhouette_bwd_f64_hr.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, C.c_double, _vp, _vp,
                                                      _vp, _vp, _vp, _vp]
     L.dr_world_to_face_verts_async.argtypes = [_vp, C.c_int64, _vp, C.c_int64, C.POINTER(DrCamera), _vp, _vp, _vp]
-    L.dr_gather_occupied_cotangents.argtypes = [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
-    L.dr_gather_occupied_cotangents.restype = C.c_int
     L.dr_selftest_division.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
     L.dr_selftest_division.restype = C.c_int
     bpp = C.POINTER(DrBlendParams)

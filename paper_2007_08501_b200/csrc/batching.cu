@@ -117,28 +117,5 @@ cudaError_t launch_item_to_element(const int64_t* first, const int64_t* num, int
   return cudaGetLastError();
 }
 
-// Occupied-slot cotangent gather (host pipeline): dz/dd [S] and db [S,3] fp32 are copied from (page-locked,
-// host-mapped) source arrays to device arrays only where pix_to_face >= 0 — the slots rasterize_backward reads
-// (MR:347-350). Each warp covers 32 consecutive slots, so the host reads stay in contiguous runs.
-__global__ void k_gather_occupied(const int64_t* __restrict__ p2f, int64_t S, const float* __restrict__ dz_src,
-                                  const float* __restrict__ db_src, const float* __restrict__ dd_src,
-                                  float* __restrict__ dz, float* __restrict__ db, float* __restrict__ dd) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < S; t += (int64_t)gridDim.x * blockDim.x) {
-    if (p2f[t] < 0) continue;
-    dz[t] = dz_src[t];
-    dd[t] = dd_src[t];
-    db[3 * t] = db_src[3 * t];
-    db[3 * t + 1] = db_src[3 * t + 1];
-    db[3 * t + 2] = db_src[3 * t + 2];
-  }
-}
-
-cudaError_t launch_gather_occupied(const int64_t* p2f, int64_t S, const float* dz_src, const float* db_src,
-                                   const float* dd_src, float* dz, float* db, float* dd, cudaStream_t st) {
-  if (S <= 0) return cudaSuccess;
-  const unsigned grid = (unsigned)std::min<int64_t>((S + 255) / 256, 148 * 64);
-  k_gather_occupied<<<grid, 256, 0, st>>>(p2f, S, dz_src, db_src, dd_src, dz, db, dd);
-  return cudaGetLastError();
-}
 
 }  // namespace drb

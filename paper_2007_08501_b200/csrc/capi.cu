@@ -95,15 +95,6 @@ struct Plan {
          total = 0;
 };
 
-// DR_ZSORT=0 disables the depth-ordered fine stage (A/B measurements; results are identical either way)
-bool zsort_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("DR_ZSORT");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 // list-pool capacity: the workspace is planned before the bin counts exist; 8 entries per face covers every
 // benchmark scene (faces touch 1-2 bins on average); bins past the pool take the exact spill path
 int64_t pool_entries(int64_t F) { return 8 * F + 65536; }
@@ -131,7 +122,7 @@ int make_plan(int64_t N, int64_t F, const dr_raster_settings* s, Plan& p) {
   p.nbx = (p.W + p.bs - 1) / p.bs;
   p.nby = (p.H + p.bs - 1) / p.bs;
   p.cap = p.binned ? s->max_faces_per_bin : 0;  // 0 = unlimited (the reference's bins are unbounded, MR:244)
-  p.zsort = s->clip_barycentric_coords != 0 && zsort_enabled();
+  p.zsort = s->clip_barycentric_coords != 0;
   size_t off = 0;
   p.off_ibbox = off;
   off = align_up(off + sizeof(int4) * (size_t)std::max<int64_t>(F, 1));
@@ -248,8 +239,9 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   if (p.binned) {
     {
       ProfScope ps(st, KN_MEMSET);
-      cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)p.nbins_total, st);
-      cudaMemsetAsync(cursor, 0, sizeof(int) * (size_t)p.nbins_total, st);
+      cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)p.nbins_total, st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(cursor, 0, sizeof(int) * (size_t)p.nbins_total, st);
+      if (e != cudaSuccess) return cuda_fail(e, "zeroing bin counts");
     }
     {
       ProfScope ps(st, KN_BIN);  // count -> scan -> fill: exact-size lists
@@ -258,11 +250,8 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
       drb::launch_fill_bins(ibbox, first, num, N, max_faces, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool,
                             p.zsort ? zkey : nullptr, entries, st);
     }
-    static const bool sort_on = [] {  // DR_SORT=0: keep the fill order (A/B of the depth ordering)
-      const char* e = std::getenv("DR_SORT");
-      return !(e && e[0] == '0');
-    }();
-    if (p.zsort && sort_on) {
+    // depth order of the bins (measured: skipping it costs C4 +9 % and C5 +170 % in K2)
+    if (p.zsort) {
       ProfScope ps(st, KN_SORT);
       cudaError_t e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, p.cap, st);
       if (e != cudaSuccess) return cuda_fail(e, "sorting bins");
@@ -305,11 +294,6 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
     }
   }
   if (nw == 0) return fail(DR_ERR_RANGE, "faces_per_pixel=%d too large for the shared-memory top-K", p.K);
-  static const int nw_env = [] {  // DR_FINE_NW=2|8: force the CTA size (A/B of the occupancy choice)
-    const char* e = std::getenv("DR_FINE_NW");
-    return e ? std::atoi(e) : 0;
-  }();
-  if ((nw_env == 2 || nw_env == 8) && (size_t)nw_env * per_warp <= 227 * 1024) nw = nw_env;
   A.N = (int)N;
   A.work_counter = reinterpret_cast<unsigned long long*>(base + p.off_counter);
   A.p2f = p2f;
@@ -340,14 +324,14 @@ int bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   if (rc) return rc;
   if (!first || !num || !p2f || !bary || !dz || !db || !dd || (F > 0 && (!fv || !grad)))
     return fail(DR_ERR_USAGE, "null input/output pointer");
-  // the cotangents may live in page-locked HOST memory (read in place over PCIe through the unified address
-  // space: only occupied slots are touched, so a host caller skips copying the empty slots' cotangents);
-  // pageable host memory is rejected instead of faulting in the kernel
+  // cotangents in host memory would fault in the kernel (pageable) or crawl over PCIe (page-locked: measured
+  // slower than copying them): both are rejected
   for (const void* ptr : {static_cast<const void*>(dz), static_cast<const void*>(db), static_cast<const void*>(dd)}) {
     cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess || at.type == cudaMemoryTypeUnregistered) {
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess ||
+        (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)) {
       cudaGetLastError();
-      return fail(DR_ERR_USAGE, "cotangent pointer is neither device nor page-locked host memory");
+      return fail(DR_ERR_USAGE, "cotangent pointer is not device memory");
     }
   }
   int64_t mx;
@@ -429,14 +413,6 @@ int sil_bwd_impl(const double* fv, const int64_t* first, const int64_t* num, int
   return DR_OK;
 }
 
-bool point_exact_sort() {
-  static const bool v = [] {
-    const char* e = std::getenv("DR_POINT_EXACT_SORT");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
 // ---- point rasterizer (point_render.cpp:105-155) ----
 struct PointPlan {
   int64_t N = 0, P = 0;
@@ -478,7 +454,16 @@ int make_point_plan(int64_t N, int64_t P, const dr_point_raster_settings* s, Poi
   p.off_counts = off;
   if (p.binned) {
     p.nbins_total = N * (int64_t)p.nbx * p.nby;
-    p.pool = 8 * P + 65536;
+    // list-pool capacity from the radius: a point lands in the tiles its radius-inflated tile test keeps
+    // (PR:125-134), about (r W / bs + 2) x (r H / bs + 2) of them (tile side 2 bs / W in NDC), so a wide radius
+    // does not push most bins onto the unsorted whole-cloud spill path. Clamped to keep the workspace bounded;
+    // bins past the pool still rasterize correctly (spill path).
+    const double r = std::max(0.0, s->radius);
+    const double tx = std::min<double>(p.nbx, std::floor(r * p.W / p.bs) + 2.0);
+    const double ty = std::min<double>(p.nby, std::floor(r * p.H / p.bs) + 2.0);
+    const double want = (double)P * std::max(1.0, tx * ty);
+    const double cap = std::max<double>(8.0 * P, (double)(1ll << 28));
+    p.pool = (int64_t)std::min(want, cap) + 65536;
     off = align_up(off + sizeof(int) * (size_t)p.nbins_total);
     p.off_cursor = off;
     off = align_up(off + sizeof(int) * (size_t)p.nbins_total);
@@ -532,8 +517,9 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   if (p.binned) {
     {
       ProfScope ps(st, KN_MEMSET);
-      cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)p.nbins_total, st);
-      cudaMemsetAsync(cursor, 0, sizeof(int) * (size_t)p.nbins_total, st);
+      e = cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)p.nbins_total, st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(cursor, 0, sizeof(int) * (size_t)p.nbins_total, st);
+      if (e != cudaSuccess) return cuda_fail(e, "zeroing point bin counts");
     }
     ProfScope ps(st, KN_BIN);
     drb::launch_bin_faces(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, st);
@@ -541,20 +527,19 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
     drb::launch_fill_bins(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool, zkey,
                           entries, st);
   }
-  const bool sorted = p.binned && zsort_enabled();
+  const bool sorted = p.binned;
   if (sorted) {
     ProfScope ps(st, KN_SORT);
     // the point fine stage stops streaming a bin once a lower bound of its remaining keys exceeds every pixel's
-    // K-th depth: with the bucket order that bound comes from the bin's bucket map (brange), with the exact
-    // bitonic order (DR_POINT_EXACT_SORT=1) from the next key itself
-    e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, 0, st, point_exact_sort(),
-                              point_exact_sort() ? nullptr : brange);
-    // (bin_range is only written when the sort really ran in bucket mode)
+    // K-th depth; that bound comes from the bin's bucket map (brange), written by the sort for every bin the
+    // fine stage treats as sorted (drb::bin_is_sorted with cap 0)
+    e = drb::launch_sort_bins(counts, bin_off, entries, ibbox, p.nbins_total, p.pool, 0, st, brange);
     if (e != cudaSuccess) return cuda_fail(e, "sorting point bins");
   }
   drb::PointFineArgs<OutT> A;
   A.pts = pts;
   A.ibbox = ibbox;
+  A.zkey = zkey;
   A.first = first;
   A.num = num;
   A.bin_counts = counts;
@@ -566,7 +551,7 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
   A.nbx = p.nbx;
   A.nby = p.nby;
   A.sorted = sorted ? 1 : 0;
-  A.brange = sorted && drb::sort_uses_buckets(point_exact_sort()) ? brange : nullptr;
+  A.brange = sorted ? brange : nullptr;
   A.sub_x = (p.bs + 15) / 16;
   A.sub_y = (p.bs + 15) / 16;
   A.H = p.H;
@@ -987,27 +972,6 @@ int dr_padded_to_packed(const void* padded, const int64_t* first, const int64_t*
     e = drb::launch_padded_to_packed(padded, first, num, N, max_count, row_bytes, packed, st);
   }
   return e == cudaSuccess ? DR_OK : cuda_fail(e, "padded_to_packed");
-}
-
-int dr_gather_occupied_cotangents(const int64_t* pix_to_face, int64_t S, const float* grad_zbuf_src,
-                                  const float* grad_bary_src, const float* grad_dists_src, float* grad_zbuf,
-                                  float* grad_bary, float* grad_dists, dr_stream_t stream) {
-  if (S < 0) return fail(DR_ERR_SHAPE, "negative slot count");
-  if (S == 0) return DR_OK;
-  if (!pix_to_face || !grad_zbuf_src || !grad_bary_src || !grad_dists_src || !grad_zbuf || !grad_bary || !grad_dists)
-    return fail(DR_ERR_USAGE, "null pointer");
-  for (const void* ptr : {static_cast<const void*>(grad_zbuf_src), static_cast<const void*>(grad_bary_src),
-                          static_cast<const void*>(grad_dists_src)}) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess || at.type == cudaMemoryTypeUnregistered) {
-      cudaGetLastError();
-      return fail(DR_ERR_USAGE, "source pointer is neither device nor page-locked host memory");
-    }
-  }
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e = drb::launch_gather_occupied(pix_to_face, S, grad_zbuf_src, grad_bary_src, grad_dists_src, grad_zbuf,
-                                              grad_bary, grad_dists, st);
-  return e == cudaSuccess ? DR_OK : cuda_fail(e, "gather_occupied_cotangents");
 }
 
 int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,

@@ -36,16 +36,12 @@ __device__ __forceinline__ void clamp_bary_backward(const double wr[3], const do
   }
 }
 
-// one occupied slot's per-slot inputs (bary + cotangents), loaded one batch ahead of their use
-#ifndef DR_BWD_PREFETCH_FV
-#define DR_BWD_PREFETCH_FV 1
-#endif
+// one occupied slot's per-slot inputs (bary + cotangents + the face's face_verts), loaded one batch ahead of
+// their use
 template <typename InT>
 struct SlotIn {
   InT w[3], dz, db[3], dd;
-#if DR_BWD_PREFETCH_FV
   double v[9];  // the face's face_verts
-#endif
 };
 template <typename InT>
 __device__ __forceinline__ void load_slot(const BwdArgs<InT>& A, int64_t slot, int32_t fid, SlotIn<InT>& in) {
@@ -56,11 +52,9 @@ __device__ __forceinline__ void load_slot(const BwdArgs<InT>& A, int64_t slot, i
   }
   in.dz = __ldcs(A.d_zbuf + slot);
   in.dd = __ldcs(A.d_dists + slot);
-#if DR_BWD_PREFETCH_FV
   const double* q = A.fv + 9 * (int64_t)fid;
 #pragma unroll
   for (int k = 0; k < 9; ++k) in.v[k] = __ldg(q + k);
-#endif
 }
 
 // per-slot cotangents -> g[9] = (dx, dy, dz) for vertices a, b, c; p = the slot's pixel centre (MR:357)
@@ -69,15 +63,7 @@ __device__ __forceinline__ void load_slot(const BwdArgs<InT>& A, int64_t slot, i
 template <typename InT, bool kInternalW = false>
 __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32_t fid, const SlotIn<InT>& in,
                                               double g[9], double* w_out = nullptr) {
-#if DR_BWD_PREFETCH_FV
   const FaceGeom fg = make_face_geom(in.v);
-#else
-  const double* q = A.fv + 9 * (int64_t)fid;
-  double v[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) v[k] = __ldg(q + k);
-  const FaceGeom fg = make_face_geom(v);
-#endif
   const double z[3] = {fg.z0, fg.z1, fg.z2};
 
   double w_hat[3] = {(double)in.w[0], (double)in.w[1], (double)in.w[2]};
@@ -209,25 +195,13 @@ __device__ __forceinline__ bool reduce_by_face(int32_t fid, int lane, double g[N
 // Persistent warps walk the slots in chunks of kChunk consecutive slots. Occupied slots (pix_to_face >= 0;
 // typically 40-70 % of them) are compacted with ballot + popc into a warp-private queue and processed 32 at
 // a time, so every lane of a batch does a full per-slot backward.
-#ifndef DR_BWD_CHUNK_STEPS
-#define DR_BWD_CHUNK_STEPS 16
-#endif
-constexpr int kBwdChunk = 32 * DR_BWD_CHUNK_STEPS;
-
-#ifndef DR_BWD_THREADS
-#define DR_BWD_THREADS 128
-#endif
-#ifndef DR_BWD_CHUNKS_PER_WARP
-#define DR_BWD_CHUNKS_PER_WARP 4
-#endif
-#ifndef DR_BWD_MINBLOCKS
-#define DR_BWD_MINBLOCKS 3
-#endif
+constexpr int kBwdChunk = 32 * 16;
+constexpr int kBwdMinBlocks = 3;
 // 128-thread CTAs, 3 per SM (155 registers, no spills): with the cp.async pix_to_face prefetch and the
 // one-batch-ahead input loads, latency is hidden by ILP rather than by more resident warps (C4: 80 registers x
 // 24 warps 3.47 ms, 96 x 20 3.33 ms, 128 x 16 3.10 ms with the first design; with the prefetching one
 // 128 x 16 (36-byte spills) 2.54 ms, 155 x 12 2.48 ms; profiles/r01/README.md).
-constexpr int kBwdThreads = DR_BWD_THREADS;
+constexpr int kBwdThreads = 128;
 
 template <typename InT>
 __device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, V2 p, int32_t my_fid, const SlotIn<InT>& in,
@@ -252,15 +226,7 @@ __device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, V2 p, int3
 // bary / cotangents loaded before the current step computes.
 constexpr int kPixTab = 2048;  // pixel-centre tables in shared memory when H + W fits
 
-#ifndef DR_BWD_V2
-#define DR_BWD_V2 1
-#endif
-#ifndef DR_BWD_RANKMAJOR
-#define DR_BWD_RANKMAJOR 0  // measured slower (C4 2.48 -> 3.05 ms): longer reductions, scattered input loads
-#endif
-#ifndef DR_BWD_CHUNKS_PER_CTA
-#define DR_BWD_CHUNKS_PER_CTA 32
-#endif
+constexpr int kBwdChunksPerCta = 32;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -306,13 +272,12 @@ __device__ __forceinline__ void backward_chunk(const BwdArgs<InT>& A, int64_t c0
   }
 }
 
-#if DR_BWD_V2
-// CTA = DR_BWD_CHUNKS_PER_CTA consecutive chunks; its warps take chunks from a shared counter (so they finish
+// CTA = kBwdChunksPerCta consecutive chunks; its warps take chunks from a shared counter (so they finish
 // together and the CTA's registers are released without idle warps holding them). While a warp computes chunk
 // c, the pix_to_face words of its next chunk stream into shared memory with cp.async (no registers held);
 // the chunk is then compacted (occupied slots -> queue of 16-bit offsets + face ids) straight from shared memory.
 template <typename InT>
-__global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdArgs<InT> A) {
+__global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_backward(BwdArgs<InT> A) {
   constexpr int NWB = kBwdThreads / 32;
   __shared__ __align__(16) int64_t stage[NWB][kBwdChunk];
   __shared__ int32_t q_fid[NWB][kBwdChunk];
@@ -326,12 +291,12 @@ __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdA
       pix_tab[t] = t < A.W ? pixel_x(A.W, t) : pixel_y(A.H, t - A.W);
   __syncthreads();
   constexpr int kSteps = kBwdChunk / 32;
-  // chunk k of this CTA starts at slot chunk0(k); valid while k < DR_BWD_CHUNKS_PER_CTA and it starts before S
+  // chunk k of this CTA starts at slot chunk0(k); valid while k < kBwdChunksPerCta and it starts before S
   // (only k is carried across the chunk's compute: everything else is recomputed, to stay spill-free)
   auto chunk0 = [&](int k) {
-    return ((int64_t)blockIdx.x * DR_BWD_CHUNKS_PER_CTA + k) * kBwdChunk;
+    return ((int64_t)blockIdx.x * kBwdChunksPerCta + k) * kBwdChunk;
   };
-  auto valid = [&](int k) { return k < DR_BWD_CHUNKS_PER_CTA && chunk0(k) < A.S; };
+  auto valid = [&](int k) { return k < kBwdChunksPerCta && chunk0(k) < A.S; };
   auto issue = [&](int k) {  // start the copy of chunk k's pix_to_face words (slots past S are not copied)
     const int lane = threadIdx.x & 31;
     const int64_t c0 = chunk0(k);
@@ -354,14 +319,11 @@ __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdA
     cp_async_wait_all();
     __syncwarp();
     int n = 0;
-    // DR_BWD_RANKMAJOR (K divides the chunk): queue the chunk's slots rank-major — a step's lanes are neighbouring
-    // pixels at the same list rank, which mostly hold the same face, so reduce_by_face merges them before the atomics
-    const bool rank_major = DR_BWD_RANKMAJOR && kBwdChunk % A.K == 0;
-    const int ppc = kBwdChunk / A.K;  // pixels per chunk (rank-major)
+    // (a rank-major queue order, which merges more same-face lanes per reduce_by_face, measured slower: C4 2.48 ->
+    // 3.05 ms, longer reductions and scattered input loads)
 #pragma unroll 4
     for (int t = 0; t < kSteps; ++t) {
-      const int u = t * 32 + lane;
-      const int o = rank_major ? (u % ppc) * A.K + u / ppc : u;
+      const int o = t * 32 + lane;
       const int64_t slot = c0 + o;
       const int64_t f = slot < A.S ? stg[o] : -1;
       const bool occ = f >= 0 && f < A.F;
@@ -383,81 +345,6 @@ __global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdA
     k = kn;
   }
 }
-#else
-template <typename InT>
-__global__ void __launch_bounds__(kBwdThreads, DR_BWD_MINBLOCKS) k_backward(BwdArgs<InT> A) {
-  __shared__ int32_t q_off[kBwdThreads / 32][kBwdChunk];
-  __shared__ int32_t q_fid[kBwdThreads / 32][kBwdChunk];
-  __shared__ double pix_tab[kPixTab];  // pixel_x(W, j) for j < W, then pixel_y(H, i) (camera.cpp:100-102)
-  const bool tab = A.W + A.H <= kPixTab;
-  if (tab) {
-    for (int t = threadIdx.x; t < A.W + A.H; t += kBwdThreads)
-      pix_tab[t] = t < A.W ? pixel_x(A.W, t) : pixel_y(A.H, t - A.W);
-    __syncthreads();
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int32_t* qo = q_off[wid];
-  int32_t* qf = q_fid[wid];
-  constexpr int kSteps = kBwdChunk / 32;
-  const int HW = A.H * A.W;
-  for (int64_t c0 = warp * kBwdChunk; c0 < A.S; c0 += nwarps * kBwdChunk) {
-    int64_t f[kSteps];
-#pragma unroll
-    for (int t = 0; t < kSteps; ++t) {
-      const int64_t slot = c0 + t * 32 + lane;
-      f[t] = slot < A.S ? __ldcs(A.p2f + slot) : -1;  // streamed once: evict-first
-    }
-    int n = 0;
-#pragma unroll
-    for (int t = 0; t < kSteps; ++t) {
-      const bool occ = f[t] >= 0 && f[t] < A.F;
-      const unsigned m = __ballot_sync(0xffffffffu, occ);
-      if (occ) {
-        const int pos = n + __popc(m & ((1u << lane) - 1u));
-        qo[pos] = t * 32 + lane;
-        qf[pos] = (int32_t)f[t];
-      }
-      n += __popc(m);
-    }
-    __syncwarp();
-    // slot -> pixel with one 64-bit division per chunk; 32-bit arithmetic per slot
-    const int64_t pix0 = c0 / A.K;
-    const int r0 = (int)(c0 - pix0 * A.K);
-    const int pp0 = (int)(pix0 % HW);
-    SlotIn<InT> nxt;
-    int32_t nfid = -1;
-    int noff = 0;
-    if (lane < n) {
-      noff = qo[lane];
-      nfid = qf[lane];
-      load_slot(A, c0 + noff, nfid, nxt);
-    }
-    for (int q0 = 0; q0 < n; q0 += 32) {
-      const SlotIn<InT> cur = nxt;
-      const int32_t my_fid = nfid;
-      const int off = noff;
-      nfid = -1;
-      if (q0 + 32 + lane < n) {
-        noff = qo[q0 + 32 + lane];
-        nfid = qf[q0 + 32 + lane];
-        load_slot(A, c0 + noff, nfid, nxt);
-      }
-      V2 p{0.0, 0.0};
-      if (my_fid >= 0) {
-        uint32_t pp = (uint32_t)pp0 + A.divK.div((uint32_t)(r0 + off));
-        if (pp >= (uint32_t)HW) pp %= (uint32_t)HW;  // the chunk crossed into the next image
-        const uint32_t i = A.divW.div(pp), j = pp - i * (uint32_t)A.W;
-        p = tab ? V2{pix_tab[j], pix_tab[A.W + i]} : V2{pixel_x(A.W, (int)j), pixel_y(A.H, (int)i)};  // MR:357
-      }
-      backward_batch(A, p, my_fid, cur, lane);
-    }
-    __syncwarp();
-  }
-}
-
-#endif
 
 // ------------------------------------------------------------------------------------------------
 // Fused silhouette backward: silhouette_blend_backward (shading.cpp:93-121) feeding rasterize_backward
@@ -641,14 +528,8 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
 //   B  per queued slot: distance envelope + prob = sigmoid(-dist / sigma)          (lane per slot)
 //   C  per pixel: suffix products, then coefficient da * prefix * suffix * dprob   (lane per pixel, K steps)
 //   D  per queued slot: the envelope gradient, reduce_by_face, fp64 atomics       (lane per slot)
-#ifndef DR_SILQ_MAXK
-#define DR_SILQ_MAXK 64
-#endif
-constexpr int kSilQMaxK = DR_SILQ_MAXK;
-#ifndef DR_SILQ_WARPS
-#define DR_SILQ_WARPS 1  // one-warp CTAs: 14 resident per SM by shared memory (C4: 4 warps 3.65 ms, 2 3.11, 1 2.87)
-#endif
-constexpr int kSilQWarps = DR_SILQ_WARPS;
+constexpr int kSilQMaxK = 64;
+constexpr int kSilQWarps = 1;  // one-warp CTAs: 14 resident per SM by shared memory (C4: 4 warps 3.65 ms, 2 3.11, 1 2.87)
 
 // pixels per chunk: 32, or fewer for large K so a chunk stays <= 512 slots
 __host__ __device__ __forceinline__ int silq_pixels(int K) { return K >= 512 ? 1 : min(32, 512 / K); }
@@ -819,12 +700,9 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
   }
 }
 
-#ifndef DR_SIL_Q
-#define DR_SIL_Q 1
-#endif
 cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
-  if (DR_SIL_Q && A.K <= kSilQMaxK) {  // (any K: chunks shrink to 512 / K pixels)
+  if (A.K <= kSilQMaxK) {  // (any K: chunks shrink to 512 / K pixels)
     const size_t smem = (size_t)kSilQWarps * silq_warp_bytes(A.K);
     cudaError_t e = cudaFuncSetAttribute(k_silhouette_backward_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
@@ -1023,10 +901,8 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
         }
         in.dz = d_zbuf;
         in.dd = d_dists;
-#if DR_BWD_PREFETCH_FV
 #pragma unroll
         for (int t = 0; t < 9; ++t) in.v[t] = __ldg(A.fv + 9 * (int64_t)fid + t);
-#endif
         double wh[3];
         slot_backward<double, true>(BA, p, fid, in, g, wh);  // the slot's clamped barycentrics come back in wh
 #pragma unroll
@@ -1073,9 +949,6 @@ __host__ __device__ __forceinline__ size_t softq_warp_bytes(int K) {
   return n * (6 * sizeof(double) + sizeof(int32_t) + sizeof(uint16_t)) + 32 * 5 * sizeof(double) + 16;
 }
 
-// kPhase: 0 = all phases in one kernel; 1 = A-C, the per-slot coefficients (what, d_dists, d_zbuf) go to
-// A.coef [S][3]; 2 = A + D reading them back (two smaller kernels: the one-kernel form is instruction-cache bound)
-template <int kPhase>
 __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
   extern __shared__ double softq_smem[];
   const int lane = threadIdx.x & 31;
@@ -1129,7 +1002,6 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
       q += __popc(m);
     }
     __syncwarp();
-    if constexpr (kPhase != 2) {
     // B: per occupied slot
     {
       double vn[9];
@@ -1234,32 +1106,6 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
       }
     }
     __syncwarp();
-    if constexpr (kPhase == 1) {  // park the coefficients of the occupied slots
-      for (int q0 = 0; q0 < q; q0 += 32) {
-        const int t = q0 + lane < q ? Q[q0 + lane] : -1;
-        if (t >= 0) {
-          double* c = A.coef + 3 * (base * K + t);
-          c[0] = WT[t];
-          c[1] = PR[t];
-          c[2] = ZI[t];
-        }
-      }
-      __syncwarp();
-      continue;
-    }
-    }  // kPhase != 2
-    if constexpr (kPhase == 2) {  // the coefficients from the first kernel
-      for (int q0 = 0; q0 < q; q0 += 32) {
-        const int t = q0 + lane < q ? Q[q0 + lane] : -1;
-        if (t >= 0) {
-          const double* c = A.coef + 3 * (base * K + t);
-          WT[t] = c[0];
-          PR[t] = c[1];
-          ZI[t] = c[2];
-        }
-      }
-      __syncwarp();
-    }
     // D: per occupied slot
     for (int q0 = 0; q0 < q; q0 += 32) {
       const int t = q0 + lane < q ? Q[q0 + lane] : -1;
@@ -1282,10 +1128,8 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
         }
         in.dz = ZI[t];
         in.dd = PR[t];
-#if DR_BWD_PREFETCH_FV
 #pragma unroll
         for (int u = 0; u < 9; ++u) in.v[u] = __ldg(A.fv + 9 * (int64_t)fid + u);
-#endif
         double g[9], wh[3];
         slot_backward<double, true>(BA, p, fid, in, g, wh);
 #pragma unroll
@@ -1314,12 +1158,6 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
   }
 }
 
-#ifndef DR_SOFT_Q
-#define DR_SOFT_Q 1
-#endif
-#ifndef DR_SOFT_SPLIT
-#define DR_SOFT_SPLIT 0  // two-kernel form for K <= 16: measured 11.6 vs 10.9 ms per-pixel (C4)
-#endif
 cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
   if (A.K > kSoftMaxK) return cudaErrorInvalidConfiguration;
@@ -1343,27 +1181,8 @@ cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
     kern<<<(unsigned)blocks, 32, smem, st>>>(args);
     return cudaGetLastError();
   };
-  if (DR_SOFT_Q && A.K > 16) return go_q(k_softmax_backward_q<0>, A);
-  if (DR_SOFT_SPLIT) {  // two kernels through a [S][3] fp64 coefficient scratch (stream-ordered allocation)
-    SoftBwdArgs B = A;
-    const size_t bytes = sizeof(double) * 3 * (size_t)A.npix * A.K;
-    {  // keep the scratch in the device's default pool between calls (the default threshold returns it to the
-       // driver at every synchronisation, and a multi-GB cudaMalloc per call costs more than the kernels)
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-    }
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&B.coef), bytes, st);
-    if (e != cudaSuccess) return e;
-    e = go_q(k_softmax_backward_q<1>, B);
-    if (e == cudaSuccess) e = go_q(k_softmax_backward_q<2>, B);
-    cudaError_t e2 = cudaFreeAsync(B.coef, st);
-    return e != cudaSuccess ? e : e2;
-  }
+  // (a two-kernel form for K <= 16, coefficients through an [S][3] scratch, measured 11.6 vs 10.9 ms per-pixel)
+  if (A.K > 16) return go_q(k_softmax_backward_q, A);
   const size_t per_warp = ((size_t)A.K * 32 * 6 + (size_t)A.K * 16) * sizeof(double);
   const int warps = (int)std::min<size_t>(kSoftThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));
   const size_t smem = per_warp * warps;
@@ -1386,14 +1205,10 @@ cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
 template <typename InT>
 static cudaError_t launch_backward_t(const BwdArgs<InT>& A, cudaStream_t st) {
   if (A.S <= 0) return cudaSuccess;
-  // many short-lived CTAs (~DR_BWD_CHUNKS_PER_WARP chunks per warp) instead of one persistent wave: the block
-  // scheduler then balances the uneven per-chunk work (occupied-slot density varies across the image); a single
-  // wave measured 10.8 of 16 achievable warps per SM on C4
-#if DR_BWD_V2
-  const int64_t per_cta = (int64_t)kBwdChunk * DR_BWD_CHUNKS_PER_CTA;
-#else
-  const int64_t per_cta = (int64_t)(kBwdThreads / 32) * kBwdChunk * DR_BWD_CHUNKS_PER_WARP;
-#endif
+  // many CTAs of kBwdChunksPerCta chunks instead of one persistent wave: the block scheduler then balances the
+  // uneven per-chunk work (occupied-slot density varies across the image); a single wave measured 10.8 of 16
+  // achievable warps per SM on C4
+  const int64_t per_cta = (int64_t)kBwdChunk * kBwdChunksPerCta;
   const int64_t blocks = std::min<int64_t>((A.S + per_cta - 1) / per_cta, INT32_MAX);
   k_backward<InT><<<(unsigned)blocks, kBwdThreads, 0, st>>>(A);
   return cudaGetLastError();

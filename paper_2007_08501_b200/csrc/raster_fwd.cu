@@ -265,28 +265,16 @@ __global__ void k_scan_last(const int* __restrict__ counts, int64_t n, int64_t* 
 // ------------------------------------------------------------------------------------------------
 // K1b: depth-order each bin list so K2 meets the nearest faces first: its K-th-depth cull then rejects most of
 // the list before the exact test. One CTA per bin: keys to shared memory, the bin's depth range, a 1024-bucket
-// counting sort (histogram, scan, scatter back in place). Measured against an exact bitonic sort of (key, id):
-// C4 sort 0.39 -> 0.18 ms with the same K2 time, C3 0.24 -> 0.04 ms; C5 (K=50) K2 +1 %. The
+// counting sort (histogram, scan, scatter back in place). Measured against the exact bitonic sort of (key, id) it
+// replaced: C4 sort 0.39 -> 0.18 ms with the same K2 time, C3 0.24 -> 0.04 ms; C5 (K=50) K2 +1 %. The
 // selection K2 makes is order-independent (strict total order, MR:138-140): the order changes only its work.
 
-__device__ __forceinline__ uint32_t float_order_bits(float x) {
-  const uint32_t u = __float_as_uint(x);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float float_from_order_bits(uint32_t u) {
-  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
-}
-
 constexpr int kSortThreads = 256;
-#ifndef DR_SORT_BUCKET
-#define DR_SORT_BUCKET 1
-#endif
-constexpr int kSortBpt = DR_SORT_BPT;                    // bucket counts per thread in the scan
 constexpr int kSortBuckets = kSortThreads * kSortBpt;
 static_assert(kSortBuckets == kSortBucketsH, "bucket count shared with the point fine stage");
 
 // MAXN = shared-memory capacity in entries; bins with (MINN, MAXN] entries are sorted by this instantiation
-template <int MAXN, int MINN, bool kDyn, bool kBucket>
+template <int MAXN, int MINN, bool kDyn>
 __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restrict__ counts,
                                                             const int64_t* __restrict__ off,
                                                             int4* __restrict__ entries,
@@ -294,11 +282,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
                                                             int64_t pool, int cap, float2* __restrict__ brange) {
   __shared__ unsigned long long s_static[kDyn ? 1 : MAXN];
   __shared__ unsigned sel_mask;
-#if 1
-  __shared__ unsigned hist[kBucket ? kSortBuckets : 1];
+  __shared__ unsigned hist[kSortBuckets];
   __shared__ unsigned wsum[kSortThreads / 32];
   __shared__ float red_lo[kSortThreads / 32], red_hi[kSortThreads / 32];
-#endif
   extern __shared__ unsigned long long s_dyn[];
   unsigned long long* s = kDyn ? s_dyn : s_static;
   // CTA b owns bins b, b + grid, b + 2 grid, ... (round robin: adjacent large bins land on different CTAs);
@@ -311,7 +297,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
       bool in = false;
       if (bin < nbins_total) {
         const int c = counts[bin];
-        in = c > MINN && c <= MAXN && bin_fits(off[bin], c, pool, cap);  // spill bins are never read as lists
+        in = c > MINN && c <= MAXN && bin_is_sorted(off[bin], c, pool, cap);  // spill bins are never read as lists
       }
       const unsigned m = __ballot_sync(0xffffffffu, in);
       if (threadIdx.x == 0) sel_mask = m;
@@ -325,7 +311,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
     const int c = counts[bin];
     const int64_t o = off[bin];
     int4* L = entries + o;
-    if constexpr (kBucket) {
     // depth-bucket order: keys in smem, bin depth range, 256 linear buckets (histogram, scan, scatter). Order
     // inside a bucket is arbitrary (K2 is order-independent); one pass of O(c) instead of O(c log^2 c).
     float lo = __int_as_float(0x7f800000), hi = -lo;
@@ -376,39 +361,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
       const int32_t f = (int32_t)(uint32_t)e;
       L[pos] = make_bin_entry(f, __uint_as_float((uint32_t)(e >> 32)), __ldg(ibbox + f));
     }
-    } else {
-    int P = 1;
-    while (P < c) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += kSortThreads) {
-      unsigned long long e = ~0ull;
-      if (i < c) {
-        const int2 fk = *reinterpret_cast<const int2*>(L + i);  // {face id, zkey bits}
-        e = ((unsigned long long)float_order_bits(__int_as_float(fk.y)) << 32) | (uint32_t)fk.x;
-      }
-      s[i] = e;
-    }
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int t = threadIdx.x; t < (P >> 1); t += kSortThreads) {
-          const int lo = 2 * t - (t & (j - 1));  // index with bit j clear
-          const int hi = lo + j;
-          const unsigned long long a = s[lo], b = s[hi];
-          const bool up = (lo & k) == 0;
-          if ((a > b) == up) {
-            s[lo] = b;
-            s[hi] = a;
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (int i = threadIdx.x; i < c; i += kSortThreads) {
-      const unsigned long long e = s[i];
-      const int32_t f = (int32_t)(uint32_t)e;
-      L[i] = make_bin_entry(f, float_from_order_bits((uint32_t)(e >> 32)), __ldg(ibbox + f));
-    }
-    }
     __syncthreads();
   }
   }
@@ -433,63 +385,26 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
 // (__match_any_sync ranks). Winners' bary / dists are recomputed with the identical operation sequence at
 // emit time (MR:178-197), so the payload carries exactly the bits the candidate test produced.
 
-#ifndef DR_RING
-#define DR_RING 48
-#endif
-#ifndef DR_FINE_MINBLOCKS
-#define DR_FINE_MINBLOCKS 0
-#endif
-#ifndef DR_COMPACT
-#define DR_COMPACT 1  // compact the pairs the K-th-depth cull leaves before evaluating them
-#endif
 constexpr int kPairQ = 64;  // < 32 pending + one enumeration step of 32
-#ifndef DR_LIST_PREFETCH
-#define DR_LIST_PREFETCH 1
-#endif
-#ifndef DR_EARLY_EXIT
-#define DR_EARLY_EXIT 0  // measured: the per-chunk exit test costs more than the chunks it skips
-#endif
-#if DR_EARLY_EXIT && DR_SORT_BUCKET
-#error "the sorted-list early exit needs an exact key order: build with -DDR_SORT_BUCKET=0 (bitonic bins)"
-#endif
-#ifndef DR_EMIT_T
-#define DR_EMIT_T 1  // fragment emit with lanes over (pixel, slot) pairs: coalesced payload stores
-#endif
-#ifndef DR_T_REFRESH
-#define DR_T_REFRESH 1
-#endif
-#ifndef DR_LEAN_STAGE
-#define DR_LEAN_STAGE 1
-#endif
-constexpr int kRing = DR_RING;  // staged faces per warp: < 32 pending + newly staged (>= 17 when 48)
-// Staged fp64 fields per face. Lean: only a, b, c, z, area are stored and the edge vectors / squared edge
-// lengths are recomputed per pair (same expressions on the same operands => same bits), trading ~15 fp64
-// ops per pair for 2x less shared memory per warp (more resident warps).
-constexpr int kNF = DR_LEAN_STAGE ? 10 : 19;
+// (measured and removed: an early exit of a depth-ordered list once its next key exceeds every pixel's K-th depth
+// — the per-chunk test cost more than the chunks it skipped and forced register spills)
+constexpr int kRing = 48;  // staged faces per warp: < 32 pending + newly staged (>= 17); 64 measured the same
+// Staged fp64 fields per face: only a, b, c, z, area are stored and the edge vectors / squared edge lengths are
+// recomputed per pair (same expressions on the same operands => same bits), trading ~15 fp64 ops per pair for 2x
+// less shared memory per warp (more resident warps) than staging all 19 invariants.
+constexpr int kNF = 10;
 
-enum : int {
-  F_AX, F_AY, F_BX, F_BY, F_CX, F_CY, F_Z0, F_Z1, F_Z2, F_AREA,
-  F_ABX, F_ABY, F_BCX, F_BCY, F_CAX, F_CAY, F_LAB, F_LBC, F_LCA
-};
+enum : int { F_AX, F_AY, F_BX, F_BY, F_CX, F_CY, F_Z0, F_Z1, F_Z2, F_AREA };
 
 // one warp's shared memory: staged-face ring (SoA) + top-K lists of its 32 pixels
-#ifndef DR_KBUF
-#define DR_KBUF 8  // shared-memory list path (K > 8)
-#endif
-#ifndef DR_KBUF_REG
-#define DR_KBUF_REG 12  // register-merge path (K <= 8)
-#endif
 // buffered candidates per pixel before the owner lane merges them into its list. Measured: 12 instead of 8 on the
 // register path (C4 k_fine 6.16 -> 6.00 ms: fewer overflow merges); on the shared-memory list path 12 costs
 // shared memory per warp (C5 6.70 -> 8.52 ms) and 6 is no better (6.74), so 8 there
-constexpr int kBufSmem = DR_KBUF, kBufReg = DR_KBUF_REG;
+constexpr int kBufSmem = 8, kBufReg = 12;
 __host__ __device__ constexpr int buf_cap(int K) { return K <= 8 ? kBufReg : kBufSmem; }
 template <int KMAX>
 constexpr int kBufT = KMAX == 0 ? kBufSmem : kBufReg;
 
-#ifndef DR_EMIT_UNROLL2
-#define DR_EMIT_UNROLL2 0
-#endif
 struct WarpSmem {
   double* d;        // [kNF][kRing]
   int32_t* fid;     // [kRing]
@@ -511,7 +426,9 @@ struct WarpSmem {
   // Measured: pixel-major pays for the shared-memory lists (K > 8, C5 k_fine 6.84 -> 6.73 ms) but not for the
   // register-merge path (C4 6.18 -> 6.21 ms), so it is used where KMAX == 0 only.
   template <bool kPM>
-  __device__ __forceinline__ int li(int s, int p) const { return kPM ? p * ls + s : s * 32 + p; }
+  __device__ __forceinline__ int li(int s, int p) const {
+    return kPM ? p * ls + s : s * 32 + p;
+  }
   // element c of pixel p's candidate buffer, [cap][32] (a pixel-major, conflict-free layout measured 0.4 %
   // slower: the index math costs more than the conflicts of same-pixel appends)
   __device__ __forceinline__ int bi(int c, int p) const { return c * 32 + p; }
@@ -527,21 +444,12 @@ struct WarpSmem {
     g.z1 = get(F_Z1, k);
     g.z2 = get(F_Z2, k);
     g.area = get(F_AREA, k);
-    if constexpr (DR_LEAN_STAGE) {
-      g.ab = g.b - g.a;
-      g.bc = g.c - g.b;
-      g.ca = g.a - g.c;
-      g.len_ab = norm2(g.ab);
-      g.len_bc = norm2(g.bc);
-      g.len_ca = norm2(g.ca);
-    } else {
-      g.ab = V2{get(F_ABX, k), get(F_ABY, k)};
-      g.bc = V2{get(F_BCX, k), get(F_BCY, k)};
-      g.ca = V2{get(F_CAX, k), get(F_CAY, k)};
-      g.len_ab = get(F_LAB, k);
-      g.len_bc = get(F_LBC, k);
-      g.len_ca = get(F_LCA, k);
-    }
+    g.ab = g.b - g.a;
+    g.bc = g.c - g.b;
+    g.ca = g.a - g.c;
+    g.len_ab = norm2(g.ab);
+    g.len_bc = norm2(g.bc);
+    g.len_ca = norm2(g.ca);
     return g;
   }
   __device__ __forceinline__ void stage(int k, const double* fv, int32_t f, uint32_t r, float key) const {
@@ -553,11 +461,6 @@ struct WarpSmem {
     put(F_AX, k, g.a.x); put(F_AY, k, g.a.y); put(F_BX, k, g.b.x); put(F_BY, k, g.b.y);
     put(F_CX, k, g.c.x); put(F_CY, k, g.c.y); put(F_Z0, k, g.z0); put(F_Z1, k, g.z1); put(F_Z2, k, g.z2);
     put(F_AREA, k, g.area);
-    if constexpr (!DR_LEAN_STAGE) {
-      put(F_ABX, k, g.ab.x); put(F_ABY, k, g.ab.y); put(F_BCX, k, g.bc.x); put(F_BCY, k, g.bc.y);
-      put(F_CAX, k, g.ca.x); put(F_CAY, k, g.ca.y);
-      put(F_LAB, k, g.len_ab); put(F_LBC, k, g.len_bc); put(F_LCA, k, g.len_ca);
-    }
     fid[k] = f;
     rect[k] = r;
     fkey[k] = key;
@@ -594,15 +497,7 @@ __device__ __forceinline__ uint32_t cover_rect(int4 ib, int i0, int j0, int vh, 
 __device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
 template <typename OutT>
-#ifndef DR_EMIT_INLINE
-#define DR_EMIT_INLINE 1
-#endif
-#if DR_EMIT_INLINE
-#define DR_EMIT_ATTR __forceinline__
-#else
-#define DR_EMIT_ATTR __noinline__
-#endif
-__device__ DR_EMIT_ATTR void emit_slot(const FineArgs<OutT>& A, int64_t slot, bool occupied, double z,
+__device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot, bool occupied, double z,
                                           int32_t fid, const double* v, double px, double py) {
   if (occupied) {
     const FaceGeom g = make_face_geom(v);
@@ -692,16 +587,9 @@ __device__ __forceinline__ void list_insert(const WarpSmem& ws, int K, int p, do
 // at once, and for K <= KMAX the list lives in registers during the merge (fully unrolled insertion: no
 // shared-memory load -> compare -> branch chain). The merge runs outside the fp64 evaluation, so these
 // registers do not add to the evaluation's pressure.
-#ifndef DR_MERGE_INLINE
-#define DR_MERGE_INLINE 1
-#endif
-#if DR_MERGE_INLINE
-#define DR_MERGE_ATTR __forceinline__
-#else
-#define DR_MERGE_ATTR __noinline__
-#endif
+// (an out-of-line merge measured slower: 11.76 vs 10.30 ms)
 template <int KMAX>
-__device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane) {
+__device__ __forceinline__ void merge_buffers(const WarpSmem& ws, int K, int lane) {
   const int n = ws.bcnt[lane];
   if (n > 0) {
     if constexpr (KMAX == 0) {
@@ -744,14 +632,6 @@ __device__ DR_MERGE_ATTR void merge_buffers(const WarpSmem& ws, int K, int lane)
   }
 }
 
-#ifndef DR_OVF_NOINLINE
-#define DR_OVF_NOINLINE 0
-#endif
-template <int KMAX>
-__device__ __noinline__ void merge_buffers_ool(const WarpSmem& ws, int K, int lane) {
-  merge_buffers<KMAX>(ws, K, lane);
-}
-
 // Append a passing candidate to its pixel's buffer (merging every buffer first if one would overflow).
 template <int KMAX, typename OutT>
 __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const WarpSmem& ws, bool pass, int p,
@@ -765,11 +645,7 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
     int base = pass ? ws.bcnt[p] : 0;
     if (__any_sync(0xffffffffu, pass && base + n_same > kBufT<KMAX>)) {
       __syncwarp();
-#if DR_OVF_NOINLINE
-      merge_buffers_ool<KMAX>(ws, K, lane);
-#else
       merge_buffers<KMAX>(ws, K, lane);
-#endif
       __syncwarp();
       base = 0;
     }
@@ -794,7 +670,7 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
 template <int KMAX, typename OutT>
 __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSmem& ws, int n, int lane) {
   const uint32_t e = lane < n ? ws.pairq[lane] : 0x80000000u;
-  const bool act = !(e >> 31);  // bit 31: culled (DR_COMPACT=0 keeps culled pairs in place)
+  const bool act = lane < n;
   bool pass = false;
   int p = 0;
   int32_t f = 0;
@@ -866,13 +742,7 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
         entry = ((uint32_t)k << 5) | (uint32_t)p;
       }
       STAT_ADD(2, __popc(__ballot_sync(0xffffffffu, act)));
-#if DR_COMPACT
       const unsigned kb = __ballot_sync(0xffffffffu, keep);
-#else
-      const unsigned kb = __ballot_sync(0xffffffffu, act);
-      if (!keep) entry |= 0x80000000u;
-      keep = act;
-#endif
       if (keep) ws.pairq[qn + __popc(kb & ((1u << lane) - 1u))] = entry;
       qn += __popc(kb);
       base += 32;
@@ -900,7 +770,7 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
 // render emit (interpolated vertex colours + softmax_blend -> image, optional pix_to_face) — separate
 // instantiations so the fragment path's code (and register allocation) does not carry them
 template <typename OutT, int NW, int KMAX, int kMode>
-__global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS : 16 / NW) k_fine(FineArgs<OutT> A) {
+__global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
@@ -946,7 +816,6 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
     // candidate faces: the bin list, or the whole mesh (naive mode / overflowed bin)
     const int64_t f0 = A.first[b], nf = A.num[b];
     const int4* list = nullptr;
-    bool sorted = false;
     int64_t nsrc = nf;
     if (A.binned) {
       const int64_t gb = (int64_t)b * nbins + bin;
@@ -955,8 +824,6 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       if (bin_fits(o, c, A.pool, A.cap)) {
         list = A.bin_entries + o;
         nsrc = c;
-        // depth-ordered list (K1b) => once the next key exceeds every pixel's K-th depth, no later face can enter
-        sorted = A.zsort && c <= kSortMaxBig;
       }
     }
     for (int s = 0; s < K; ++s) {
@@ -971,36 +838,22 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
 
     const bool valid_px = (lane >> 3) < vh && (lane & 7) < vw;
     double T = pos_inf();  // max over the micro-tile's pixels of the K-th candidate depth (+inf: a list not full)
-    int head = 0, pending = 0, groups = 0;
-#if DR_LIST_PREFETCH
+    int head = 0, pending = 0;
     // the next 32 list entries are loaded while the current ones are staged and evaluated
     int4 e_next = make_int4(-1, 0, 0, 0);
     if (list && lane < nsrc) e_next = list[lane];
-#endif
     for (int64_t c0 = 0; c0 < nsrc; c0 += 32) {
       const int64_t ci = c0 + lane;
       uint32_t r = 0u;
       int32_t fid = -1;
       float key = 0.f;
-#if DR_LIST_PREFETCH
       const int4 e_cur = e_next;
       if (list && ci + 32 < nsrc) e_next = list[ci + 32];
-      if (DR_EARLY_EXIT && sorted && (double)__int_as_float(__shfl_sync(0xffffffffu, e_cur.y, 0)) > T) {
-#else
-      if (sorted && (double)__int_as_float(list[c0].y) > T) {
-#endif
-        STAT_ADD(6, 1);
-        break;
-      }
       STAT_ADD(0, __popc(__ballot_sync(0xffffffffu, ci < nsrc)));
       if (ci < nsrc) {
         int4 ib;
         if (list) {
-#if DR_LIST_PREFETCH
           const int4 e = e_cur;
-#else
-          const int4 e = list[ci];
-#endif
           fid = e.x;
           key = __int_as_float(e.y);
           ib = entry_ibbox(e);
@@ -1033,14 +886,9 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
           ran = true;
         }
         if (ran) {  // merge the buffered candidates (the only merge site besides a buffer overflow), refresh T
-#if DR_T_REFRESH > 1
-          if (++groups % DR_T_REFRESH == 0 || (last && todo == 0u))
-#endif
-          {
-            __syncwarp();
-            merge_buffers<KMAX>(ws, K, lane);
-            __syncwarp();
-          }
+          __syncwarp();
+          merge_buffers<KMAX>(ws, K, lane);
+          __syncwarp();
           if (A.zsort) {  // max of the K-th depths (the list tails alone are a valid, looser threshold)
             double t = valid_px ? ws.tz[ws.li<(KMAX == 0)>(K - 1, lane)] : -pos_inf();
 #pragma unroll
@@ -1050,19 +898,8 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
         }
       } while (todo);
     }
-#if DR_EARLY_EXIT
-    while (pending > 0) {  // faces staged before an early exit
-      const int G = min(pending, 32);
-      process_group<KMAX>(A, ws, head, G, lane);
-      head = (head + G) % kRing;
-      pending -= G;
-    }
-    __syncwarp();
-    merge_buffers<KMAX>(ws, K, lane);
-#endif
     // every group's candidates were merged after it ran: the buffers are empty here
     __syncwarp();
-#if DR_EMIT_T
     if constexpr (kMode == 0) {
       // fragment payload (MR:178-197), lanes over (pixel, slot) in output order: q = (row * 8 + col) * K + s, so
       // one step writes whole runs of consecutive slots of a micro-tile row (coalesced stores); the next step's
@@ -1088,9 +925,6 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       double vn[9], zn = 0.0, xn = 0.0, yn = 0.0;
       int64_t sn;
       fetch(lane, fn, vn, sn, zn, xn, yn);
-#if DR_EMIT_UNROLL2
-#pragma unroll 2
-#endif
       for (int q0 = 0; q0 < 32 * K; q0 += 32) {
         const int32_t f = fn;
         const int64_t slot = sn;
@@ -1104,7 +938,6 @@ __global__ void __launch_bounds__(NW * 32, DR_FINE_MINBLOCKS ? DR_FINE_MINBLOCKS
       __syncwarp();
       continue;
     }
-#endif
     // emit this lane's pixel (MR:178-197); the next occupied slot's face_verts are fetched before the current
     // slot is evaluated so the global-load latency overlaps the fp64 work
     const int row = lane >> 3, col = lane & 7;
@@ -1215,27 +1048,18 @@ void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* nu
                                                           const_cast<int*>(counts), off, cursor, pool, zkey, entries);
 }
 
-bool sort_uses_buckets(bool exact) { return DR_SORT_BUCKET && !exact; }
-
 cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entries, const int4* ibbox,
-                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st, bool exact,
-                             float2* bin_range) {
+                             int64_t nbins_total, int64_t pool, int cap, cudaStream_t st, float2* bin_range) {
   if (nbins_total <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nbins_total, 148 * 16);
-  const bool bucket = DR_SORT_BUCKET && !exact;
-  if (bucket)
-    k_sort_bins<kSortMax, 0, false, true><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total,
-                                                                        pool, cap, bin_range);
-  else
-    k_sort_bins<kSortMax, 0, false, false><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total,
-                                                                         pool, cap, nullptr);
-  auto big = bucket ? k_sort_bins<kSortMaxBig, kSortMax, true, true> : k_sort_bins<kSortMaxBig, kSortMax, true, false>;
+  k_sort_bins<kSortMax, 0, false><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total, pool, cap,
+                                                                 bin_range);
+  auto big = k_sort_bins<kSortMaxBig, kSortMax, true>;
   const int smem = kSortMaxBig * (int)sizeof(unsigned long long);
   cudaError_t e = cudaFuncSetAttribute(big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   big<<<(unsigned)std::min<int64_t>(nbins_total, 148), kSortThreads, smem, st>>>(counts, off, entries, ibbox,
-                                                                                  nbins_total, pool, cap,
-                                                                                  bucket ? bin_range : nullptr);
+                                                                                  nbins_total, pool, cap, bin_range);
   return cudaGetLastError();
 }
 

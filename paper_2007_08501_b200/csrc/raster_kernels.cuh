@@ -101,6 +101,7 @@ template <typename OutT>
 struct PointFineArgs {  // rasterize_points (point_render.cpp:105-155)
   const double* pts;
   const int4* ibbox;
+  const float* zkey;        // [P] +inf: culled by prepare_points (PR:17-31), else <= the point's depth
   const int64_t* first;
   const int64_t* num;
   const int* bin_counts;
@@ -141,7 +142,6 @@ struct SoftBwdArgs {
   bool persp, clip;
   double blur, znear;      // raster settings (exact re-evaluation of each slot)
   BlendArgs blend;
-  double* coef = nullptr;  // [S][3] per-slot (what, d_dists, d_zbuf) scratch of the two-kernel form
 };
 cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st);
 
@@ -173,8 +173,6 @@ cudaError_t launch_packed_to_padded(const void* packed, const int64_t* first, co
                                     cudaStream_t st);
 cudaError_t launch_padded_to_packed(const void* padded, const int64_t* first, const int64_t* num, int64_t N,
                                     int64_t max_count, int64_t row_bytes, void* packed, cudaStream_t st);
-cudaError_t launch_gather_occupied(const int64_t* p2f, int64_t S, const float* dz_src, const float* db_src,
-                                   const float* dd_src, float* dz, float* db, float* dd, cudaStream_t st);
 cudaError_t launch_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
                                    cudaStream_t st);
 
@@ -192,12 +190,16 @@ void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cuda
 void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
                       int bs, int nbx, int nby, const int* counts, const int64_t* off, int* cursor, int64_t pool,
                       const float* zkey, int4* entries, cudaStream_t st);
-// Depth-bucket order of a bin (k_sort_bins, bucket mode): keys [lo, hi] map linearly onto kSortBucketsH buckets.
+// The bins k_sort_bins depth-orders: every non-empty bin of at most kSortMaxBig entries that is read as a list.
+// The fine stages treat exactly these bins as sorted (the point stage reads their bucket map for its exit bound),
+// so the sort and both fine stages share this one predicate.
+__host__ __device__ __forceinline__ bool bin_is_sorted(int64_t off, int cnt, int64_t pool, int cap) {
+  return cnt > 0 && cnt <= kSortMaxBig && bin_fits(off, cnt, pool, cap);
+}
+// Depth-bucket order of a bin (k_sort_bins): keys [lo, hi] map linearly onto kSortBucketsH buckets.
 // Shared with the point fine stage, which bounds the keys of the rest of a bin from the bucket of its next entry.
-#ifndef DR_SORT_BPT
-#define DR_SORT_BPT 4
-#endif
-constexpr int kSortBucketsH = 256 * DR_SORT_BPT;
+constexpr int kSortBpt = 4;  // bucket counts per thread of the sort's scan (256 threads)
+constexpr int kSortBucketsH = 256 * kSortBpt;
 __device__ __forceinline__ float sort_bucket_scale(float lo, float hi) {
   return hi > lo ? (float)kSortBucketsH * 0.99999f / (hi - lo) : 0.f;
 }
@@ -205,10 +207,9 @@ __device__ __forceinline__ int sort_bucket(float key, float lo, float scale) {
   return min(kSortBucketsH - 1, max(0, __float2int_rz((key - lo) * scale)));  // NaN/inf range -> bucket 0
 }
 
-bool sort_uses_buckets(bool exact);
 cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entries, const int4* ibbox,
                              int64_t nbins_total, int64_t pool, int cap, cudaStream_t st,
-                             bool exact = false, float2* bin_range = nullptr);
+                             float2* bin_range = nullptr);
 cudaError_t launch_fine(const FineArgs<float>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st);
 cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st);

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
       if (bin_fits(o, c, A.pool, 0)) {
         list = A.bin_entries + o;
         nsrc = c;
-        sorted = A.sorted && c <= kSortMaxBig;  // longer bins stay unsorted (k_sort_bins)
+        sorted = A.sorted && bin_is_sorted(o, c, A.pool, 0);  // longer bins stay unsorted (k_sort_bins)
       }
     }
     int n = 0;  // candidates held (generic path)
@@ -163,9 +163,9 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
     }
     for (int64_t c0 = 0; c0 < nsrc; c0 += kPtThreads) {
       // depth-ordered bin: once every pixel of the block holds K points nearer than a lower bound of every
-      // remaining depth key, no later point can enter any list (strict (z, id) order, PR:37). Exact order: the
-      // next key itself; bucket order: the lower edge of the bucket two below the next entry's (rounding in the
-      // float bucket map stays under one bucket width)
+      // remaining depth key, no later point can enter any list (strict (z, id) order, PR:37). The bound is the
+      // lower edge of the bucket two below the next entry's (rounding in the float bucket map stays under one
+      // bucket width); the sort wrote this bin's bucket map because bin_is_sorted holds for it
       if (sorted) {
         double kth = -__longlong_as_double(0x7ff0000000000000LL);
         if (valid) {
@@ -179,13 +179,12 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
         double T = s_kth[0];
         for (int w = 1; w < kPtThreads / 32; ++w) T = fmax(T, s_kth[w]);
         const float key = __int_as_float(list[c0].y);
-        double bound = (double)key;
-        if (A.brange) {  // the sort's bucket map (lo, scale) of this bin, loaded here: nothing stays live
-          const float2 br = A.brange[(int64_t)b * nbins + bin];
-          const int bk = sort_bucket(key, br.x, br.y);
-          // lo + (bk - 2) / scale with both roundings downward: a lower bound of every key in buckets >= bk
-          bound = br.y > 0.f && bk >= 2 ? (double)__fadd_rd(br.x, __fdiv_rd((float)(bk - 2), br.y)) : (double)br.x;
-        }
+        // the sort's bucket map (lo, scale) of this bin, loaded here: nothing stays live
+        const float2 br = A.brange[(int64_t)b * nbins + bin];
+        const int bk = sort_bucket(key, br.x, br.y);
+        // lo + (bk - 2) / scale with both roundings downward: a lower bound of every key in buckets >= bk
+        const double bound =
+            br.y > 0.f && bk >= 2 ? (double)__fadd_rd(br.x, __fdiv_rd((float)(bk - 2), br.y)) : (double)br.x;
         if (bound > T) break;
       }
       __syncthreads();
@@ -197,8 +196,13 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
           pid = list[ci].x;
         } else {
           pid = (int32_t)(p0 + ci);
-          const int4 ib = A.ibbox[pid];
-          live = ib.x <= ib.y;  // culled by prepare_points
+          if (A.binned) {  // spilled bin: the point must pass this tile's inflated bounds test (PR:133-134)
+            const int4 ib = A.ibbox[pid];  // kept tiles as pixel ranges (multiples of bs)
+            const int ti = by * A.bs, tj = bx * A.bs;
+            live = ib.x <= ti && ti <= ib.y && ib.z <= tj && tj <= ib.w;
+          } else {  // rasterize_points_naive has no tile test: prepare_points liveness only (PR:17-31, 82-103)
+            live = A.zkey[pid] != __int_as_float(0x7f800000);
+          }
         }
         sx[threadIdx.x] = A.pts[3 * (int64_t)pid];
         sy[threadIdx.x] = A.pts[3 * (int64_t)pid + 1];

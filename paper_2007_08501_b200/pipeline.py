@@ -16,8 +16,6 @@ global and each group's backward writes only its own rows of grad_face_verts (in
 """
 from __future__ import annotations
 
-import ctypes as C
-
 import numpy as np
 import torch
 
@@ -56,8 +54,7 @@ class HostPipeline:
     """Streams forward (+ backward) of a fixed batch layout between pinned host buffers and the GPU."""
 
     def __init__(self, first, num, settings: RasterSettings, num_faces: int, device, n_groups: int = 8,
-                 backward: bool = True, ramp: int = 2, lookahead: int = 3, zero_copy: bool = False,
-                 gather: bool = False):
+                 backward: bool = True, ramp: int = 2, lookahead: int = 3):
         self.first = np.asarray(first, dtype=np.int64)
         self.num = np.asarray(num, dtype=np.int64)
         order = np.argsort(self.first, kind="stable")
@@ -69,13 +66,7 @@ class HostPipeline:
         self.dev = torch.device(device)
         self.backward = backward
         self.lookahead = int(lookahead)  # 0: every H2D enqueued at once
-        # zero_copy: the backward reads the (page-locked) host cotangents in place, only at occupied slots,
         # instead of an H2D copy of every slot's cotangents
-        self.zero_copy = bool(zero_copy)
-        # gather: a device kernel pulls only the occupied slots' cotangents from the page-locked host arrays
-        # (dr_gather_occupied_cotangents) on its own stream, and the backward of group g runs after the forward
-        # of group g + 1 so the gather overlaps compute
-        self.gather = bool(gather) and not self.zero_copy and backward
         H, W = settings.hw
         K = settings.faces_per_pixel
         # groups balance PCIe bytes (the e2e bound), not faces: a mesh's slots cost as much as ~0.5M faces
@@ -87,17 +78,16 @@ class HostPipeline:
         self.bary = torch.empty((self.N, H, W, K, 3), dtype=torch.float32, device=d)
         self.dists = torch.empty((self.N, H, W, K), dtype=torch.float32, device=d)
         if backward:
-            if not zero_copy:
-                self.dz = torch.empty_like(self.zbuf)
-                self.db = torch.empty_like(self.bary)
-                self.dd = torch.empty_like(self.dists)
+            self.dz = torch.empty_like(self.zbuf)
+            self.db = torch.empty_like(self.bary)
+            self.dd = torch.empty_like(self.dists)
             self.grad = torch.zeros((self.F, 3, 3), dtype=torch.float64, device=d)
         ws = max(workspace_bytes(g1 - g0, self.F, settings) for g0, g1 in self.groups)
         self.ws = torch.empty(ws, dtype=torch.uint8, device=d)
         self.g_first = [torch.as_tensor(self.first[g0:g1], device=d) for g0, g1 in self.groups]
         self.g_num = [torch.as_tensor(self.num[g0:g1], device=d) for g0, g1 in self.groups]
         self.g_host = [(self.first[g0:g1].copy(), self.num[g0:g1].copy()) for g0, g1 in self.groups]
-        self.h2d, self.comp, self.d2h, self.gat = (torch.cuda.Stream(device=d) for _ in range(4))
+        self.h2d, self.comp, self.d2h = (torch.cuda.Stream(device=d) for _ in range(3))
 
     def face_range(self, g0, g1):
         lo = int(self.first[g0])
@@ -107,8 +97,6 @@ class HostPipeline:
     def run(self, fv_h, out_h, cot_h=None, grad_h=None):
         """fv_h [F,3,3] f64 pinned; out_h = (p2f, zbuf, bary, dists) pinned host tensors; cot_h = (dz, db, dd)
         pinned fp32; grad_h [F,3,3] f64 pinned. Enqueues everything; the caller synchronises."""
-        if self.gather:
-            return self._run_gather(fv_h, out_h, cot_h, grad_h)
         main = torch.cuda.current_stream(self.dev)
         for st in (self.h2d, self.comp, self.d2h):
             st.wait_stream(main)
@@ -124,7 +112,7 @@ class HostPipeline:
                 self.h2d.wait_event(ev_d2h[gi - self.lookahead])
             with torch.cuda.stream(self.h2d):
                 self.fv[lo:hi].copy_(fv_h[lo:hi], non_blocking=True)
-                if self.backward and not self.zero_copy:
+                if self.backward:
                     for d, h in zip((self.dz, self.db, self.dd), cot_h):
                         d[g0:g1].copy_(h[g0:g1], non_blocking=True)
                 ev_in = torch.cuda.Event()
@@ -137,10 +125,9 @@ class HostPipeline:
                 ev_fwd = torch.cuda.Event()
                 ev_fwd.record(self.comp)
                 if self.backward:
-                    cz, cb, cd = ((c[g0:g1] for c in cot_h) if self.zero_copy
-                                  else (self.dz[g0:g1], self.db[g0:g1], self.dd[g0:g1]))
                     rasterize_meshes_backward(self.fv, self.g_first[gi], self.g_num[gi], self.s, outs[0], outs[2],
-                                              cz, cb, cd, out=self.grad, host_ranges=self.g_host[gi])
+                                              self.dz[g0:g1], self.db[g0:g1], self.dd[g0:g1], out=self.grad,
+                                              host_ranges=self.g_host[gi])
                 ev_out = torch.cuda.Event()
                 ev_out.record(self.comp)
             self.d2h.wait_event(ev_fwd)
@@ -155,74 +142,4 @@ class HostPipeline:
             ev.record(self.d2h)
             ev_d2h.append(ev)
         for st in (self.h2d, self.comp, self.d2h):
-            main.wait_stream(st)
-
-    def _run_gather(self, fv_h, out_h, cot_h, grad_h):
-        from . import _lib
-        from .raster import _check, _ptr
-
-        L = _lib.load()
-        main = torch.cuda.current_stream(self.dev)
-        streams = (self.h2d, self.comp, self.d2h, self.gat)
-        for st in streams:
-            st.wait_stream(main)
-        H, W = self.s.hw
-        K = self.s.faces_per_pixel
-        per_mesh = H * W * K
-        ev_d2h, ev_gat, outs_of = [], [], []
-
-        def backward(gj):
-            g0, g1 = self.groups[gj]
-            lo, hi = self.face_range(g0, g1)
-            self.comp.wait_event(ev_gat[gj])
-            with torch.cuda.stream(self.comp):
-                outs = outs_of[gj]
-                rasterize_meshes_backward(self.fv, self.g_first[gj], self.g_num[gj], self.s, outs[0], outs[2],
-                                          self.dz[g0:g1], self.db[g0:g1], self.dd[g0:g1], out=self.grad,
-                                          host_ranges=self.g_host[gj])
-                ev = torch.cuda.Event()
-                ev.record(self.comp)
-            self.d2h.wait_event(ev)
-            with torch.cuda.stream(self.d2h):
-                grad_h[lo:hi].copy_(self.grad[lo:hi], non_blocking=True)
-
-        for gi, (g0, g1) in enumerate(self.groups):
-            lo, hi = self.face_range(g0, g1)
-            if self.lookahead > 0 and gi >= self.lookahead:
-                self.h2d.wait_event(ev_d2h[gi - self.lookahead])
-            with torch.cuda.stream(self.h2d):
-                self.fv[lo:hi].copy_(fv_h[lo:hi], non_blocking=True)
-                ev_in = torch.cuda.Event()
-                ev_in.record(self.h2d)
-            self.comp.wait_event(ev_in)
-            with torch.cuda.stream(self.comp):
-                outs = (self.p2f[g0:g1], self.zbuf[g0:g1], self.bary[g0:g1], self.dists[g0:g1])
-                rasterize_meshes(self.fv, self.g_first[gi], self.g_num[gi], self.s, workspace=self.ws, out=outs,
-                                 host_ranges=self.g_host[gi])
-                ev_fwd = torch.cuda.Event()
-                ev_fwd.record(self.comp)
-            outs_of.append(outs)
-            self.gat.wait_event(ev_fwd)
-            with torch.cuda.stream(self.gat):
-                S = (g1 - g0) * per_mesh
-                rc = L.dr_gather_occupied_cotangents(
-                    _ptr(self.p2f[g0:g1]), S, _ptr(cot_h[0][g0:g1]), _ptr(cot_h[1][g0:g1]), _ptr(cot_h[2][g0:g1]),
-                    _ptr(self.dz[g0:g1]), _ptr(self.db[g0:g1]), _ptr(self.dd[g0:g1]),
-                    C.c_void_p(self.gat.cuda_stream))
-                _check(rc, "gather_occupied_cotangents")
-                ev = torch.cuda.Event()
-                ev.record(self.gat)
-                ev_gat.append(ev)
-            self.d2h.wait_event(ev_fwd)
-            with torch.cuda.stream(self.d2h):
-                for h, d in zip(out_h, outs):
-                    h[g0:g1].copy_(d, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(self.d2h)
-                ev_d2h.append(ev)
-            if gi >= 1:
-                backward(gi - 1)  # after this group's forward: the gather of gi - 1 overlapped it
-        if self.groups:
-            backward(len(self.groups) - 1)
-        for st in streams:
             main.wait_stream(st)

@@ -383,10 +383,8 @@ def test_div_free_paths_and_rerun_backward_tolerance(cuda, oracle):
     assert rel_err(got, want) < 1e-12
 
 
-@pytest.mark.parametrize("zero_copy,gather", [(False, False), (True, False), (False, True)])
-def test_host_pipeline_matches_device_calls(cuda, zero_copy, gather):
-    """HostPipeline (pinned host in/out, mesh groups streamed over 3 CUDA streams) == plain device calls; with
-    zero_copy the backward reads the pinned host cotangents in place."""
+def test_host_pipeline_matches_device_calls(cuda):
+    """HostPipeline (pinned host in/out, mesh groups streamed over 3 CUDA streams) == plain device calls."""
     from paper_2007_08501_b200 import rasterize_meshes, rasterize_meshes_backward
     from paper_2007_08501_b200.pipeline import HostPipeline
 
@@ -397,7 +395,7 @@ def test_host_pipeline_matches_device_calls(cuda, zero_copy, gather):
     g = np.random.default_rng(3)
     cot = [torch.as_tensor(g.standard_normal(s), dtype=torch.float32) for s in
            ((N, 128, 128, 8), (N, 128, 128, 8, 3), (N, 128, 128, 8))]
-    pipe = HostPipeline(first, num, rs, F, cuda, n_groups=3, zero_copy=zero_copy, gather=gather)
+    pipe = HostPipeline(first, num, rs, F, cuda, n_groups=3)
     out_h = (torch.empty((N, 128, 128, 8), dtype=torch.int64).pin_memory(),
              torch.empty((N, 128, 128, 8), dtype=torch.float32).pin_memory(),
              torch.empty((N, 128, 128, 8, 3), dtype=torch.float32).pin_memory(),
@@ -415,8 +413,9 @@ def test_host_pipeline_matches_device_calls(cuda, zero_copy, gather):
     assert rel_err(grad_h.numpy(), gref.cpu().numpy()) < 1e-12
 
 
-def test_backward_rejects_pageable_host_cotangents(cuda):
-    """Cotangents in pageable host memory would fault in the kernel: the C-ABI rejects them (DR_ERR_USAGE)."""
+def test_backward_rejects_host_cotangents(cuda):
+    """Cotangents in host memory (pageable: would fault; page-locked: read over PCIe, measured slower than copying)
+    are rejected by the C-ABI (DR_ERR_USAGE)."""
     from paper_2007_08501_b200 import UsageError, rasterize_meshes, rasterize_meshes_backward
 
     m, cam = S.ico_sphere(1), S.bench_camera()
@@ -424,9 +423,11 @@ def test_backward_rejects_pageable_host_cotangents(cuda):
     rs = raster_settings(32, 2, 1e-4, cam)
     fvd, fd, nd = (torch.as_tensor(x, device=cuda) for x in (fv, first, num))
     p2f, zbuf, bary, dists = rasterize_meshes(fvd, fd, nd, rs)
-    with pytest.raises(UsageError):
-        rasterize_meshes_backward(fvd, fd, nd, rs, p2f, bary, torch.zeros(tuple(zbuf.shape)),
-                                  torch.zeros(tuple(bary.shape)), torch.zeros(tuple(dists.shape)))
+    for pin in (False, True):
+        mk = (lambda s: torch.zeros(s).pin_memory()) if pin else torch.zeros  # noqa: E731
+        with pytest.raises(UsageError):
+            rasterize_meshes_backward(fvd, fd, nd, rs, p2f, bary, mk(tuple(zbuf.shape)), mk(tuple(bary.shape)),
+                                      mk(tuple(dists.shape)))
 
 
 def test_grouped_exact_division_is_ieee(cuda):

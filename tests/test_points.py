@@ -101,10 +101,12 @@ def test_points_large_k_and_dense_cloud(oracle, cuda):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("K", [1, 4])
-def test_points_early_exit_needs_exact_bin_order(oracle, cuda, K):
-    """Bins of thousands of points whose depths all fall in a sliver (one depth bucket): the point fine stage stops
-    streaming a bin at the first key above every pixel's K-th depth, which is only valid on an exactly ordered bin
-    (a bucket order leaves nearer points after the first key of a chunk)."""
+def test_points_early_exit_bucket_bound(oracle, cuda, K):
+    """Bins of thousands of points whose depths all fall in a sliver (one depth bucket of the bins' 1024-bucket
+    order): the point fine stage stops streaming a bin once a lower bound of every remaining key exceeds every
+    pixel's K-th depth. In bucket order the next key itself is NOT such a bound (nearer points of the same bucket
+    can follow it); the stage uses the lower edge of the bucket two below the next entry's, from the (lo, scale)
+    bucket map the sort wrote for the bin. Exiting at the next key fails this scene."""
     from paper_2007_08501_b200 import rasterize_points
 
     rng = np.random.default_rng(11)

@@ -82,7 +82,9 @@ def test_fused_silhouette_forward_and_backward(name, H, K, blur, flags, oracle, 
                                       torch.as_tensor(da, device=cuda)).cpu().numpy()
     assert np.abs(g_want).max() > 0
     assert rel_err(g, g_want) < GRAD_RTOL, f"{name}: grad rel err {rel_err(g, g_want):.2e}"
-    grad_close(g, g_want, name)
+    # per element: the fp32-cotangent path evaluates the opacity sigmoid with fp32 exp (raster_bwd.cu), ~1e-7
+    # relative per slot contribution, so the absolute term is 1e-6 of the largest gradient here (1e-8 for K3)
+    grad_close(g, g_want, name, atol_scale=1e-6)
     assert np.all(g[..., 2] == 0.0)  # d_zbuf = d_bary = 0: no depth gradient
 
 
