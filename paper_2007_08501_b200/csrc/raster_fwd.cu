@@ -642,7 +642,10 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
     const unsigned peers = __match_any_sync(0xffffffffu, pass ? p : 32 + lane);
     const int rank = __popc(peers & ((1u << lane) - 1u));
     const int n_same = __popc(peers);
-    int base = pass ? ws.bcnt[p] : 0;
+    // only the group's leader (rank 0) reads and writes the pixel's count: no lane reads a word another lane of
+    // the warp writes in the same step (racecheck-clean without an extra __syncwarp)
+    int base = pass && rank == 0 ? ws.bcnt[p] : 0;
+    base = __shfl_sync(0xffffffffu, base, __ffs(peers) - 1);
     if (__any_sync(0xffffffffu, pass && base + n_same > kBufT<KMAX>)) {
       __syncwarp();
       merge_buffers<KMAX>(ws, K, lane);
