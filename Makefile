@@ -7,13 +7,17 @@ ARCH = -gencode arch=compute_100a,code=sm_100a
 NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v
 PKG = paper_2007_08501_b200
 SRCS = $(PKG)/csrc/raster_fwd.cu $(PKG)/csrc/raster_bwd.cu $(PKG)/csrc/raster_camera.cu $(PKG)/csrc/capi.cu \
-       $(PKG)/csrc/adaptor.cu $(PKG)/csrc/batching.cu $(PKG)/csrc/raster_points.cu $(PKG)/csrc/selftest.cu
+       $(PKG)/csrc/adaptor.cu $(PKG)/csrc/batching.cu $(PKG)/csrc/raster_points.cu $(PKG)/csrc/selftest.cu \
+       $(PKG)/csrc/shard.cu
 HDRS = $(PKG)/csrc/raster_math.cuh $(PKG)/csrc/raster_kernels.cuh include/dr_raster.h include/dr_b200/mesh_raster.hpp \
-       include/dr_b200/point_render.hpp include/dr_b200/shading.hpp
+       include/dr_b200/point_render.hpp include/dr_b200/shading.hpp include/dr_shard.h
 LIB = $(PKG)/libdr_raster_b200.so
 OBJS = $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 
-all: $(LIB) oracle cpptest
+# NCCL executor of the mesh-shard gather (include/dr_shard.h): a separate library so the rasterizer does not link NCCL
+SHARDLIB = $(PKG)/libdr_shard_b200.so
+
+all: $(LIB) $(SHARDLIB) oracle cpptest
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build
@@ -21,6 +25,12 @@ build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+$(SHARDLIB): $(PKG)/csrc/shard_nccl.cu include/dr_shard.h include/dr_raster.h $(LIB)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o build/shard_nccl.o 2> build/shard_nccl.ptxas.txt || (cat build/shard_nccl.ptxas.txt; false)
+	$(NVCC) $(ARCH) -shared -o $@ build/shard_nccl.o -L$(PKG) -ldr_raster_b200 -lnccl -lcudart \
+	  -Xlinker -rpath -Xlinker '$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle liboracle.so
@@ -36,6 +46,6 @@ cpptest: $(LIB) oracle
 	fi
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(SHARDLIB)
 
 .PHONY: all oracle cpptest clean

@@ -53,16 +53,14 @@ def parse():
     ap.add_argument("--cpu-runs", type=int, default=3, help="CPU baseline runs (median reported)")
     ap.add_argument("--cpu-sample-faces-1t", type=float, default=0.03,
                     help="fraction of the batch's faces the 1-thread CPU figure covers")
+    ap.add_argument("--gather", type=int, default=0,
+                    help="N>1: 1 = the timed step also gathers every mesh's fragments and grad_face_verts rows to "
+                         "rank 0 over NCCL (pipelined); the line reports the other mode under 'gather_mode'")
+    ap.add_argument("--gather-groups", type=int, default=4, help="pipeline groups of the gather (local meshes)")
     ap.add_argument("--like-for-like", type=int, default=1,
                     help="1: also time the GPU at reference semantics (flags off) on the whole batch and on the "
                          "CPU sample")
     return ap.parse_args()
-
-
-def lpt_shards(face_counts, world):
-    from paper_2007_08501_b200.shard import lpt_partition
-
-    return lpt_partition(face_counts, world)
 
 
 def config_settings(cfg):
@@ -386,60 +384,120 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
 
-    shards = lpt_shards(meshes_all.num_faces_per_mesh(), world)
-    my = subset(meshes_all, shards[rank])
+    # mesh sharding (include/dr_shard.h): every rank holds the whole packed face_verts and rasterizes ITS meshes
+    # (LPT by face count) through their GLOBAL face ranges: global face ids, its own rows of grad_face_verts, no
+    # collective on the data path
+    from paper_2007_08501_b200.shard import ShardPlan
+
+    plan = ShardPlan(meshes_all.num_faces_per_mesh(), world)
+    mine = plan.meshes(rank)
     cam = S.bench_camera()
     rs = config_settings(cfg)
-    fv_np = S.face_verts(my, cam)
-    first_np, num_np = my.mesh_to_face_first_idx(), my.num_faces_per_mesh()
-    N, F = len(num_np), len(fv_np)
+    fv_all = S.face_verts(meshes_all, cam)
+    first_all, num_all = meshes_all.mesh_to_face_first_idx(), meshes_all.num_faces_per_mesh()
+    first_np, num_np = first_all[mine], num_all[mine]
+    N, F, F_all = len(num_np), int(num_np.sum()), len(fv_all)
+    N_all = len(num_all)
     K = c["K"]
     S_ = N * H * W * K
-    fv = torch.as_tensor(fv_np, device=dev)
+    fv = torch.as_tensor(fv_all, device=dev)
     first = torch.as_tensor(first_np, device=dev)
     num = torch.as_tensor(num_np, device=dev)
-    ws = torch.empty(workspace_bytes(N, F, rs), dtype=torch.uint8, device=dev)
+    ws = torch.empty(workspace_bytes(N, F_all, rs), dtype=torch.uint8, device=dev) if N else None
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     dz = torch.randn((N, H, W, K), generator=gen, device=dev)
     db = torch.randn((N, H, W, K, 3), generator=gen, device=dev)
     dd = torch.randn((N, H, W, K), generator=gen, device=dev)
+    p2f_l = torch.empty((N, H, W, K), dtype=torch.int64, device=dev)
+    zb_l, di_l = (torch.empty((N, H, W, K), dtype=torch.float32, device=dev) for _ in range(2))
+    ba_l = torch.empty((N, H, W, K, 3), dtype=torch.float32, device=dev)
+    grad_l = torch.zeros((F_all, 3, 3), dtype=torch.float64, device=dev)
 
-    host_ranges = (first_np, num_np)  # host copies of the mesh ranges: the calls never synchronise the stream
+    # optional gather of every mesh's fragments + grad_face_verts rows to rank 0 (NCCL over NVLink,
+    # libdr_shard_b200.so), pipelined: the local meshes run in groups and each group's gather runs on a side stream
+    # while the next group computes
+    gather = None
+    n_groups = max(1, min(args.gather_groups, int(plan.local_index.max()) + 1 if N_all else 1))
+    gsize = -(-(int(plan.local_index.max()) + 1) // n_groups) if N_all else 1
+    glob = None
+    if world > 1:
+        from paper_2007_08501_b200.shard import NcclGather
 
-    def step():
-        p2f, zbuf, bary, dists = rasterize_meshes(fv, first, num, rs, workspace=ws, host_ranges=host_ranges)
-        grad = None
+        gather = NcclGather(rank, world)
+        comm_st = torch.cuda.Stream(device=dev)
+        if rank == 0:
+            glob = {"pix_to_face": torch.empty((N_all, H, W, K), dtype=torch.int64, device=dev),
+                    "zbuf": torch.empty((N_all, H, W, K), dtype=torch.float32, device=dev),
+                    "bary": torch.empty((N_all, H, W, K, 3), dtype=torch.float32, device=dev),
+                    "dists": torch.empty((N_all, H, W, K), dtype=torch.float32, device=dev),
+                    "grad_face_verts": grad_l}  # the root's own rows are already in place (copy skipped)
+    local_bufs = {"pix_to_face": p2f_l, "zbuf": zb_l, "bary": ba_l, "dists": di_l, "grad_face_verts": grad_l}
+
+    def run_group(lo, hi):
+        hr = (first_np[lo:hi], num_np[lo:hi])  # host copies of the ranges: the calls never synchronise the stream
+        fr, nm = first[lo:hi], num[lo:hi]
+        outs = (p2f_l[lo:hi], zb_l[lo:hi], ba_l[lo:hi], di_l[lo:hi])
+        rasterize_meshes(fv, fr, nm, rs, workspace=ws, out=outs, host_ranges=hr)
         if c["backward"]:
-            grad = rasterize_meshes_backward(fv, first, num, rs, p2f, bary, dz, db, dd, host_ranges=host_ranges)
-        return p2f, grad
+            rasterize_meshes_backward(fv, fr, nm, rs, outs[0], outs[2], dz[lo:hi], db[lo:hi], dd[lo:hi], out=grad_l,
+                                      host_ranges=hr)
+
+    def step(with_gather=False):
+        if not with_gather:
+            if N:
+                run_group(0, N)
+            return
+        st_main = torch.cuda.current_stream()
+        for lo in range(0, gsize * n_groups, gsize):
+            hi = min(lo + gsize, N)
+            if lo < hi:
+                run_group(lo, hi)
+            ev = torch.cuda.Event()
+            ev.record(st_main)
+            comm_st.wait_event(ev)
+            gather.gather(plan, first_all, num_all, H * W * K, 4, c["backward"], local_bufs, glob, comm_st,
+                          local_lo=lo, local_hi=lo + gsize)
+        st_main.wait_stream(comm_st)
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_launch0 = launch_count()
-    with ClockSampler(local) as clk, KernelTimer() as kt:
+    def timed(with_gather, steps):
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(st)
-        for _ in range(args.steps):
-            step()
+        for _ in range(steps):
+            step(with_gather)
         e1.record(st)
         barrier()
+        t = e0.elapsed_time(e1) / steps
+        if dist is not None:
+            tt = torch.tensor([t], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    headline_gather = bool(args.gather) and gather is not None
+    for _ in range(args.warmup):
+        step(headline_gather)
+    barrier()
+    n_launch0 = launch_count()
+    with ClockSampler(local) as clk, KernelTimer() as kt:
+        ms = timed(headline_gather, args.steps)
     launches = launch_count() - n_launch0
-    ms_local = e0.elapsed_time(e1) / args.steps
-    ms = ms_local
-    if dist is not None:
-        t = torch.tensor([ms_local], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     value = total_fpx / (ms * 1e-3) / 1e6
+    other = None
+    if gather is not None:  # the other mode, so one line carries compute-only and with-gather scaling
+        for _ in range(2):
+            step(not headline_gather)
+        oms = timed(not headline_gather, max(3, min(args.steps, 10)))
+        gathered = (N_all * H * W * K * (8 + 4 + 12 + 4) + (F_all * 72 if c["backward"] else 0))
+        other = {"gather": not headline_gather, "ms_per_step": oms, "value": total_fpx / (oms * 1e-3) / 1e6,
+                 "gathered_bytes_to_root": gathered, "groups": n_groups}
 
     # roofline of the dominant kernel (per-launch averages from the library's event timing)
     shares = {}
@@ -472,9 +530,13 @@ def main():
     if not args.no_e2e:
         from paper_2007_08501_b200.pipeline import HostPipeline
 
-        del ws  # the pipeline owns its own device buffers
+        del ws, fv, p2f_l, zb_l, ba_l, di_l, grad_l, local_bufs, glob  # the pipeline owns its device buffers
         torch.cuda.empty_cache()
-        pipe = HostPipeline(first_np, num_np, rs, F, dev, n_groups=args.e2e_groups, backward=c["backward"],
+        # a host caller of a shard packs its own meshes (rank-local face ids): only they cross PCIe
+        my = subset(meshes_all, mine)
+        fv_np = S.face_verts(my, cam)
+        lfirst, lnum = my.mesh_to_face_first_idx(), my.num_faces_per_mesh()
+        pipe = HostPipeline(lfirst, lnum, rs, F, dev, n_groups=args.e2e_groups, backward=c["backward"],
                             ramp=args.e2e_ramp, lookahead=args.e2e_lookahead)
         h_fv = torch.from_numpy(fv_np).pin_memory()
         cot_h = tuple(t.cpu().pin_memory() for t in (dz, db, dd)) if c["backward"] else None
@@ -488,6 +550,8 @@ def main():
         pipe.run(h_fv, out_h, cot_h, grad_h)
         barrier()
         h2d = h_fv.numel() * 8 + (sum(t.numel() for t in cot_h) * 4 if c["backward"] else 0)
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         for _ in range(e2e_steps):
             pipe.run(h_fv, out_h, cot_h, grad_h)
@@ -538,9 +602,12 @@ def main():
                           "blur_radius": c["blur"], "bin_size": c["bin_size"], "parallelism": f"mesh-shard{world}",
                           "l2": "inputs+outputs (GBs) exceed the 126 MB L2; no flush"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "like_for_like": like,
+               "gather_to_root": bool(args.gather) and world > 1, "gather_mode": other,
                "gpu_launches": int(launches),
                "clocks": clk.summary()}
         print(json.dumps(out))
+    if gather is not None:
+        gather.close()
     if dist is not None:
         dist.destroy_process_group()
 

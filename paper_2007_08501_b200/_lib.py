@@ -55,6 +55,51 @@ EXPORTED_SYMBOLS = (
     "dr_selftest_division",
 )
 
+# include/dr_shard.h: the plan / op-list half lives in libdr_raster_b200.so, the NCCL executor in libdr_shard_b200.so
+SHARD_PLAN_SYMBOLS = ("dr_shard_plan_lpt", "dr_shard_gather_ops")
+SHARD_NCCL_SYMBOLS = ("dr_shard_unique_id", "dr_shard_comm_init", "dr_shard_comm_destroy", "dr_shard_gather",
+                      "dr_shard_last_error")
+SHARD_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdr_shard_b200.so")
+
+
+class DrShardOp(C.Structure):
+    """dr_shard_op (include/dr_shard.h)."""
+
+    _fields_ = [("kind", C.c_int32), ("peer", C.c_int32), ("buffer", C.c_int32), ("mesh", C.c_int32),
+                ("src_offset", C.c_int64), ("dst_offset", C.c_int64), ("bytes", C.c_int64)]
+
+
+class DrShardBuffers(C.Structure):
+    """dr_shard_buffers (include/dr_shard.h)."""
+
+    _fields_ = [("pix_to_face", C.c_void_p), ("zbuf", C.c_void_p), ("bary", C.c_void_p), ("dists", C.c_void_p),
+                ("grad_face_verts", C.c_void_p)]
+
+
+_shard_lib = None
+
+
+def load_shard():
+    """libdr_shard_b200.so (NCCL executor of the gather); loads libdr_raster_b200.so first."""
+    global _shard_lib
+    if _shard_lib is not None:
+        return _shard_lib
+    load()
+    if not os.path.exists(SHARD_LIB_PATH):
+        raise RuntimeError(f"{SHARD_LIB_PATH} missing: run `make` (it needs NCCL)")
+    L = C.CDLL(SHARD_LIB_PATH)
+    _vp = C.c_void_p
+    L.dr_shard_unique_id.argtypes = [C.c_char_p]
+    L.dr_shard_comm_init.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.POINTER(_vp)]
+    L.dr_shard_comm_destroy.argtypes = [_vp]
+    L.dr_shard_gather.argtypes = [_vp, C.c_int32, C.c_int64, _vp, _vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32,
+                                  C.c_int32, C.c_int32, C.POINTER(DrShardBuffers), C.POINTER(DrShardBuffers), _vp]
+    for fn in ("dr_shard_unique_id", "dr_shard_comm_init", "dr_shard_comm_destroy", "dr_shard_gather"):
+        getattr(L, fn).restype = C.c_int
+    L.dr_shard_last_error.restype = C.c_char_p
+    _shard_lib = L
+    return L
+
 
 class DrRasterSettings(C.Structure):
     """dr_raster_settings (include/dr_raster.h)."""
@@ -176,6 +221,12 @@ def load() -> C.CDLL:
                "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_fwd_hr", "dr_rasterize_meshes_bwd_hr",
                "dr_rasterize_meshes_bin_stats"):
         getattr(L, fn).restype = C.c_int
+    L.dr_shard_plan_lpt.argtypes = [_vp, C.c_int64, C.c_int32, _vp, _vp]
+    L.dr_shard_gather_ops.argtypes = [C.c_int64, _vp, _vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(DrShardOp), C.c_int64,
+                                      C.POINTER(C.c_int64)]
+    L.dr_shard_plan_lpt.restype = C.c_int
+    L.dr_shard_gather_ops.restype = C.c_int
     _lib = L
     return L
 

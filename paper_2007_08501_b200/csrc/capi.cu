@@ -176,21 +176,26 @@ int read_ranges(const int64_t* first, const int64_t* num, int64_t N, int64_t F, 
   return DR_OK;
 }
 
-// Zero grad rows (`row` doubles per packed item) on the union of the batch's item ranges only (merged
-// intervals), so a caller may run the backward on disjoint groups of one packed buffer concurrently.
-cudaError_t zero_rows(double* grad, int row, const std::vector<int64_t>& h, int64_t N, cudaStream_t st) {
-  std::vector<std::pair<int64_t, int64_t>> iv;
+// The union of the batch's item ranges as sorted, merged [lo, hi) intervals (h = first[N] then num[N]).
+std::vector<std::pair<int64_t, int64_t>> merged_ranges(const std::vector<int64_t>& h, int64_t N) {
+  std::vector<std::pair<int64_t, int64_t>> iv, out;
   for (int64_t b = 0; b < N; ++b)
     if (h[N + b] > 0) iv.push_back({h[b], h[b] + h[N + b]});
   std::sort(iv.begin(), iv.end());
-  size_t i = 0;
-  while (i < iv.size()) {
-    int64_t lo = iv[i].first, hi = iv[i].second;
-    size_t j = i + 1;
-    while (j < iv.size() && iv[j].first <= hi) hi = std::max(hi, iv[j++].second);
-    cudaError_t e = cudaMemsetAsync(grad + (int64_t)row * lo, 0, sizeof(double) * row * (size_t)(hi - lo), st);
+  for (const auto& x : iv) {
+    if (!out.empty() && x.first <= out.back().second) out.back().second = std::max(out.back().second, x.second);
+    else out.push_back(x);
+  }
+  return out;
+}
+
+// Zero grad rows (`row` doubles per packed item) on the union of the batch's item ranges only (merged
+// intervals), so a caller may run the backward on disjoint groups of one packed buffer concurrently.
+cudaError_t zero_rows(double* grad, int row, const std::vector<int64_t>& h, int64_t N, cudaStream_t st) {
+  for (const auto& iv : merged_ranges(h, N)) {
+    cudaError_t e = cudaMemsetAsync(grad + (int64_t)row * iv.first, 0,
+                                    sizeof(double) * row * (size_t)(iv.second - iv.first), st);
     if (e != cudaSuccess) return e;
-    i = j;
   }
   return cudaSuccess;
 }
@@ -213,13 +218,6 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   std::vector<int64_t> ranges;
   rc = read_ranges(first, num, N, F, st, &max_faces, &ranges, host_first, host_num);
   if (rc) return rc;
-  // K0 only needs the faces the batch's meshes own: [lowest first, highest end)
-  int64_t f_lo = F, f_hi = 0;
-  for (int64_t b = 0; b < N; ++b)
-    if (ranges[N + b] > 0) {
-      f_lo = std::min(f_lo, ranges[b]);
-      f_hi = std::max(f_hi, ranges[b] + ranges[N + b]);
-    }
 
   char* base = static_cast<char*>(ws);
   int4* ibbox = reinterpret_cast<int4*>(base + p.off_ibbox);
@@ -232,9 +230,8 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
 
   {
     ProfScope ps(st, KN_SETUP);
-    if (f_hi > f_lo)
-      drb::launch_face_setup(fv, f_lo, f_hi, p.H, p.W, inflate, s->znear, s->clip_nonpositive_z, s->cull_backfaces,
-                             ibbox, zkey, st);
+    drb::launch_face_setup(fv, first, num, N, max_faces, merged_ranges(ranges, N), p.H, p.W, inflate, s->znear,
+                           s->clip_nonpositive_z, s->cull_backfaces, ibbox, zkey, st);
   }
   if (p.binned) {
     {
@@ -988,6 +985,9 @@ int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t 
 }
 
 const char* dr_last_error(void) { return g_err.c_str(); }
+
+// used by the host-only translation units of this library (shard.cu) to report through dr_last_error()
+int dr_set_error(int status, const char* msg) { return fail(status, "%s", msg); }
 
 int dr_rasterize_meshes_bin_stats(int64_t N, int64_t F, const dr_raster_settings* s, const void* ws,
                                   dr_stream_t stream, int64_t out[4]) {

@@ -15,6 +15,8 @@
 #include <cstdint>
 #include <algorithm>
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "raster_kernels.cuh"
 #include "raster_math.cuh"
@@ -71,12 +73,9 @@ __device__ __forceinline__ int last_row_ge(double L, int H) {
 // ------------------------------------------------------------------------------------------------
 // K0: face setup
 
-__global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ fv, int64_t f_lo, int64_t f_hi, int H,
-                                                    int W, double inflate, double znear, int clip_nonpositive_z,
-                                                    int cull_backfaces, int4* __restrict__ ibbox,
-                                                    float* __restrict__ zkey) {
-  int64_t f = f_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= f_hi) return;
+__device__ __forceinline__ void face_setup_one(const double* __restrict__ fv, int64_t f, int H, int W, double inflate,
+                                               double znear, int clip_nonpositive_z, int cull_backfaces,
+                                               int4* __restrict__ ibbox, float* __restrict__ zkey) {
   const double* p = fv + 9 * f;
   double v[9];
 #pragma unroll
@@ -120,6 +119,26 @@ __global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ f
   }
   ibbox[f] = out;
   if (zkey) zkey[f] = key;
+}
+
+// Only the batch's own faces are set up (a mesh-sharded rank passes its meshes' ranges of the whole packed batch):
+// k_face_setup_range covers one merged interval of the ranges; k_face_setup (grid (x, N), blockIdx.y = mesh) is
+// used when the ranges fall into many intervals. Overlapping ranges write identical values.
+__global__ void __launch_bounds__(256) k_face_setup_range(const double* __restrict__ fv, int64_t f_lo, int64_t f_hi,
+                                                          int H, int W, double inflate, double znear,
+                                                          int clip_nonpositive_z, int cull_backfaces,
+                                                          int4* __restrict__ ibbox, float* __restrict__ zkey) {
+  const int64_t f = f_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < f_hi) face_setup_one(fv, f, H, W, inflate, znear, clip_nonpositive_z, cull_backfaces, ibbox, zkey);
+}
+
+__global__ void __launch_bounds__(256) k_face_setup(const double* __restrict__ fv, const int64_t* __restrict__ first,
+                                                    const int64_t* __restrict__ num, int H, int W, double inflate,
+                                                    double znear, int clip_nonpositive_z, int cull_backfaces,
+                                                    int4* __restrict__ ibbox, float* __restrict__ zkey) {
+  const int64_t nf = num[blockIdx.y], f0 = first[blockIdx.y];
+  for (int64_t lf = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lf < nf; lf += (int64_t)gridDim.x * blockDim.x)
+    face_setup_one(fv, f0 + lf, H, W, inflate, znear, clip_nonpositive_z, cull_backfaces, ibbox, zkey);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1017,11 +1036,19 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
 // ------------------------------------------------------------------------------------------------
 // host-side launchers (called from capi.cu)
 
-void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int W, double inflate, double znear,
-                       int clip_z, int cull, int4* ibbox, float* zkey, cudaStream_t st) {
-  if (f_hi <= f_lo) return;
-  unsigned grid = (unsigned)((f_hi - f_lo + 255) / 256);
-  k_face_setup<<<grid, 256, 0, st>>>(fv, f_lo, f_hi, H, W, inflate, znear, clip_z, cull, ibbox, zkey);
+void launch_face_setup(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
+                       const std::vector<std::pair<int64_t, int64_t>>& intervals, int H, int W, double inflate,
+                       double znear, int clip_z, int cull, int4* ibbox, float* zkey, cudaStream_t st) {
+  if (max_faces <= 0) return;
+  if (intervals.size() <= 8) {  // one launch per merged interval of the ranges (one for a whole packed batch)
+    for (const auto& iv : intervals)
+      k_face_setup_range<<<(unsigned)((iv.second - iv.first + 255) / 256), 256, 0, st>>>(
+          fv, iv.first, iv.second, H, W, inflate, znear, clip_z, cull, ibbox, zkey);
+    return;
+  }
+  const unsigned gx = (unsigned)std::min<int64_t>((max_faces + 255) / 256, 65535);
+  k_face_setup<<<dim3(gx, (unsigned)N), 256, 0, st>>>(fv, first, num, H, W, inflate, znear, clip_z, cull, ibbox,
+                                                      zkey);
 }
 
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,

@@ -5,6 +5,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <utility>
+#include <vector>
 
 namespace drb {
 
@@ -176,8 +178,9 @@ cudaError_t launch_padded_to_packed(const void* padded, const int64_t* first, co
 cudaError_t launch_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
                                    cudaStream_t st);
 
-void launch_face_setup(const double* fv, int64_t f_lo, int64_t f_hi, int H, int W, double inflate, double znear,
-                       int clip_z, int cull, int4* ibbox, float* zkey, cudaStream_t st);
+void launch_face_setup(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
+                       const std::vector<std::pair<int64_t, int64_t>>& intervals, int H, int W, double inflate,
+                       double znear, int clip_z, int cull, int4* ibbox, float* zkey, cudaStream_t st);
 constexpr int kSortMax = 4096;      // bins up to this length are sorted by k_sort_bins (32 KB shared memory)
 constexpr int kSortMaxBig = 16384;  // ... up to this one by its 128 KB variant; longer bins stay unsorted
 // bin usable as a list: fits the pool and the caller's max_faces_per_bin (0 = unlimited)

@@ -80,3 +80,18 @@ def test_python_surface_rejects_cpu_tensors():
 
     with pytest.raises(UsageError):
         rasterize_meshes(torch.zeros(1, 3, 3, dtype=torch.float64), [0], [1])
+
+
+def test_shard_libraries_export_dr_shard_h():
+    """include/dr_shard.h: the plan / op-list functions live in libdr_raster_b200.so, the NCCL executor in
+    libdr_shard_b200.so (loadable without a GPU)."""
+    src = open(os.path.join(ROOT, "include", "dr_shard.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = sorted(set(re.findall(r"\b(dr_[a-z0-9_]+)\s*\(", src)))
+    assert names == sorted(_lib.SHARD_PLAN_SYMBOLS + _lib.SHARD_NCCL_SYMBOLS)
+    L, LS = _lib.load(), _lib.load_shard()
+    for n in _lib.SHARD_PLAN_SYMBOLS:
+        assert hasattr(L, n), n
+    for n in _lib.SHARD_NCCL_SYMBOLS:
+        assert hasattr(LS, n), n
+    assert C.sizeof(_lib.DrShardOp) == 40 and C.sizeof(_lib.DrShardBuffers) == 40
