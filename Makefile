@@ -8,7 +8,7 @@ NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas 
 PKG = paper_2007_08501_b200
 SRCS = $(PKG)/csrc/raster_fwd.cu $(PKG)/csrc/raster_bwd.cu $(PKG)/csrc/raster_camera.cu $(PKG)/csrc/capi.cu \
        $(PKG)/csrc/adaptor.cu $(PKG)/csrc/batching.cu $(PKG)/csrc/raster_points.cu $(PKG)/csrc/selftest.cu \
-       $(PKG)/csrc/shard.cu
+       $(PKG)/csrc/shard.cu $(PKG)/csrc/pipeline.cu
 HDRS = $(PKG)/csrc/raster_math.cuh $(PKG)/csrc/raster_kernels.cuh include/dr_raster.h include/dr_b200/mesh_raster.hpp \
        include/dr_b200/point_render.hpp include/dr_b200/shading.hpp include/dr_shard.h
 LIB = $(PKG)/libdr_raster_b200.so

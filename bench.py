@@ -57,6 +57,9 @@ def parse():
                     help="N>1: 1 = the timed step also gathers every mesh's fragments and grad_face_verts rows to "
                          "rank 0 over NCCL (pipelined); the line reports the other mode under 'gather_mode'")
     ap.add_argument("--gather-groups", type=int, default=4, help="pipeline groups of the gather (local meshes)")
+    ap.add_argument("--other-configs", type=int, default=1,
+                    help="1 (N=1): also time the other BASELINE configs (C1/C2/C3/C5) device-resident, each with its "
+                         "dominant kernel's roofline, under 'other_configs'")
     ap.add_argument("--like-for-like", type=int, default=1,
                     help="1: also time the GPU at reference semantics (flags off) on the whole batch and on the "
                          "CPU sample")
@@ -247,6 +250,84 @@ def cpu_sample(meshes: S.Meshes, frac: float):
         if acc >= target:
             break
     return idx
+
+
+KERNELS = ("k_face_setup", "k_bin_faces", "k_sort_bins", "k_fine", "k_backward")
+
+
+def roofline_of(kt, cfg, steps, N, F, S_):
+    """Roofline of the dominant kernel from the library's per-launch CUDA-event times (KernelTimer records).
+    Algorithmic bytes per launch: k_fine 72 F + 16 N + 28 S, k_backward 40 S + 144 F, else 88 F."""
+    shares = {}
+    for name in KERNELS:
+        tot, n = kt.total(name)
+        if n:
+            shares[name] = (tot, n)
+    dom = max(shares, key=lambda k: shares[k][0])
+    dom_ms = shares[dom][0] / shares[dom][1]
+    if dom == "k_backward":
+        alg_bytes = 40 * S_ + 144 * F
+    elif dom == "k_fine":
+        alg_bytes = 72 * F + 16 * N + 28 * S_
+    else:
+        alg_bytes = 72 * F + 16 * F
+    peaks, peak_kind = measured_peaks()
+    achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
+    step_ms_sum = sum(v[0] for v in shares.values()) / steps
+    return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(cfg, dom), "kernel": dom,
+            "kernel_ms": dom_ms, "kernel_share_of_step": shares[dom][0] / steps / max(step_ms_sum, 1e-9),
+            "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind, "issue": ncu_issue(cfg, dom),
+            "per_kernel_ms_per_step": {k: v[0] / steps for k, v in shares.items()}}
+
+
+def config_leg(cfg, dev, steps=5, warmup=2):
+    """One other BASELINE config (C1/C2/C3/C5), device-resident: step time, Mfaces·px/s and the dominant kernel's
+    roofline, the same way the headline is measured."""
+    import torch
+
+    from paper_2007_08501_b200 import KernelTimer, rasterize_meshes, rasterize_meshes_backward, workspace_bytes
+
+    c = S.CONFIGS[cfg]
+    H = W = c["image"]
+    K = c["K"]
+    m, cam, rs = S.config_meshes(cfg), S.bench_camera(), config_settings(cfg)
+    fv_np = S.face_verts(m, cam)
+    first_np, num_np = m.mesh_to_face_first_idx(), m.num_faces_per_mesh()
+    N, F = len(num_np), len(fv_np)
+    fv, first, num = (torch.as_tensor(x, device=dev) for x in (fv_np, first_np, num_np))
+    ws = torch.empty(workspace_bytes(N, F, rs), dtype=torch.uint8, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    cot = [torch.randn(s_, generator=gen, device=dev) for s_ in ((N, H, W, K), (N, H, W, K, 3), (N, H, W, K))] \
+        if c["backward"] else None
+    hr = (first_np, num_np)
+
+    def step():
+        p2f, _, bary, _ = rasterize_meshes(fv, first, num, rs, workspace=ws, host_ranges=hr)
+        if c["backward"]:
+            rasterize_meshes_backward(fv, first, num, rs, p2f, bary, *cot, host_ranges=hr)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with KernelTimer() as kt:
+        e0.record(st)
+        for _ in range(steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    S_ = N * H * W * K
+    rl = roofline_of(kt, cfg, steps, N, F, S_)
+    del ws, fv, cot
+    torch.cuda.empty_cache()
+    return {"desc": c["desc"], "fwd_bwd": bool(c["backward"]), "ms_per_step": ms,
+            "value": face_px(m, H, W) / (ms * 1e-3) / 1e6, "unit": UNIT, "steps": steps,
+            "roofline": {k: rl[k] for k in ("kernel", "kernel_ms", "frac", "achieved", "peak", "unit",
+                                            "algorithmic_bytes_per_launch", "per_kernel_ms_per_step")}}
 
 
 def like_for_like_leg(args, cfg, meshes_all, cam, dev):
@@ -499,30 +580,7 @@ def main():
         other = {"gather": not headline_gather, "ms_per_step": oms, "value": total_fpx / (oms * 1e-3) / 1e6,
                  "gathered_bytes_to_root": gathered, "groups": n_groups}
 
-    # roofline of the dominant kernel (per-launch averages from the library's event timing)
-    shares = {}
-    for name in ("k_face_setup", "k_bin_faces", "k_sort_bins", "k_fine", "k_backward"):
-        tot, n = kt.total(name)
-        if n:
-            shares[name] = (tot, n)
-    dom = max(shares, key=lambda k: shares[k][0])
-    dom_ms = shares[dom][0] / shares[dom][1]
-    if dom == "k_backward":
-        alg_bytes = 40 * S_ + 144 * F
-    elif dom == "k_fine":
-        alg_bytes = 72 * F + 16 * N + 28 * S_
-    else:
-        alg_bytes = 72 * F + 16 * F
-    peaks, peak_kind = measured_peaks()
-    traffic = ncu_traffic(cfg, dom)
-    achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
-    step_ms_sum = sum(v[0] for v in shares.values()) / args.steps
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "kernel": dom,
-                "kernel_ms": dom_ms, "kernel_share_of_step": shares[dom][0] / args.steps / max(step_ms_sum, 1e-9),
-                "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
-                "issue": ncu_issue(cfg, dom),
-                "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in shares.items()}}
+    roofline = roofline_of(kt, cfg, args.steps, N, F, S_)
 
     # end to end through the public API with host buffers (pinned), copies inside the timed region: the
     # HostPipeline streams groups of meshes so H2D / kernels / D2H overlap (paper_2007_08501_b200/pipeline.py)
@@ -565,11 +623,14 @@ def main():
         e2e = {"value": total_fpx / (ems * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "pcie_gbs": (h2d + d2h) / (ems * 1e-3) / 1e9, "groups": len(pipe.groups), "ramp": args.e2e_ramp, "lookahead": args.e2e_lookahead,
-               "api": "paper_2007_08501_b200.pipeline.HostPipeline.run (pinned host in/out)"}
+               "api": "paper_2007_08501_b200.pipeline.HostPipeline.run -> dr_host_pipeline_run (C++, pinned host in/out)"}
 
     like = None
     if rank == 0 and world == 1 and args.like_for_like and (rs.perspective_correct or rs.cull_backfaces):
         like = like_for_like_leg(args, cfg, meshes_all, cam, dev)
+    others = None
+    if rank == 0 and world == 1 and args.other_configs:
+        others = {o: config_leg(o, dev) for o in sorted(S.CONFIGS) if o != cfg}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -602,7 +663,7 @@ def main():
                           "blur_radius": c["blur"], "bin_size": c["bin_size"], "parallelism": f"mesh-shard{world}",
                           "l2": "inputs+outputs (GBs) exceed the 126 MB L2; no flush"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "like_for_like": like,
-               "gather_to_root": bool(args.gather) and world > 1, "gather_mode": other,
+               "gather_to_root": bool(args.gather) and world > 1, "gather_mode": other, "other_configs": others,
                "gpu_launches": int(launches),
                "clocks": clk.summary()}
         print(json.dumps(out))

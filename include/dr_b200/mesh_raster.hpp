@@ -121,6 +121,67 @@ struct MeshFragments {
   int64_t slot(int b, int i, int j, int s) const { return ((int64_t(b) * h + i) * w + j) * k + s; }
 };
 
+// Page-locked host memory for the streamed pipeline's buffers (cudaHostAlloc): copies from / to it overlap the
+// kernels; from pageable std::vector memory they would serialise.
+template <typename T>
+struct PinnedAllocator {
+  using value_type = T;
+  PinnedAllocator() = default;
+  template <typename U>
+  PinnedAllocator(const PinnedAllocator<U>&) {}
+  T* allocate(size_t n);
+  void deallocate(T* p, size_t) noexcept;
+  template <typename U>
+  bool operator==(const PinnedAllocator<U>&) const { return true; }
+  template <typename U>
+  bool operator!=(const PinnedAllocator<U>&) const { return false; }
+};
+template <typename T>
+using pinned_vector = std::vector<T, PinnedAllocator<T>>;
+
+// fp32-payload fragments in page-locked host memory (the layout of MeshFragments, floats instead of doubles):
+// what HostPipeline streams back. pix_to_face is bit-identical to MeshFragments'; zbuf / bary / dists are the
+// fp64 values rounded once (within 1e-5 relative / 1e-6 absolute of the reference, BASELINE north_star).
+struct MeshFragments32 {
+  int batch = 0, h = 0, w = 0, k = 0;
+  pinned_vector<int64_t> pix_to_face;
+  pinned_vector<float> zbuf;
+  pinned_vector<float> bary;
+  pinned_vector<float> dists;
+  int64_t slots() const { return int64_t(batch) * h * w * k; }
+  void resize(int b, int hh, int ww, int kk);
+};
+
+// The streamed host path (include/dr_raster.h dr_host_pipeline_*): forward + backward of one fixed batch layout
+// between page-locked host buffers and the GPU, mesh groups pipelined over three CUDA streams (H2D of group g+1,
+// kernels of g, D2H of g-1). Construct once per (batch layout, settings); run() per step. Inputs are the
+// north-star boundary (packed face_verts [F,3,3] = world_to_ndc per face vertex, e.g. from face_verts_packed);
+// outputs land in `out` / `grad_face_verts` when run() returns (it synchronises its stream).
+class HostPipeline {
+ public:
+  HostPipeline(const std::vector<int64_t>& mesh_to_face_first_idx, const std::vector<int64_t>& num_faces_per_mesh,
+               int64_t num_faces, const RasterSettings& s, const Camera& c, int n_groups = 24, int ramp = 2,
+               int lookahead = 3, bool backward = true);
+  ~HostPipeline();
+  HostPipeline(const HostPipeline&) = delete;
+  HostPipeline& operator=(const HostPipeline&) = delete;
+  // face_verts [F*9]; cotangents fp32 in the fragment layout (bary x3); grad_face_verts [F*9] (fp64)
+  void run(const pinned_vector<double>& face_verts, MeshFragments32& out, const pinned_vector<float>& d_zbuf,
+           const pinned_vector<float>& d_bary, const pinned_vector<float>& d_dists,
+           pinned_vector<double>& grad_face_verts);
+  int groups() const;
+
+ private:
+  void* handle_ = nullptr;
+  void* stream_ = nullptr;
+  int n_ = 0, h_ = 0, w_ = 0, k_ = 0;
+  int64_t f_ = 0;
+  bool backward_ = true;
+};
+
+// world_to_ndc of every packed vertex gathered per face (the north-star face_verts [F,3,3]) into host memory.
+pinned_vector<double> face_verts_packed(const MeshBatch& m, const Camera& c);
+
 MeshFragments rasterize_meshes(const MeshBatch& m, const Camera& c, const RasterSettings& s);
 MeshFragments rasterize_meshes_naive(const MeshBatch& m, const Camera& c, const RasterSettings& s);
 std::vector<Vec3> rasterize_backward(const MeshBatch& m, const Camera& c, const RasterSettings& s,

@@ -174,6 +174,25 @@ int dr_padded_to_packed(const void* padded, const int64_t* first, const int64_t*
 int dr_packed_item_to_element(const int64_t* first, const int64_t* num, int64_t N, int64_t total, int32_t* out,
                               dr_stream_t stream);
 
+/* ---- streamed host pipeline (the reference's host-in / host-out calling convention, mesh_raster.hpp:41,66-69) ----
+ * rasterize_meshes forward (+ backward) between HOST buffers and the GPU: the batch is cut into contiguous groups
+ * of meshes balanced by PCIe bytes (smaller groups at both ends, `ramp`) and run on three streams so H2D of
+ * group g+1, the kernels of group g and D2H of group g-1 overlap; group g's H2D waits for the D2H of group
+ * g - lookahead (0: no gating). Host ranges: ordered, non-overlapping mesh ranges of the packed batch (host
+ * arrays). The pipeline owns its device buffers (one allocation) and streams; run() is stream-ordered: it
+ * enqueues everything and makes `stream` wait for completion. Host buffers should be page-locked for the copies
+ * to overlap. fp32 payload / cotangents (the dr_rasterize_meshes_fwd / _bwd layouts), fp64 grad_face_verts. */
+typedef struct dr_host_pipeline* dr_host_pipeline_t;
+int dr_host_pipeline_create(const int64_t* host_first, const int64_t* host_num, int64_t N, int64_t F,
+                            const dr_raster_settings* s, int32_t n_groups, int32_t ramp, int32_t lookahead,
+                            int32_t backward, dr_host_pipeline_t* out);
+/* Number of groups; writes up to cap [g0, g1) mesh ranges into bounds[2 * g], bounds[2 * g + 1]. */
+int dr_host_pipeline_groups(dr_host_pipeline_t p, int64_t* bounds, int64_t cap);
+int dr_host_pipeline_run(dr_host_pipeline_t p, const double* face_verts, int64_t* pix_to_face, float* zbuf,
+                         float* bary_coords, float* pix_dists, const float* grad_zbuf, const float* grad_bary,
+                         const float* grad_dists, double* grad_face_verts, dr_stream_t stream);
+int dr_host_pipeline_destroy(dr_host_pipeline_t p);
+
 /* ---- fused fragment consumer: silhouette ----
  * dr_rasterize_silhouette_fwd = silhouette_blend(rasterize_meshes(...), sigma)
  *   (shading.cpp:75-91 over mesh_raster.cpp:234): alpha [N,H,W] fp32 = 1 - prod_k (1 - sigmoid(-dist_k / sigma))

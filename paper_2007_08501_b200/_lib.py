@@ -53,6 +53,10 @@ EXPORTED_SYMBOLS = (
     "dr_profile_read",
     "dr_profile_kernel_name",
     "dr_selftest_division",
+    "dr_host_pipeline_create",
+    "dr_host_pipeline_groups",
+    "dr_host_pipeline_run",
+    "dr_host_pipeline_destroy",
 )
 
 # include/dr_shard.h: the plan / op-list half lives in libdr_raster_b200.so, the NCCL executor in libdr_shard_b200.so
@@ -220,6 +224,14 @@ def load() -> C.CDLL:
                "dr_rasterize_meshes_fwd_f64", "dr_rasterize_meshes_bwd",
                "dr_rasterize_meshes_bwd_f64", "dr_rasterize_meshes_fwd_hr", "dr_rasterize_meshes_bwd_hr",
                "dr_rasterize_meshes_bin_stats"):
+        getattr(L, fn).restype = C.c_int
+    L.dr_host_pipeline_create.argtypes = [_vp, _vp, C.c_int64, C.c_int64, sp, C.c_int32, C.c_int32, C.c_int32,
+                                          C.c_int32, C.POINTER(_vp)]
+    L.dr_host_pipeline_groups.argtypes = [_vp, _vp, C.c_int64]
+    L.dr_host_pipeline_run.argtypes = [_vp] * 11
+    L.dr_host_pipeline_destroy.argtypes = [_vp]
+    for fn in ("dr_host_pipeline_create", "dr_host_pipeline_groups", "dr_host_pipeline_run",
+               "dr_host_pipeline_destroy"):
         getattr(L, fn).restype = C.c_int
     L.dr_shard_plan_lpt.argtypes = [_vp, C.c_int64, C.c_int32, _vp, _vp]
     L.dr_shard_gather_ops.argtypes = [C.c_int64, _vp, _vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32,

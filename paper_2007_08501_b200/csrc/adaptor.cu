@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <new>
 #include <string>
 #include <utility>
 
@@ -230,6 +231,82 @@ Camera Camera::look_from_distance(double d, ProjectionKind kind, double focal) {
 
 MeshFragments rasterize_meshes(const MeshBatch& m, const Camera& c, const RasterSettings& s) {
   return run_forward(m, c, s, /*naive=*/s.tile_size <= 0);
+}
+
+template <typename T>
+T* PinnedAllocator<T>::allocate(size_t n) {
+  void* p = nullptr;
+  if (n && cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocDefault) != cudaSuccess) throw std::bad_alloc();
+  return static_cast<T*>(p);
+}
+template <typename T>
+void PinnedAllocator<T>::deallocate(T* p, size_t) noexcept {
+  if (p) cudaFreeHost(p);
+}
+template struct PinnedAllocator<int64_t>;
+template struct PinnedAllocator<float>;
+template struct PinnedAllocator<double>;
+
+void MeshFragments32::resize(int b, int hh, int ww, int kk) {
+  batch = b;
+  h = hh;
+  w = ww;
+  k = kk;
+  const size_t S = (size_t)slots();
+  pix_to_face.resize(S);
+  zbuf.resize(S);
+  bary.resize(3 * S);
+  dists.resize(S);
+}
+
+pinned_vector<double> face_verts_packed(const MeshBatch& m, const Camera& c) {
+  DeviceMesh d(m, c);
+  pinned_vector<double> out(9 * (size_t)d.F);
+  download(out.data(), d.fv, 9 * (size_t)d.F);
+  return out;
+}
+
+HostPipeline::HostPipeline(const std::vector<int64_t>& first, const std::vector<int64_t>& num, int64_t num_faces,
+                           const RasterSettings& s, const Camera& c, int n_groups, int ramp, int lookahead,
+                           bool backward)
+    : n_((int)num.size()), h_(s.image_h), w_(s.image_w), k_(s.faces_per_pixel), f_(num_faces), backward_(backward) {
+  if (first.size() != num.size()) throw ShapeError("HostPipeline: first / num lengths differ");
+  dr_raster_settings rs = to_c(s, c, s.tile_size <= 0);
+  dr_host_pipeline_t h = nullptr;
+  check(dr_host_pipeline_create(first.data(), num.data(), (int64_t)num.size(), num_faces, &rs, n_groups, ramp,
+                                lookahead, backward ? 1 : 0, &h),
+        "HostPipeline");
+  handle_ = h;
+  cudaStream_t st = nullptr;
+  cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "HostPipeline stream");
+  stream_ = st;
+}
+
+HostPipeline::~HostPipeline() {
+  dr_host_pipeline_destroy(static_cast<dr_host_pipeline_t>(handle_));
+  if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+}
+
+int HostPipeline::groups() const {
+  return dr_host_pipeline_groups(static_cast<dr_host_pipeline_t>(handle_), nullptr, 0);
+}
+
+void HostPipeline::run(const pinned_vector<double>& face_verts, MeshFragments32& out,
+                       const pinned_vector<float>& d_zbuf, const pinned_vector<float>& d_bary,
+                       const pinned_vector<float>& d_dists, pinned_vector<double>& grad_face_verts) {
+  const int64_t S = (int64_t)n_ * h_ * w_ * k_;
+  if ((int64_t)face_verts.size() != 9 * f_) throw ShapeError("HostPipeline::run: face_verts is not [F,3,3]");
+  if (backward_ && ((int64_t)d_zbuf.size() != S || (int64_t)d_bary.size() != 3 * S || (int64_t)d_dists.size() != S))
+    throw ShapeError("HostPipeline::run: cotangent shapes do not match the fragments");  // mesh_raster.cpp:333-336
+  if (out.batch != n_ || out.h != h_ || out.w != w_ || out.k != k_) out.resize(n_, h_, w_, k_);
+  if (backward_) grad_face_verts.resize(9 * (size_t)f_);
+  auto st = static_cast<cudaStream_t>(stream_);
+  check(dr_host_pipeline_run(static_cast<dr_host_pipeline_t>(handle_), face_verts.data(), out.pix_to_face.data(),
+                             out.zbuf.data(), out.bary.data(), out.dists.data(), backward_ ? d_zbuf.data() : nullptr,
+                             backward_ ? d_bary.data() : nullptr, backward_ ? d_dists.data() : nullptr,
+                             backward_ ? grad_face_verts.data() : nullptr, reinterpret_cast<dr_stream_t>(st)),
+        "HostPipeline::run");
+  cuda_check(cudaStreamSynchronize(st), "HostPipeline::run");
 }
 
 MeshFragments rasterize_meshes_naive(const MeshBatch& m, const Camera& c, const RasterSettings& s) {

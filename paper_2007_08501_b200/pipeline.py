@@ -1,5 +1,6 @@
 """End-to-end host path: rasterize_meshes forward + backward from pinned HOST buffers, streamed over groups of
-meshes so PCIe copies overlap the kernels.
+meshes so PCIe copies overlap the kernels. The pipeline itself is native (csrc/pipeline.cu, dr_host_pipeline_* in
+include/dr_raster.h); this module is its Python binding plus the grouping rule restated for the CPU tests.
 
 The reference's rasterize_meshes / rasterize_backward take and return host data (MeshFragments by value,
 mesh_raster.hpp:41,66-69). A host caller of the B200 path pays H2D for face_verts (72 B/face) and the
@@ -16,14 +17,18 @@ global and each group's backward writes only its own rows of grad_face_verts (in
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 
-from .raster import RasterSettings, rasterize_meshes, rasterize_meshes_backward, workspace_bytes
+from . import _lib
+from .raster import RasterSettings, _check, _ptr
 
 
 def contiguous_groups(costs, n_groups: int, ramp: int = 0) -> list:
-    """Split items 0..N-1 into <= n_groups contiguous runs of roughly equal total cost. ``ramp`` > 0 makes the
+    """(The rule csrc/pipeline.cu applies; tests/test_gpu_parity.py checks the native pipeline's groups against
+    it.) Split items 0..N-1 into <= n_groups contiguous runs of roughly equal total cost. ``ramp`` > 0 makes the
     first and last ``ramp`` groups geometrically smaller (1/2, 1/4, ... of a full one): the pipeline's fill (the
     first group's H2D + kernels, before any D2H) and drain (the last group's D2H) then run on small groups."""
     counts = np.asarray(costs, dtype=np.float64)
@@ -51,95 +56,57 @@ def transfer_costs(num_faces_per_mesh, hw_k: int, backward: bool) -> np.ndarray:
 
 
 class HostPipeline:
-    """Streams forward (+ backward) of a fixed batch layout between pinned host buffers and the GPU."""
+    """Streams forward (+ backward) of a fixed batch layout between pinned host buffers and the GPU
+    (dr_host_pipeline_*: one device allocation, three streams, the caller's stream waits for completion)."""
 
     def __init__(self, first, num, settings: RasterSettings, num_faces: int, device, n_groups: int = 8,
                  backward: bool = True, ramp: int = 2, lookahead: int = 3):
-        self.first = np.asarray(first, dtype=np.int64)
-        self.num = np.asarray(num, dtype=np.int64)
-        order = np.argsort(self.first, kind="stable")
-        if not np.array_equal(order, np.arange(len(order))) or np.any(self.first[1:] < self.first[:-1] + self.num[:-1]):
-            raise ValueError("HostPipeline needs packed, ordered, non-overlapping mesh ranges")
+        self.first = np.ascontiguousarray(first, dtype=np.int64)
+        self.num = np.ascontiguousarray(num, dtype=np.int64)
         self.s = settings
         self.F = int(num_faces)
         self.N = len(self.num)
         self.dev = torch.device(device)
         self.backward = backward
-        self.lookahead = int(lookahead)  # 0: every H2D enqueued at once
-        # instead of an H2D copy of every slot's cotangents
-        H, W = settings.hw
-        K = settings.faces_per_pixel
-        # groups balance PCIe bytes (the e2e bound), not faces: a mesh's slots cost as much as ~0.5M faces
-        self.groups = contiguous_groups(transfer_costs(self.num, H * W * K, backward), n_groups, ramp)
-        d = self.dev
-        self.fv = torch.empty((self.F, 3, 3), dtype=torch.float64, device=d)
-        self.p2f = torch.empty((self.N, H, W, K), dtype=torch.int64, device=d)
-        self.zbuf = torch.empty((self.N, H, W, K), dtype=torch.float32, device=d)
-        self.bary = torch.empty((self.N, H, W, K, 3), dtype=torch.float32, device=d)
-        self.dists = torch.empty((self.N, H, W, K), dtype=torch.float32, device=d)
-        if backward:
-            self.dz = torch.empty_like(self.zbuf)
-            self.db = torch.empty_like(self.bary)
-            self.dd = torch.empty_like(self.dists)
-            self.grad = torch.zeros((self.F, 3, 3), dtype=torch.float64, device=d)
-        ws = max(workspace_bytes(g1 - g0, self.F, settings) for g0, g1 in self.groups)
-        self.ws = torch.empty(ws, dtype=torch.uint8, device=d)
-        self.g_first = [torch.as_tensor(self.first[g0:g1], device=d) for g0, g1 in self.groups]
-        self.g_num = [torch.as_tensor(self.num[g0:g1], device=d) for g0, g1 in self.groups]
-        self.g_host = [(self.first[g0:g1].copy(), self.num[g0:g1].copy()) for g0, g1 in self.groups]
-        self.h2d, self.comp, self.d2h = (torch.cuda.Stream(device=d) for _ in range(3))
-
-    def face_range(self, g0, g1):
-        lo = int(self.first[g0])
-        hi = int(self.first[g1 - 1] + self.num[g1 - 1])
-        return lo, hi
+        self.L = _lib.load()
+        self._c = settings.to_c()
+        self.h = C.c_void_p()
+        with torch.cuda.device(self.dev):
+            rc = self.L.dr_host_pipeline_create(self.first.ctypes.data, self.num.ctypes.data, self.N, self.F,
+                                                C.byref(self._c), int(n_groups), int(ramp), int(lookahead),
+                                                int(bool(backward)), C.byref(self.h))
+        _check(rc, "HostPipeline")
+        n = self.L.dr_host_pipeline_groups(self.h, None, 0)
+        b = np.zeros(2 * max(n, 1), np.int64)
+        self.L.dr_host_pipeline_groups(self.h, b.ctypes.data, n)
+        self.groups = [(int(b[2 * g]), int(b[2 * g + 1])) for g in range(n)]
 
     def run(self, fv_h, out_h, cot_h=None, grad_h=None):
         """fv_h [F,3,3] f64 pinned; out_h = (p2f, zbuf, bary, dists) pinned host tensors; cot_h = (dz, db, dd)
-        pinned fp32; grad_h [F,3,3] f64 pinned. Enqueues everything; the caller synchronises."""
-        main = torch.cuda.current_stream(self.dev)
-        for st in (self.h2d, self.comp, self.d2h):
-            st.wait_stream(main)
-        # per group: H2D on h2d, kernels on comp, D2H on d2h. The device->host direction carries more bytes than
-        # the host->device one (fragments 28 B/slot vs cotangents 20 B/slot), and the two directions share the
-        # link's bidirectional budget: group g's H2D waits for the D2H of group g - lookahead, so the inputs arrive
-        # just in time instead of taking half the link while the outputs queue. The *_hr entry points take host
-        # copies of the mesh ranges, so no call synchronises and the host runs ahead.
-        ev_d2h = []
-        for gi, (g0, g1) in enumerate(self.groups):
-            lo, hi = self.face_range(g0, g1)
-            if self.lookahead > 0 and gi >= self.lookahead:
-                self.h2d.wait_event(ev_d2h[gi - self.lookahead])
-            with torch.cuda.stream(self.h2d):
-                self.fv[lo:hi].copy_(fv_h[lo:hi], non_blocking=True)
-                if self.backward:
-                    for d, h in zip((self.dz, self.db, self.dd), cot_h):
-                        d[g0:g1].copy_(h[g0:g1], non_blocking=True)
-                ev_in = torch.cuda.Event()
-                ev_in.record(self.h2d)
-            self.comp.wait_event(ev_in)
-            with torch.cuda.stream(self.comp):
-                outs = (self.p2f[g0:g1], self.zbuf[g0:g1], self.bary[g0:g1], self.dists[g0:g1])
-                rasterize_meshes(self.fv, self.g_first[gi], self.g_num[gi], self.s, workspace=self.ws, out=outs,
-                                 host_ranges=self.g_host[gi])
-                ev_fwd = torch.cuda.Event()
-                ev_fwd.record(self.comp)
-                if self.backward:
-                    rasterize_meshes_backward(self.fv, self.g_first[gi], self.g_num[gi], self.s, outs[0], outs[2],
-                                              self.dz[g0:g1], self.db[g0:g1], self.dd[g0:g1], out=self.grad,
-                                              host_ranges=self.g_host[gi])
-                ev_out = torch.cuda.Event()
-                ev_out.record(self.comp)
-            self.d2h.wait_event(ev_fwd)
-            with torch.cuda.stream(self.d2h):
-                for h, d in zip(out_h, outs):
-                    h[g0:g1].copy_(d, non_blocking=True)
-            if self.backward:
-                self.d2h.wait_event(ev_out)
-                with torch.cuda.stream(self.d2h):
-                    grad_h[lo:hi].copy_(self.grad[lo:hi], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(self.d2h)
-            ev_d2h.append(ev)
-        for st in (self.h2d, self.comp, self.d2h):
-            main.wait_stream(st)
+        pinned fp32; grad_h [F,3,3] f64 pinned. Enqueues everything; the current stream waits for completion."""
+        H, W = self.s.hw
+        K = self.s.faces_per_pixel
+        shp = (self.N, H, W, K)
+        for t, want, dt in zip(out_h, (shp, shp, shp + (3,), shp), (torch.int64,) + (torch.float32,) * 3):
+            if tuple(t.shape) != want or t.dtype != dt or t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"HostPipeline.run: host output {tuple(t.shape)} {t.dtype}, want {want} {dt}")
+        cz = cb = cd = gr = None
+        if self.backward:
+            cz, cb, cd = (t.contiguous() for t in cot_h)
+            gr = grad_h
+        with torch.cuda.device(self.dev):
+            st = C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+            rc = self.L.dr_host_pipeline_run(self.h, _ptr(fv_h), *(_ptr(t) for t in out_h), _ptr(cz), _ptr(cb),
+                                             _ptr(cd), _ptr(gr), st)
+        _check(rc, "HostPipeline.run")
+
+    def close(self):
+        if self.h:
+            self.L.dr_host_pipeline_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -3,6 +3,7 @@
 // reference library dr:: (oracle/_ref/libdr3d_ref.so, the unmodified reference sources) on the same inputs.
 // Built by the top-level Makefile (target `cpptest`, needs /root/reference headers at build time) and run by
 // tests/test_cpp_mirror.py on a GPU box. Prints one line per case; exit code = number of failed checks.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -324,6 +325,49 @@ static void fused_silhouette_matches_reference_fit_step() {
   CHECK(max_rel(flat(got), flat(want)) < 1e-4);
 }
 
+// The streamed host pipeline (dr_b200::HostPipeline, include/dr_raster.h dr_host_pipeline_*) on a synthetic batch:
+// pix_to_face bit-identical to the reference dr::rasterize_meshes, the fp32 payload within the north-star
+// tolerance of the reference's fp64 one, and the same gradients whether the batch streams as 1 or 5 mesh groups.
+static void host_pipeline_matches_reference() {
+  ref::MeshBatch m = ref::synthetic_batch(3000.0, 1500.0, 6, 3);
+  ref::Camera cam = ref::Camera::look_from_distance(3.0, ref::ProjectionKind::Perspective, 2.0);
+  ref::RasterSettings s;
+  s.image_h = s.image_w = 64;
+  s.faces_per_pixel = 4;
+  s.blur_radius = 1e-4;
+  ref::MeshFragments want = ref::rasterize_meshes(m, cam, s);
+  gpu::MeshBatch gm = to_gpu(m);
+  const int64_t F = gm.total_faces();
+  std::vector<int64_t> first(gm.faces_packed().offsets.begin(), gm.faces_packed().offsets.end() - 1);
+  gpu::pinned_vector<double> fv = gpu::face_verts_packed(gm, to_gpu(cam));
+  const size_t S = size_t(want.slots());
+  ref::Rng rng(5);
+  gpu::pinned_vector<float> dz(S), db(3 * S), dd(S);
+  for (auto& x : dz) x = float(rng.normal());
+  for (auto& x : db) x = float(rng.normal());
+  for (auto& x : dd) x = float(rng.normal());
+  gpu::pinned_vector<double> g1, g5;
+  for (int groups : {1, 5}) {
+    gpu::HostPipeline pipe(first, gm.num_faces_per_mesh(), F, to_gpu(s), to_gpu(cam), groups, 1, 2, true);
+    CHECK(pipe.groups() >= 1 && pipe.groups() <= groups);
+    gpu::MeshFragments32 out;
+    for (int rep = 0; rep < 2; ++rep) pipe.run(fv, out, dz, db, dd, groups == 1 ? g1 : g5);
+    CHECK(std::equal(want.pix_to_face.begin(), want.pix_to_face.end(), out.pix_to_face.begin()));
+    bool close = true;
+    for (size_t i = 0; i < S; ++i) {
+      close = close && std::fabs(out.zbuf[i] - want.zbuf[i]) <= 1e-6 + 1e-5 * std::fabs(want.zbuf[i]);
+      close = close && std::fabs(out.dists[i] - want.dists[i]) <= 1e-6 + 1e-5 * std::fabs(want.dists[i]);
+    }
+    for (size_t i = 0; i < 3 * S; ++i) close = close && std::fabs(out.bary[i] - want.bary[i]) <= 1e-6 + 1e-5 * std::fabs(want.bary[i]);
+    CHECK(close);
+  }
+  std::vector<double> a(g1.begin(), g1.end()), b(g5.begin(), g5.end());
+  CHECK(max_rel(a, b) < 1e-12);
+  double mx = 0;
+  for (double x : a) mx = std::max(mx, std::fabs(x));
+  CHECK(mx > 0);
+}
+
 int main() {
   struct Case {
     const char* name;
@@ -334,7 +378,8 @@ int main() {
                {"backward_matches_fd_and_reference", backward_matches_fd_and_reference},
                {"errors_mirror_reference", errors_mirror_reference},
                {"points_tiled_naive_reference", points_tiled_naive_reference},
-               {"fused_silhouette_matches_reference_fit_step", fused_silhouette_matches_reference_fit_step}};
+               {"fused_silhouette_matches_reference_fit_step", fused_silhouette_matches_reference_fit_step},
+               {"host_pipeline_matches_reference", host_pipeline_matches_reference}};
   for (auto& c : cases) {
     int before = g_fail;
     try {

@@ -396,6 +396,9 @@ def test_host_pipeline_matches_device_calls(cuda):
     cot = [torch.as_tensor(g.standard_normal(s), dtype=torch.float32) for s in
            ((N, 128, 128, 8), (N, 128, 128, 8, 3), (N, 128, 128, 8))]
     pipe = HostPipeline(first, num, rs, F, cuda, n_groups=3)
+    from paper_2007_08501_b200.pipeline import contiguous_groups, transfer_costs
+
+    assert pipe.groups == contiguous_groups(transfer_costs(num, 128 * 128 * 8, True), 3, 2)  # native == Python rule
     out_h = (torch.empty((N, 128, 128, 8), dtype=torch.int64).pin_memory(),
              torch.empty((N, 128, 128, 8), dtype=torch.float32).pin_memory(),
              torch.empty((N, 128, 128, 8, 3), dtype=torch.float32).pin_memory(),
