@@ -5,7 +5,7 @@ set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
 out=build/variants/$name; mkdir -p $out
-SRCS=$(cd paper_2007_08501_b200/csrc && ls *.cu | sed 's/\.cu$//')
+SRCS=$(cd paper_2007_08501_b200/csrc && ls *.cu | sed 's/\.cu$//' | grep -v '^shard_nccl$')
 for f in $SRCS; do
   fmad=-fmad=false
   for g in $FMAD_FILES; do [ "$g" = "$f" ] && fmad=-fmad=true; done
