@@ -238,6 +238,33 @@ class RefLib:
         L.ref_fit_silhouette.argtypes = [C.c_char_p, _i32p, _dp, _dp, _dp, _dp, C.c_int64, _i64p]
         L.ref_mesh_losses.argtypes = [C.c_void_p, _dp, _dp, _dp]
         L.ref_silhouette_iou.argtypes = [_dp, _dp, C.c_int64, C.c_double, _dp, _dp]
+        L.ref_packed_to_padded.argtypes = [_dp, _i64p, C.c_int64, C.c_int32, C.c_double, _dp]
+        L.ref_padded_to_packed.argtypes = [_dp, C.c_int64, C.c_int64, _i64p, C.c_int32, _dp, _i32p]
+
+    def packed_to_padded(self, packed, offsets, pad):
+        """dr::packed_to_padded (batching.hpp:48-60) on rows of 1 or 9 doubles -> [B, max_count, row]."""
+        x = np.ascontiguousarray(packed, np.float64)
+        row = 1 if x.ndim == 1 else int(np.prod(x.shape[1:]))
+        off = np.ascontiguousarray(offsets, np.int64)
+        B = len(off) - 1
+        M = int(np.max(np.diff(off))) if B else 0
+        out = np.empty((B, M, row))
+        if self.lib.ref_packed_to_padded(_p(x, _dp), _p(off, _i64p), B, row, pad, _p(out, _dp)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return out
+
+    def padded_to_packed(self, padded, counts):
+        """dr::padded_to_packed (batching.hpp:62-75) -> (packed [sum(counts), row], item_to_element)."""
+        x = np.ascontiguousarray(padded, np.float64)
+        B, M = x.shape[:2]
+        row = int(np.prod(x.shape[2:])) if x.ndim > 2 else 1
+        cnt = np.ascontiguousarray(counts, np.int64)
+        out = np.empty((int(cnt.sum()), row))
+        ite = np.empty(int(cnt.sum()), np.int32)
+        if self.lib.ref_padded_to_packed(_p(x, _dp), B, M, _p(cnt, _i64p), row, _p(out, _dp),
+                                         ite.ctypes.data_as(_i32p)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return out, ite
 
     def set_num_threads(self, n: int):
         self.lib.ref_set_num_threads(n)

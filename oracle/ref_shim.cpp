@@ -13,6 +13,7 @@
 //   dr::rasterize_points / _naive, splat_position_backward (point_render.hpp:33-36, 66-68)
 //   dr::fit_silhouette (pipeline.hpp:91-95, pipeline.cpp:100-205) and its regularizers / loss
 //   (geometry.hpp:96-107)
+//   dr::packed_to_padded / padded_to_packed (batching.hpp:48-75) over fixed-size rows
 // Errors are caught and reported through ref_last_error() (the reference throws).
 #include <cstdint>
 #include <cstring>
@@ -467,6 +468,50 @@ int ref_silhouette_iou(const double* pred, const double* gt, int64_t n, double d
     *loss = dr::silhouette_iou_loss(p, g);
     std::vector<double> d = dr::silhouette_iou_loss_backward(p, g, d_loss);
     std::memcpy(grad, d.data(), sizeof(double) * size_t(n));
+  });
+}
+
+// dr::packed_to_padded / padded_to_packed (batching.hpp:48-75) over rows of `row` doubles (T = a fixed-size row)
+extern "C++" {
+namespace {
+template <int R>
+struct Row {
+  double v[R];
+};
+template <int R>
+void p2pad(const double* data, const int64_t* offsets, int64_t B, double pad, double* out) {
+  dr::PackedView<Row<R>> pv;
+  pv.offsets.assign(offsets, offsets + B + 1);
+  pv.data.resize(size_t(offsets[B]));
+  std::memcpy(pv.data.data(), data, sizeof(double) * R * size_t(offsets[B]));
+  Row<R> p;
+  for (int k = 0; k < R; ++k) p.v[k] = pad;
+  std::vector<Row<R>> o = dr::packed_to_padded(pv, p);
+  std::memcpy(out, o.data(), sizeof(double) * R * o.size());
+}
+template <int R>
+void pad2p(const double* padded, int64_t B, int64_t max_count, const int64_t* counts, double* out, int32_t* ite) {
+  std::vector<Row<R>> pd(size_t(B * max_count));
+  std::memcpy(pd.data(), padded, sizeof(double) * R * pd.size());
+  dr::PackedView<Row<R>> pv = dr::padded_to_packed(pd, std::vector<int64_t>(counts, counts + B));
+  std::memcpy(out, pv.data.data(), sizeof(double) * R * pv.data.size());
+  for (size_t i = 0; i < pv.item_to_element.size(); ++i) ite[i] = pv.item_to_element[i];
+}
+}  // namespace
+}  // extern "C++"
+
+// row = 1 or 9 doubles per packed item; out = [B, max_count, row] (max over the element counts)
+int ref_packed_to_padded(const double* data, const int64_t* offsets, int64_t B, int32_t row, double pad, double* out) {
+  return guarded([&] {
+    if (row == 9) p2pad<9>(data, offsets, B, pad, out);
+    else p2pad<1>(data, offsets, B, pad, out);
+  });
+}
+int ref_padded_to_packed(const double* padded, int64_t B, int64_t max_count, const int64_t* counts, int32_t row,
+                         double* out, int32_t* item_to_element) {
+  return guarded([&] {
+    if (row == 9) pad2p<9>(padded, B, max_count, counts, out, item_to_element);
+    else pad2p<1>(padded, B, max_count, counts, out, item_to_element);
   });
 }
 
