@@ -293,6 +293,13 @@ int fwd_impl(const double* fv, const int64_t* first, const int64_t* num, int64_t
   if (nw == 0) return fail(DR_ERR_RANGE, "faces_per_pixel=%d too large for the shared-memory top-K", p.K);
   A.N = (int)N;
   A.work_counter = reinterpret_cast<unsigned long long*>(base + p.off_counter);
+  {
+    const int mtx = (p.bs + 7) >> 3, mty = (p.bs + 3) >> 2;  // micro-tiles per bin row / column (k_fine)
+    A.div_mt = drb::FastDivU32((uint32_t)(mtx * mty));
+    A.div_bins = drb::FastDivU32((uint32_t)(p.nbx * p.nby));
+    A.div_nbx = drb::FastDivU32((uint32_t)p.nbx);
+    A.div_mtx = drb::FastDivU32((uint32_t)mtx);
+  }
   A.p2f = p2f;
   A.zbuf = zbuf;
   A.bary = bary;

@@ -823,14 +823,23 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
     if (lane == 0) item = (int64_t)atomicAdd(A.work_counter, 1ull);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
-    const int mt = (int)(item % mt_per_bin);
-    const int64_t bb = item / mt_per_bin;
-    const int bin = (int)(bb % nbins);
-    const int b = (int)(bb / nbins);
-    const int by = bin / A.nbx, bx = bin % A.nbx;
+    int mt, bin, b;
+    if (n_items <= 0xffffffffll) {  // (uniform) 32-bit decode with precomputed reciprocals
+      const uint32_t it = (uint32_t)item, q1 = A.div_mt.div(it), q2 = A.div_bins.div(q1);
+      mt = (int)(it - q1 * (uint32_t)mt_per_bin);
+      bin = (int)(q1 - q2 * (uint32_t)nbins);
+      b = (int)q2;
+    } else {
+      mt = (int)(item % mt_per_bin);
+      const int64_t bb = item / mt_per_bin;
+      bin = (int)(bb % nbins);
+      b = (int)(bb / nbins);
+    }
+    const int by = (int)A.div_nbx.div((uint32_t)bin), bx = bin - by * A.nbx;
     const int bi0 = by * A.bs, bj0 = bx * A.bs;
     const int bi1 = min(A.H, bi0 + A.bs) - 1, bj1 = min(A.W, bj0 + A.bs) - 1;
-    const int mi0 = bi0 + (mt / mtx) * 4, mj0 = bj0 + (mt % mtx) * 8;
+    const int mtr = (int)A.div_mtx.div((uint32_t)mt);
+    const int mi0 = bi0 + mtr * 4, mj0 = bj0 + (mt - mtr * mtx) * 8;
     const int vh = min(4, bi1 - mi0 + 1), vw = min(8, bj1 - mj0 + 1);  // existing pixels of the micro-tile
     if (vh <= 0 || vw <= 0) continue;
     STAT_ADD(5, 1);
@@ -925,15 +934,27 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
     if constexpr (kMode == 0) {
       // fragment payload (MR:178-197), lanes over (pixel, slot) in output order: q = (row * 8 + col) * K + s, so
       // one step writes whole runs of consecutive slots of a micro-tile row (coalesced stores); the next step's
-      // face_verts are fetched before the current slot is evaluated
-      auto fetch = [&](int q, int32_t& f, double* v, int64_t& slot, double& z, double& qx, double& qy) {
+      // face_verts are fetched before the current slot is evaluated. A lane's (pixel, slot) advances by 32 slots per
+      // step incrementally (no integer division by K per step) and its output slot is the micro-tile's base plus
+      // 32-bit offsets.
+      const int64_t slot_base = (((int64_t)b * A.H + mi0) * A.W + mj0) * K;
+      const int row_stride = A.W * K;
+      const int dpix = 32 / K, ds = 32 - dpix * K;
+      int fpix = lane / K, fs = lane - fpix * K;  // (pixel, slot) of this lane's next fetch
+      auto fetch = [&](int32_t& f, double* v, int64_t& slot, double& z, double& qx, double& qy) {
+        const int pix = fpix, s = fs;
+        fs += ds;
+        fpix += dpix;
+        if (fs >= K) {
+          fs -= K;
+          ++fpix;
+        }
         f = INT_MAX;
         slot = -1;
-        if (q >= 32 * K) return;
-        const int pix = q / K, s = q - pix * K;
+        if (pix >= 32) return;
         const int row = pix >> 3, col = pix & 7;
         if (row >= vh || col >= vw) return;
-        slot = (((int64_t)b * A.H + mi0 + row) * A.W + mj0 + col) * K + s;
+        slot = slot_base + (int64_t)(row * row_stride + col * K + s);
         f = ws.tid[ws.li<(KMAX == 0)>(s, pix)];
         z = ws.tz[ws.li<(KMAX == 0)>(s, pix)];
         qx = ws.pxy[col];
@@ -946,7 +967,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
       int32_t fn;
       double vn[9], zn = 0.0, xn = 0.0, yn = 0.0;
       int64_t sn;
-      fetch(lane, fn, vn, sn, zn, xn, yn);
+      fetch(fn, vn, sn, zn, xn, yn);
       for (int q0 = 0; q0 < 32 * K; q0 += 32) {
         const int32_t f = fn;
         const int64_t slot = sn;
@@ -954,7 +975,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
         double v[9];
 #pragma unroll
         for (int t = 0; t < 9; ++t) v[t] = vn[t];
-        fetch(q0 + 32 + lane, fn, vn, sn, zn, xn, yn);
+        fetch(fn, vn, sn, zn, xn, yn);
         if (slot >= 0) emit_slot<OutT>(A, slot, f != INT_MAX, z, f, v, qx, qy);
       }
       __syncwarp();

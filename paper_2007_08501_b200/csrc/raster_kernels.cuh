@@ -20,6 +20,25 @@ struct BlendArgs {
   double znear = 0.1, zfar = 100.0;     // Camera.znear / zfar
 };
 
+// Unsigned 32-bit division by a run-time invariant divisor with one multiply-high (Granlund & Montgomery,
+// "Division by invariant integers using multiplication", Fig. 4.1): exact for every 32-bit dividend.
+struct FastDivU32 {
+  uint32_t d = 1, m = 1;
+  int sh1 = 0, sh2 = 0;
+  FastDivU32() = default;
+  explicit FastDivU32(uint32_t div) : d(div) {
+    int l = 0;
+    while (l < 32 && (1ull << l) < div) ++l;  // l = ceil(log2 d)
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+    sh1 = l < 1 ? l : 1;
+    sh2 = l - 1 > 0 ? l - 1 : 0;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    const uint32_t t1 = __umulhi(m, n);
+    return (t1 + ((n - t1) >> sh1)) >> sh2;
+  }
+};
+
 template <typename OutT>
 struct FineArgs {
   const double* fv;         // [F,3,3] face_verts
@@ -40,6 +59,8 @@ struct FineArgs {
   bool persp, clip;
   int N;
   unsigned long long* work_counter;  // zeroed before launch; warps pull micro-tiles from it
+  // micro-tile index -> (mesh, bin, micro-tile) without integer division instructions (set by the launcher)
+  FastDivU32 div_mt, div_bins, div_nbx, div_mtx;
   int64_t* p2f;
   OutT* zbuf;
   OutT* bary;
@@ -50,24 +71,6 @@ struct FineArgs {
   BlendArgs blend;
 };
 
-// Unsigned 32-bit division by a run-time invariant divisor with one multiply-high (Granlund & Montgomery,
-// "Division by invariant integers using multiplication", Fig. 4.1): exact for every 32-bit dividend.
-struct FastDivU32 {
-  uint32_t d = 1, m = 1;
-  int sh1 = 0, sh2 = 0;
-  FastDivU32() = default;
-  explicit FastDivU32(uint32_t div) : d(div) {
-    int l = 0;
-    while (l < 32 && (1ull << l) < div) ++l;  // l = ceil(log2 d)
-    m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
-    sh1 = l < 1 ? l : 1;
-    sh2 = l - 1 > 0 ? l - 1 : 0;
-  }
-  __device__ __forceinline__ uint32_t div(uint32_t n) const {
-    const uint32_t t1 = __umulhi(m, n);
-    return (t1 + ((n - t1) >> sh1)) >> sh2;
-  }
-};
 
 template <typename InT>
 struct BwdArgs {
