@@ -498,8 +498,13 @@ __host__ __device__ constexpr size_t warp_smem_bytes_cap(int K) {
 }
 // (the kernel uses the compile-time-capacity form: a runtime select in the warp's base offset cost ptxas ~20
 // registers and spills)
+// The register-list instantiations (KMAX = 1, 4, 8: the launcher's K thresholds) lay their lists out for KMAX
+// entries, so every per-warp array sits at a compile-time offset from the warp's base (one base register, immediate
+// offsets) instead of K-dependent run-time pointers the compiler rematerialises in the loops.
+__host__ __device__ constexpr int list_kmax(int K) { return K == 1 ? 1 : (K <= 4 ? 4 : (K <= 8 ? 8 : 0)); }
+__host__ __device__ constexpr int layout_k(int K) { return list_kmax(K) ? list_kmax(K) : K; }
 __host__ __device__ constexpr size_t warp_smem_bytes(int K) {
-  return K <= 8 ? warp_smem_bytes_cap<kBufReg>(K) : warp_smem_bytes_cap<kBufSmem>(K);
+  return K <= 8 ? warp_smem_bytes_cap<kBufReg>(layout_k(K)) : warp_smem_bytes_cap<kBufSmem>(K);
 }
 
 // Rectangle of the micro-tile (rows i0..i0+3, cols j0..j0+7, limited to vh x vw existing pixels) covered by
@@ -798,15 +803,16 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
   const int K = A.K;
   WarpSmem ws;
   {
-    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes_cap<kBufT<KMAX>>(K);
+    const int KL = KMAX > 0 ? KMAX : K;  // list layout (compile-time on the register path)
+    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes_cap<kBufT<KMAX>>(KL);
     ws.d = reinterpret_cast<double*>(base);
     ws.tz = ws.d + kNF * kRing;
-    ws.bz = ws.tz + (K + 1) * 32;
+    ws.bz = ws.tz + (KL + 1) * 32;
     ws.ls = K + 1;
     ws.pxy = ws.bz + kBufT<KMAX> * 32;  // == buf_cap(K): KMAX == 0 exactly when K > 8
     ws.fid = reinterpret_cast<int32_t*>(ws.pxy + 12);
     ws.tid = ws.fid + kRing;
-    ws.bid = ws.tid + (K + 1) * 32;
+    ws.bid = ws.tid + (KL + 1) * 32;
     ws.rect = reinterpret_cast<uint32_t*>(ws.bid + kBufT<KMAX> * 32);
     ws.fkey = reinterpret_cast<float*>(ws.rect + kRing);
     ws.bcnt = reinterpret_cast<int32_t*>(ws.fkey + kRing);
