@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restric
 // touch it are compacted (ballot + popc) into a warp-private ring in shared memory together with their
 // per-face invariants (structure-of-arrays) and their covered pixel rectangle. Every 32 staged faces the warp
 // enumerates their (face, pixel) pairs — prefix sum of the rectangle areas across lanes, then 32 pairs per
-// step, one per lane (binary search over the prefix with shuffles) — so every lane evaluates a pair
+// step, one per lane (the pair's face from a ballot and the block's face-start bits) — so every lane evaluates a pair
 // (MR:166-176) regardless of how small the triangles are. Passing candidates go into the pixel's sorted
 // (z, id) list in shared memory; lanes that hit the same pixel in one step insert one after another
 // (__match_any_sync ranks). Winners' bary / dists are recomputed with the identical operation sequence at
@@ -744,13 +744,14 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
       const int j = base + lane;
       const bool act = j < total;
       // face lane = first lane whose inclusive prefix exceeds j
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const int pv = __shfl_sync(0xffffffffu, incl, lo + step - 1);
-        if (pv <= j) lo += step;
-      }
-      lo = min(lo, 31);
+      // = (faces starting at or before `base`) - 1 + (faces starting in (base, j]): one ballot, one OR-reduction
+      // of the start bits of this block of 32 pairs, one popc per lane (staged faces are lanes < G, cnt >= 1).
+      // (It replaced a 5-step shuffle binary search over the prefix: C4 k_fine -1.3 %, C5 -3.2 %.)
+      const int excl_l = incl - cnt;
+      const int f0 = __popc(__ballot_sync(0xffffffffu, cnt > 0 && excl_l <= base)) - 1;
+      const unsigned starts = __reduce_or_sync(
+          0xffffffffu, (cnt > 0 && excl_l > base && excl_l < base + 32) ? (1u << (excl_l - base)) : 0u);
+      const int lo = min(max(f0 + __popc(starts & ((2u << lane) - 1u)), 0), 31);
       const int excl = __shfl_sync(0xffffffffu, incl - cnt, lo);
       const uint32_t r = __shfl_sync(0xffffffffu, rl, lo);
       bool keep = false;
