@@ -718,8 +718,8 @@ __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSm
 
 
 // Enumerate the (face, pixel) pairs of ring slots [head, head+G) (mod kRing): prefix sum of the covered
-// rectangle areas across lanes, then 32 pairs per step, one per lane (binary search over the prefix with
-// shuffles). Pairs the K-th-depth cull cannot rule out are compacted (ballot) into the warp's pair queue and
+// rectangle areas across lanes, then 32 pairs per step, one per lane (the pair's face from the block's face-start
+// bits). Pairs the K-th-depth cull cannot rule out are compacted (ballot) into the warp's pair queue and
 // evaluated 32 at a time, so culled pairs cost no fp64 work and evaluation steps keep every lane busy. The
 // queue is drained before returning (its entries name ring slots the caller recycles).
 template <int KMAX, typename OutT>
