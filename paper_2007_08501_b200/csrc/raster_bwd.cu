@@ -60,9 +60,12 @@ __device__ __forceinline__ void load_slot(const BwdArgs<InT>& A, int64_t slot, i
 // per-slot cotangents -> g[9] = (dx, dy, dz) for vertices a, b, c; p = the slot's pixel centre (MR:357)
 // kInternalW: the clamped barycentrics used by the z-interpolation term are derived here from the recomputed
 // weights (and returned in w_out) instead of being read from the forward's bary output (fused consumers)
-template <typename InT, bool kInternalW = false>
+// kPC / kCL: perspective_correct / clip_barycentric_coords fixed at compile time (0 / 1), or read from A (2): the
+// fixed instantiations carry only their own branch of the chain (smaller code: K3 is instruction-cache sensitive)
+template <typename InT, bool kInternalW = false, int kPC = 2, int kCL = 2>
 __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32_t fid, const SlotIn<InT>& in,
                                               double g[9], double* w_out = nullptr) {
+  const bool persp = kPC == 2 ? A.persp : kPC == 1, clip = kCL == 2 ? A.clip : kCL == 1;
   const FaceGeom fg = make_face_geom(in.v);
   const double z[3] = {fg.z0, fg.z1, fg.z2};
 
@@ -76,14 +79,14 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32
   double d_w[3], dzv[3] = {0.0, 0.0, 0.0};
   if constexpr (kInternalW) {  // w_hat = the forward's bary: clamp(persp(w_raw)) / clamp(w_raw) (MR:172)
     double u[3];
-    if (A.persp) {
+    if (persp) {
       persp_correct<false>(w_raw, fg.z0, fg.z1, fg.z2, u);
     } else {
       u[0] = w_raw[0];
       u[1] = w_raw[1];
       u[2] = w_raw[2];
     }
-    if (A.clip) {
+    if (clip) {
       clamp_barycentric<false>(u, w_hat);
     } else {
       w_hat[0] = u[0];
@@ -94,10 +97,10 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32
     w_out[1] = w_hat[1];
     w_out[2] = w_hat[2];
   }
-  if (A.persp) {  // builder-defined: u = persp_correct(w_raw, z); bary = clamp(u)
+  if (persp) {  // builder-defined: u = persp_correct(w_raw, z); bary = clamp(u)
     double u[3], d_u[3], d_top[3];
     const double den = persp_correct<false>(w_raw, fg.z0, fg.z1, fg.z2, u);
-    if (A.clip) {
+    if (clip) {
       clamp_bary_backward(u, d_hat, d_u);
     } else {
       d_u[0] = d_hat[0];
@@ -119,7 +122,7 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32
     dzv[0] = d_top[1] * w_raw[1] * z[2] + d_top[2] * w_raw[2] * z[1];
     dzv[1] = d_top[0] * w_raw[0] * z[2] + d_top[2] * w_raw[2] * z[0];
     dzv[2] = d_top[0] * w_raw[0] * z[1] + d_top[1] * w_raw[1] * z[0];
-  } else if (A.clip) {
+  } else if (clip) {
     clamp_bary_backward(w_raw, d_hat, d_w);  // MR:367
   } else {
     d_w[0] = d_hat[0];
@@ -203,12 +206,12 @@ constexpr int kBwdMinBlocks = 3;
 // 128 x 16 (36-byte spills) 2.54 ms, 155 x 12 2.48 ms; profiles/r01/README.md).
 constexpr int kBwdThreads = 128;
 
-template <typename InT>
+template <typename InT, int kPC, int kCL>
 __device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, V2 p, int32_t my_fid, const SlotIn<InT>& in,
                                                int lane) {
   double g[9];
   if (my_fid >= 0) {
-    slot_backward(A, p, my_fid, in, g);
+    slot_backward<InT, false, kPC, kCL>(A, p, my_fid, in, g);
   } else {
 #pragma unroll
     for (int k = 0; k < 9; ++k) g[k] = 0.0;
@@ -235,7 +238,7 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <typename InT>
+template <typename InT, int kPC, int kCL>
 __device__ __forceinline__ void backward_chunk(const BwdArgs<InT>& A, int64_t c0, int n, const uint16_t* qo,
                                                const int32_t* qf, const double* pix_tab, bool tab, int lane) {
   const int HW = A.H * A.W;
@@ -268,7 +271,7 @@ __device__ __forceinline__ void backward_chunk(const BwdArgs<InT>& A, int64_t c0
       const uint32_t i = A.divW.div(pp), j = pp - i * (uint32_t)A.W;
       p = tab ? V2{pix_tab[j], pix_tab[A.W + i]} : V2{pixel_x(A.W, (int)j), pixel_y(A.H, (int)i)};  // MR:357
     }
-    backward_batch(A, p, my_fid, cur, lane);
+    backward_batch<InT, kPC, kCL>(A, p, my_fid, cur, lane);
   }
 }
 
@@ -276,7 +279,7 @@ __device__ __forceinline__ void backward_chunk(const BwdArgs<InT>& A, int64_t c0
 // together and the CTA's registers are released without idle warps holding them). While a warp computes chunk
 // c, the pix_to_face words of its next chunk stream into shared memory with cp.async (no registers held);
 // the chunk is then compacted (occupied slots -> queue of 16-bit offsets + face ids) straight from shared memory.
-template <typename InT>
+template <typename InT, int kPC, int kCL>
 __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_backward(BwdArgs<InT> A) {
   constexpr int NWB = kBwdThreads / 32;
   __shared__ __align__(16) int64_t stage[NWB][kBwdChunk];
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_backward(BwdArgs
     if (lane == 0) kn = atomicAdd(&next_chunk, 1);
     kn = __shfl_sync(0xffffffffu, kn, 0);
     if (valid(kn)) issue(kn);  // overlaps this chunk's compute
-    backward_chunk(A, c0, n, qo, qf, pix_tab, A.W + A.H <= kPixTab, lane);
+    backward_chunk<InT, kPC, kCL>(A, c0, n, qo, qf, pix_tab, A.W + A.H <= kPixTab, lane);
     __syncwarp();
     k = kn;
   }
@@ -1210,8 +1213,13 @@ static cudaError_t launch_backward_t(const BwdArgs<InT>& A, cudaStream_t st) {
   // achievable warps per SM on C4
   const int64_t per_cta = (int64_t)kBwdChunk * kBwdChunksPerCta;
   const int64_t blocks = std::min<int64_t>((A.S + per_cta - 1) / per_cta, INT32_MAX);
-  k_backward<InT><<<(unsigned)blocks, kBwdThreads, 0, st>>>(A);
-  return cudaGetLastError();
+  // one instantiation per (perspective_correct, clip_barycentric_coords)
+  auto go = [&](auto kern) {
+    kern<<<(unsigned)blocks, kBwdThreads, 0, st>>>(A);
+    return cudaGetLastError();
+  };
+  if (A.persp) return A.clip ? go(k_backward<InT, 1, 1>) : go(k_backward<InT, 1, 0>);
+  return A.clip ? go(k_backward<InT, 0, 1>) : go(k_backward<InT, 0, 0>);
 }
 
 cudaError_t launch_backward(const BwdArgs<float>& A, cudaStream_t st) { return launch_backward_t(A, st); }
