@@ -522,13 +522,13 @@ __device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0
 
 template <typename OutT>
 __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot, bool occupied, double z,
-                                          int32_t fid, const double* v, double px, double py) {
+                                          int32_t fid, const double* v, double px, double py, bool persp) {
   if (occupied) {
     const FaceGeom g = make_face_geom(v);
     PixelFaceResult r;
     // fp64 payload: the identical operation sequence => the bits the candidate test produced; fp32 payload: the
     // same formulas with fast (<= 1 ulp) divisions, rounded once to fp32 (selection is already decided)
-    eval_pixel_face<true, std::is_same<OutT, double>::value>(V2{px, py}, g, A.blur, A.znear, A.persp, A.clip, r);
+    eval_pixel_face<true, std::is_same<OutT, double>::value>(V2{px, py}, g, A.blur, A.znear, persp, A.clip, r);
     A.p2f[slot] = fid;
     A.zbuf[slot] = (OutT)z;
     A.bary[3 * slot + 0] = (OutT)r.bary[0];
@@ -695,7 +695,8 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
 
 // Evaluate the first n (<= 32) queued (face slot, pixel) pairs, one per lane, and insert the survivors.
 template <int KMAX, typename OutT>
-__device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSmem& ws, int n, int lane) {
+__device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSmem& ws, int n, int lane,
+                                           bool persp) {
   const uint32_t e = lane < n ? ws.pairq[lane] : 0x80000000u;
   const bool act = lane < n;
   bool pass = false;
@@ -707,7 +708,7 @@ __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSm
     p = (int)(e & 31u);
     const FaceGeom fg = ws.geom(k);
     const V2 pix{ws.pxy[p & 7], ws.pxy[8 + (p >> 3)]};
-    pass = eval_pixel_face<false>(pix, fg, A.blur, A.znear, A.persp, A.clip, res);
+    pass = eval_pixel_face<false>(pix, fg, A.blur, A.znear, persp, A.clip, res);
     f = ws.fid[k];
   }
   STAT_ADD(3, __popc(__ballot_sync(0xffffffffu, act)));
@@ -724,7 +725,7 @@ __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSm
 // queue is drained before returning (its entries name ring slots the caller recycles).
 template <int KMAX, typename OutT>
 __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const WarpSmem& ws, int head, int G,
-                                              int lane) {
+                                              int lane, bool persp) {
   const int K = A.K;
   const int slot_l = (head + lane) % kRing;
   const uint32_t rl = lane < G ? ws.rect[slot_l] : 0u;
@@ -779,7 +780,7 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
     const bool drain = base >= total;
     if (qn >= 32 || (drain && qn > 0)) {
       const int n = min(qn, 32);
-      eval_pairs<KMAX>(A, ws, n, lane);
+      eval_pairs<KMAX>(A, ws, n, lane, persp);
       qn -= n;
       if (qn > 0) {  // move the remainder to the front
         const uint32_t t = lane < qn ? ws.pairq[32 + lane] : 0u;
@@ -797,11 +798,14 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
 // kMode: 0 = the fragment payload; 1 = fused silhouette emit (alpha, optional pix_to_face); 2 = fused softmax
 // render emit (interpolated vertex colours + softmax_blend -> image, optional pix_to_face) — separate
 // instantiations so the fragment path's code (and register allocation) does not carry them
-template <typename OutT, int NW, int KMAX, int kMode>
+// kPC: perspective_correct fixed at compile time (0 / 1) for the fragment instantiations, read from A (2) for the
+// fused consumers (their own instantiations already multiply the kernel count)
+template <typename OutT, int NW, int KMAX, int kMode, int kPC = 2>
 __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
+  const bool persp = kPC == 2 ? A.persp : kPC == 1;
   WarpSmem ws;
   {
     const int KL = KMAX > 0 ? KMAX : K;  // list layout (compile-time on the register path)
@@ -918,7 +922,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
         bool ran = false;
         while (pending >= 32 || (last && todo == 0u && pending > 0)) {
           const int G = min(pending, 32);
-          process_group<KMAX>(A, ws, head, G, lane);
+          process_group<KMAX>(A, ws, head, G, lane, persp);
           head = (head + G) % kRing;
           pending -= G;
           ran = true;
@@ -983,7 +987,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
 #pragma unroll
         for (int t = 0; t < 9; ++t) v[t] = vn[t];
         fetch(fn, vn, sn, zn, xn, yn);
-        if (slot >= 0) emit_slot<OutT>(A, slot, f != INT_MAX, z, f, v, qx, qy);
+        if (slot >= 0) emit_slot<OutT>(A, slot, f != INT_MAX, z, f, v, qx, qy, persp);
       }
       __syncwarp();
       continue;
@@ -1039,7 +1043,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
             acc[2] += c[2] * w;
           }
         } else {
-          emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[ws.li<(KMAX == 0)>(s, lane)], f, v, px, py);
+          emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[ws.li<(KMAX == 0)>(s, lane)], f, v, px, py, persp);
         }
       }
       if constexpr (kMode == 1) A.alpha[((int64_t)b * A.H + pi) * A.W + pj] = (OutT)(1.0 - keep);  // shading.cpp:86
@@ -1155,10 +1159,16 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
         return cudaErrorInvalidValue;
       }
     }
-    if (A.K == 1) return go(k_fine<OutT, NW, 1, 0>);
-    if (A.K <= 4) return go(k_fine<OutT, NW, 4, 0>);
-    if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0>);
-    return go(k_fine<OutT, NW, 0, 0>);
+    if (A.persp) {
+      if (A.K == 1) return go(k_fine<OutT, NW, 1, 0, 1>);
+      if (A.K <= 4) return go(k_fine<OutT, NW, 4, 0, 1>);
+      if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0, 1>);
+      return go(k_fine<OutT, NW, 0, 0, 1>);
+    }
+    if (A.K == 1) return go(k_fine<OutT, NW, 1, 0, 0>);
+    if (A.K <= 4) return go(k_fine<OutT, NW, 4, 0, 0>);
+    if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0, 0>);
+    return go(k_fine<OutT, NW, 0, 0, 0>);
   };
   if (nw == 8) return by_k(std::integral_constant<int, 8>{});
   return by_k(std::integral_constant<int, 2>{});
