@@ -292,6 +292,97 @@ constexpr int kSortThreads = 256;
 constexpr int kSortBuckets = kSortThreads * kSortBpt;
 static_assert(kSortBuckets == kSortBucketsH, "bucket count shared with the point fine stage");
 
+// Short bins (<= kWarpSortMax entries, most of them): one WARP per bin, no CTA barrier. The warp reads the bin's
+// (id, key) pairs into registers (8 per lane), reduces the depth range with shuffles, counts kWarpSortBuckets
+// linear buckets in its own shared-memory histogram, scans it (8 buckets per lane), scatters the re-packed entries
+// back in place. Bucket map (lo, scale) as for the CTA sort, so the point stage's exit bound stays valid.
+constexpr int kWarpSortMax = 256;
+constexpr int kWarpSortPer = kWarpSortMax / 32;
+constexpr int kWarpSortBuckets = 256;
+constexpr int kWarpSortWarps = 8;
+__global__ void __launch_bounds__(kWarpSortWarps * 32) k_sort_bins_warp(const int* __restrict__ counts,
+                                                                     const int64_t* __restrict__ off,
+                                                                     int4* __restrict__ entries,
+                                                                     const int4* __restrict__ ibbox,
+                                                                     int64_t nbins_total, int64_t pool, int cap,
+                                                                     float2* __restrict__ brange) {
+  __shared__ unsigned hist_all[kWarpSortWarps][kWarpSortBuckets];
+  const int lane = threadIdx.x & 31;
+  unsigned* hist = hist_all[threadIdx.x >> 5];
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpSortWarps;
+  // warp w owns bins w, w + nwarps, ...; 32 of its counts are read at once and the in-range ones kept
+  for (int64_t k0 = (int64_t)blockIdx.x * kWarpSortWarps + (threadIdx.x >> 5); k0 < nbins_total; k0 += 32 * nwarps) {
+    const int64_t mybin = k0 + (int64_t)lane * nwarps;
+    bool in = false;
+    if (mybin < nbins_total) {
+      const int c = counts[mybin];
+      in = c > 0 && c <= kWarpSortMax && bin_is_sorted(off[mybin], c, pool, cap);
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, in);
+    while (todo) {
+      const int64_t bin = k0 + (int64_t)(__ffs(todo) - 1) * nwarps;
+      todo &= todo - 1;
+      const int c = counts[bin];
+      int4* L = entries + off[bin];
+      int fid[kWarpSortPer];
+      float key[kWarpSortPer];
+      float lo = __int_as_float(0x7f800000), hi = -lo;
+#pragma unroll
+      for (int t = 0; t < kWarpSortPer; ++t) {
+        const int i = t * 32 + lane;
+        fid[t] = -1;
+        key[t] = 0.f;
+        if (i < c) {
+          const int2 fk = *reinterpret_cast<const int2*>(L + i);  // {face id, zkey bits}
+          fid[t] = fk.x;
+          key[t] = __int_as_float(fk.y);
+          lo = fminf(lo, key[t]);
+          hi = fmaxf(hi, key[t]);
+        }
+      }
+      for (int d = 16; d; d >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+      }
+      const float scale = hi > lo ? (float)kWarpSortBuckets * 0.99999f / (hi - lo) : 0.f;
+      if (brange && lane == 0) brange[bin] = make_float2(lo, scale);  // the bucket map (sort_bucket stays < 256)
+#pragma unroll
+      for (int j = 0; j < kWarpSortBuckets / 32; ++j) hist[lane * (kWarpSortBuckets / 32) + j] = 0;
+      __syncwarp();
+      int bk[kWarpSortPer];
+#pragma unroll
+      for (int t = 0; t < kWarpSortPer; ++t) {
+        bk[t] = min(kWarpSortBuckets - 1, sort_bucket(key[t], lo, scale));
+        if (fid[t] >= 0) atomicAdd(&hist[bk[t]], 1u);
+      }
+      __syncwarp();
+      {  // exclusive scan: lane l holds buckets [8 l, 8 l + 8)
+        constexpr int PB = kWarpSortBuckets / 32;
+        unsigned v[PB], tot = 0;
+#pragma unroll
+        for (int j = 0; j < PB; ++j) { v[j] = hist[lane * PB + j]; tot += v[j]; }
+        unsigned x = tot;
+        for (int d = 1; d < 32; d <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
+        }
+        unsigned base = x - tot;
+#pragma unroll
+        for (int j = 0; j < PB; ++j) { hist[lane * PB + j] = base; base += v[j]; }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < kWarpSortPer; ++t) {
+        if (fid[t] >= 0) {
+          const int pos = (int)atomicAdd(&hist[bk[t]], 1u);
+          L[pos] = make_bin_entry(fid[t], key[t], __ldg(ibbox + fid[t]));
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // MAXN = shared-memory capacity in entries; bins with (MINN, MAXN] entries are sorted by this instantiation
 template <int MAXN, int MINN, bool kDyn>
 __global__ void __launch_bounds__(kSortThreads) k_sort_bins(const int* __restrict__ counts,
@@ -1106,8 +1197,10 @@ cudaError_t launch_sort_bins(const int* counts, const int64_t* off, int4* entrie
                              int64_t nbins_total, int64_t pool, int cap, cudaStream_t st, float2* bin_range) {
   if (nbins_total <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nbins_total, 148 * 16);
-  k_sort_bins<kSortMax, 0, false><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox, nbins_total, pool, cap,
-                                                                 bin_range);
+  k_sort_bins_warp<<<(unsigned)std::min<int64_t>((nbins_total + kWarpSortWarps - 1) / kWarpSortWarps, 148 * 8),
+                     kWarpSortWarps * 32, 0, st>>>(counts, off, entries, ibbox, nbins_total, pool, cap, bin_range);
+  k_sort_bins<kSortMax, kWarpSortMax, false><<<grid, kSortThreads, 0, st>>>(counts, off, entries, ibbox,
+                                                                            nbins_total, pool, cap, bin_range);
   auto big = k_sort_bins<kSortMaxBig, kSortMax, true>;
   const int smem = kSortMaxBig * (int)sizeof(unsigned long long);
   cudaError_t e = cudaFuncSetAttribute(big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
