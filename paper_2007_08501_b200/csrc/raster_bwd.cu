@@ -938,6 +938,178 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
   }
 }
 
+// Split form, pass 4 without the geometry chain: lane per pixel as in k_softmax_backward, but the slot's
+// cotangents on the fragment (d_zbuf, d_dists, d_bary_i = d_col . colour(v_i)) and its clamped barycentrics are
+// written to fp32 scratch for K3 (k_backward, the same per-slot chain, MR:345-378), and only the vertex-colour
+// cotangent (interpolate_face_attributes_backward, shading.cpp:46-72) is reduced here. Passes 1-3 keep d_what =
+// d_image . colour per slot instead of the colour itself, so the barycentrics fit in the freed arrays.
+__global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_coef(SoftBwdArgs A, SoftCoefOut O) {
+  extern __shared__ double coef_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int K = A.K;
+  const size_t per_warp = (size_t)K * 32 * 4 + (size_t)K * 16 + (size_t)K * 32 * 3 / 2;  // doubles
+  double* ZI = coef_smem + (size_t)wid * per_warp;  // [K][32] zinv (-1: empty slot; +2: clamped)
+  double* PR = ZI + K * 32;                         // [K][32] prob
+  double* WT = PR + K * 32;                         // [K][32] softmax weight
+  double* DW = WT + K * 32;                         // [K][32] d_image . colour
+  float* B0 = reinterpret_cast<float*>(DW + K * 32);  // [K][32] clamped barycentrics (fp32: they go to fp32 scratch)
+  float* B1 = B0 + K * 32;
+  float* B2 = B1 + K * 32;
+  int32_t* FID = reinterpret_cast<int32_t*>(B2 + K * 32);  // [32][K] the warp's pix_to_face block
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t HW = (int64_t)A.H * A.W;
+  const double zrange = A.blend.zfar - A.blend.znear;
+  for (int64_t base = warp * 32; base < A.npix; base += nwarps * 32) {
+    const int64_t pix = base + lane;
+    double dimg[3] = {0.0, 0.0, 0.0};
+    if (pix < A.npix) {
+      dimg[0] = (double)A.d_image[3 * pix];
+      dimg[1] = (double)A.d_image[3 * pix + 1];
+      dimg[2] = (double)A.d_image[3 * pix + 2];
+    }
+    {
+      const int64_t n = (A.npix - base < 32 ? A.npix - base : 32) * K;
+      const int64_t* src = A.p2f + base * K;
+      for (int t = lane; t < 32 * K; t += 32) {
+        const int64_t f = t < n ? __ldcs(src + t) : -1;
+        FID[t] = (f >= 0 && f < A.F) ? (int32_t)f : -1;
+      }
+      __syncwarp();
+    }
+    const int32_t* row = FID + lane * K;
+    const int rem = pix < A.npix ? (int)(pix % HW) : 0;
+    const int i = rem / A.W, j = rem - (rem / A.W) * A.W;
+    const V2 p{pixel_x(A.W, j), pixel_y(A.H, i)};
+    // pass 1: slot evaluation (fast divisions), zinv_max / argmax (shading.cpp:185-197), opacity, d_image . colour
+    double zinv_max = -1.0;
+    int argmax = -1;
+    bool any = false;
+    for (int s = 0; s < K; ++s) {
+      const int32_t f = pix < A.npix ? row[s] : -1;
+      double zi = -1.0;
+      if (f >= 0) {
+        any = true;
+        double v[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)f + t);
+        const FaceGeom g = make_face_geom(v);
+        PixelFaceResult r;
+        eval_pixel_face<true, false>(p, g, A.blur, A.znear, A.persp, A.clip, r);
+        bool clamped;
+        zi = blend_zinv_b(r.z, A.blend, clamped);
+        if (argmax < 0) {  // the first occupied slot (see k_softmax_backward)
+          zinv_max = zi;
+          argmax = s;
+        }
+        double c[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {  // interpolate_face_attributes (shading.cpp:21-29)
+          const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)f + q];
+          c[0] += r.bary[q] * __ldg(a);
+          c[1] += r.bary[q] * __ldg(a + 1);
+          c[2] += r.bary[q] * __ldg(a + 2);
+        }
+        DW[s * 32 + lane] = dimg[0] * c[0] + dimg[1] * c[1] + dimg[2] * c[2];
+        B0[s * 32 + lane] = (float)r.bary[0];
+        B1[s * 32 + lane] = (float)r.bary[1];
+        B2[s * 32 + lane] = (float)r.bary[2];
+        PR[s * 32 + lane] = 1.0 / (1.0 + exp(r.dist / A.blend.sigma));  // sigmoid(-dists / sigma)
+        if (clamped) zi += 2.0;
+      }
+      ZI[s * 32 + lane] = zi;
+    }
+    // pass 2: weights and their sum (shading.cpp:202-209)
+    double wsum = 0.0;
+    for (int s = 0; s < K; ++s) {
+      double zi = ZI[s * 32 + lane];
+      if (zi < -0.5) continue;
+      if (zi > 1.5) zi -= 2.0;
+      const double w = PR[s * 32 + lane] * exp((zi - zinv_max) / A.blend.gamma);
+      WT[s * 32 + lane] = w;
+      wsum += w;
+    }
+    // pass 3: the mean term (shading.cpp:218-222) and d_zinv_max (shading.cpp:228)
+    double mean_term = 0.0;
+    for (int s = 0; s < K; ++s) {
+      if (ZI[s * 32 + lane] < -0.5) continue;
+      mean_term += DW[s * 32 + lane] * (WT[s * 32 + lane] / wsum);
+    }
+    double d_zinv_max = 0.0;
+    for (int s = 0; s < K; ++s) {
+      if (ZI[s * 32 + lane] < -0.5) continue;
+      const double w = WT[s * 32 + lane];
+      const double d_w = (DW[s * 32 + lane] - mean_term) / wsum;
+      d_zinv_max += -d_w * w / A.blend.gamma;
+    }
+    // pass 4: per-slot cotangents to scratch, vertex-colour cotangent reduced and accumulated
+    const int64_t slot0 = pix * K;
+    for (int s = 0; s < K; ++s) {
+      const double zis = (pix < A.npix && any) ? ZI[s * 32 + lane] : -1.0;
+      int32_t fid = -1;
+      double gc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) gc[k] = 0.0;
+      if (zis >= -0.5) {
+        fid = row[s];
+        const bool clamped = zis > 1.5;
+        const double w = WT[s * 32 + lane], pr = PR[s * 32 + lane];
+        const double what = w / wsum;
+        const double d_col[3] = {dimg[0] * what, dimg[1] * what, dimg[2] * what};
+        const double d_w = (DW[s * 32 + lane] - mean_term) / wsum;
+        const double d_prob = d_w * w / pr;
+        const double d_zinv = d_w * w / A.blend.gamma;
+        const double d_dists = d_prob * (-pr * (1.0 - pr) / A.blend.sigma);
+        double d_zbuf = clamped ? 0.0 : d_zinv * (-1.0 / zrange);
+        if (s == argmax && !clamped) d_zbuf += d_zinv_max * (-1.0 / zrange);
+        const double wh[3] = {(double)B0[s * 32 + lane], (double)B1[s * 32 + lane], (double)B2[s * 32 + lane]};
+        const int64_t slot = slot0 + s;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)fid + q];
+          O.d_bary[3 * slot + q] = (float)(d_col[0] * __ldg(a) + d_col[1] * __ldg(a + 1) + d_col[2] * __ldg(a + 2));
+          O.bary[3 * slot + q] = (float)wh[q];
+          gc[3 * q + 0] = wh[q] * d_col[0];
+          gc[3 * q + 1] = wh[q] * d_col[1];
+          gc[3 * q + 2] = wh[q] * d_col[2];
+        }
+        O.d_zbuf[slot] = (float)d_zbuf;
+        O.d_dists[slot] = (float)d_dists;
+      }
+      if (reduce_by_face<9>(fid, lane, gc)) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          double* oc = A.grad_colors + 3 * A.blend.faces[3 * (int64_t)fid + q];
+          for (int d = 0; d < 3; ++d)
+            if (gc[3 * q + d] != 0.0) atomicAdd(oc + d, gc[3 * q + d]);
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_softmax_coef(const SoftBwdArgs& A, const SoftCoefOut& O, cudaStream_t st) {
+  if (A.npix <= 0) return cudaSuccess;
+  if (A.K > kSoftCoefMaxK) return cudaErrorInvalidConfiguration;
+  const size_t per_warp = ((size_t)A.K * 32 * 4 + (size_t)A.K * 16 + (size_t)A.K * 32 * 3 / 2) * sizeof(double);
+  const int warps = (int)std::min<size_t>(kSoftThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));
+  const size_t smem = per_warp * warps;
+  cudaError_t e = cudaFuncSetAttribute(k_softmax_coef, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(smem, 48 * 1024));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_softmax_coef, warps * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int64_t blocks = (int64_t)sms * per_sm;
+  const int64_t need = (A.npix + warps * 32 - 1) / (warps * 32);
+  if (blocks > need) blocks = need;
+  k_softmax_coef<<<(unsigned)blocks, warps * 32, smem, st>>>(A, O);
+  return cudaGetLastError();
+}
+
 // Slot-compacted variant: a warp takes P = min(32, 512 / K) consecutive pixels; their occupied slots are queued
 // and the two geometry-heavy passes run lane-per-slot, 32 occupied slots per step:
 //   B  per slot: exact-sequence re-evaluation (fast divisions), inverse depth, opacity, interpolated colour

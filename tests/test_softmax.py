@@ -44,13 +44,18 @@ def test_softmax_render_vs_reference(name, H, K, blur, sigma, gamma, reflib, cud
     d_img = np.random.default_rng(5).standard_normal(img_ref.shape).astype(np.float32)
     dv_ref, dc_ref = reflib.softmax_render_backward(rb, cam.packed(), H, H, K, blur, vc, sigma, gamma,
                                                     d_img.astype(np.float64), bg)
-    g_fv, g_vc = rasterize_softmax_backward(dev(fv), dev(first), dev(num), rs, bp, dev(vc), dev(faces), p2f,
-                                            dev(d_img))
-    d_got = S.scatter_face_grads(m, cam, g_fv.cpu().numpy())
     assert np.abs(dv_ref).max() > 0 and np.abs(dc_ref).max() > 0
-    assert rel_err(d_got, dv_ref) < 1e-4, f"{name}: d_verts rel err {rel_err(d_got, dv_ref):.2e}"
-    grad_close(d_got, dv_ref, name)
-    assert rel_err(g_vc.cpu().numpy(), dc_ref) < 1e-6, f"{name}: d_colors rel err {rel_err(g_vc.cpu().numpy(), dc_ref):.2e}"
+    # K <= 16: the split form (blend cotangents through fp32 scratch into the rasterizer's backward kernel) and the
+    # fused one; K > 16 has the fused slot-compacted kernel only
+    for split in ((True, False) if K <= 16 else (True,)):
+        g_fv, g_vc = rasterize_softmax_backward(dev(fv), dev(first), dev(num), rs, bp, dev(vc), dev(faces), p2f,
+                                                dev(d_img), split=split)
+        d_got = S.scatter_face_grads(m, cam, g_fv.cpu().numpy())
+        what = f"{name} split={split}"
+        assert rel_err(d_got, dv_ref) < 1e-4, f"{what}: d_verts rel err {rel_err(d_got, dv_ref):.2e}"
+        grad_close(d_got, dv_ref, what)
+        assert rel_err(g_vc.cpu().numpy(), dc_ref) < 1e-6, \
+            f"{what}: d_colors rel err {rel_err(g_vc.cpu().numpy(), dc_ref):.2e}"
 
 
 def test_softmax_autograd_and_errors(cuda):
