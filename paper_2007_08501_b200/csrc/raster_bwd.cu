@@ -199,11 +199,11 @@ __device__ __forceinline__ bool reduce_by_face(int32_t fid, int lane, double g[N
 // typically 40-70 % of them) are compacted with ballot + popc into a warp-private queue and processed 32 at
 // a time, so every lane of a batch does a full per-slot backward.
 constexpr int kBwdChunk = 32 * 16;
-constexpr int kBwdMinBlocks = 3;
-// 128-thread CTAs, 3 per SM (155 registers, no spills): with the cp.async pix_to_face prefetch and the
-// one-batch-ahead input loads, latency is hidden by ILP rather than by more resident warps (C4: 80 registers x
-// 24 warps 3.47 ms, 96 x 20 3.33 ms, 128 x 16 3.10 ms with the first design; with the prefetching one
-// 128 x 16 (36-byte spills) 2.54 ms, 155 x 12 2.48 ms; profiles/r01/README.md).
+constexpr int kBwdMinBlocks = 4;
+// 128-thread CTAs, 4 per SM (128 registers, no spills since the (perspective_correct, clip) instantiations; C4
+// 2.44 -> 2.29 ms against 3 per SM at 155 registers). Round 1: 80 registers x 24 warps 3.47 ms, 96 x 20 3.33 ms,
+// 128 x 16 3.10 ms with the first design; with the prefetching one 128 x 16 (36-byte spills) 2.54 ms, 155 x 12
+// 2.48 ms (profiles/r01/README.md, profiles/r02/README.md).
 constexpr int kBwdThreads = 128;
 
 template <typename InT, int kPC, int kCL>
