@@ -613,13 +613,14 @@ __device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0
 
 template <typename OutT>
 __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot, bool occupied, double z,
-                                          int32_t fid, const double* v, double px, double py, bool persp) {
+                                          int32_t fid, const double* v, double px, double py, bool persp,
+                                          bool clip) {
   if (occupied) {
     const FaceGeom g = make_face_geom(v);
     PixelFaceResult r;
     // fp64 payload: the identical operation sequence => the bits the candidate test produced; fp32 payload: the
     // same formulas with fast (<= 1 ulp) divisions, rounded once to fp32 (selection is already decided)
-    eval_pixel_face<true, std::is_same<OutT, double>::value>(V2{px, py}, g, A.blur, A.znear, persp, A.clip, r);
+    eval_pixel_face<true, std::is_same<OutT, double>::value>(V2{px, py}, g, A.blur, A.znear, persp, clip, r);
     A.p2f[slot] = fid;
     A.zbuf[slot] = (OutT)z;
     A.bary[3 * slot + 0] = (OutT)r.bary[0];
@@ -779,7 +780,7 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
 // Evaluate the first n (<= 32) queued (face slot, pixel) pairs, one per lane, and insert the survivors.
 template <int KMAX, typename OutT>
 __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSmem& ws, int n, int lane,
-                                           bool persp) {
+                                           bool persp, bool clip) {
   const uint32_t e = lane < n ? ws.pairq[lane] : 0x80000000u;
   const bool act = lane < n;
   bool pass = false;
@@ -791,7 +792,7 @@ __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSm
     p = (int)(e & 31u);
     const FaceGeom fg = ws.geom(k);
     const V2 pix{ws.pxy[p & 7], ws.pxy[8 + (p >> 3)]};
-    pass = eval_pixel_face<false>(pix, fg, A.blur, A.znear, persp, A.clip, res);
+    pass = eval_pixel_face<false>(pix, fg, A.blur, A.znear, persp, clip, res);
     f = ws.fid[k];
   }
   STAT_ADD(3, __popc(__ballot_sync(0xffffffffu, act)));
@@ -808,7 +809,7 @@ __device__ __forceinline__ void eval_pairs(const FineArgs<OutT>& A, const WarpSm
 // queue is drained before returning (its entries name ring slots the caller recycles).
 template <int KMAX, typename OutT>
 __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const WarpSmem& ws, int head, int G,
-                                              int lane, bool persp) {
+                                              int lane, bool persp, bool clip) {
   const int K = A.K;
   const int slot_l = (head + lane) % kRing;
   const uint32_t rl = lane < G ? ws.rect[slot_l] : 0u;
@@ -850,7 +851,7 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
         const int k = (head + lo) % kRing;
         // K-th-depth cull: every z this face can produce is > its key; if the key already exceeds the pixel's
         // current K-th candidate the face cannot enter the pixel's list (strict (z, id) order, MR:138-140)
-        keep = !A.zsort || !((double)ws.fkey[k] > ws.tz[ws.li<(KMAX == 0)>(K - 1, p)]);
+        keep = !clip || !((double)ws.fkey[k] > ws.tz[ws.li<(KMAX == 0)>(K - 1, p)]);  // zsort == clip
         entry = ((uint32_t)k << 5) | (uint32_t)p;
       }
       STAT_ADD(2, __popc(__ballot_sync(0xffffffffu, act)));
@@ -863,7 +864,7 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
     const bool drain = base >= total;
     if (qn >= 32 || (drain && qn > 0)) {
       const int n = min(qn, 32);
-      eval_pairs<KMAX>(A, ws, n, lane, persp);
+      eval_pairs<KMAX>(A, ws, n, lane, persp, clip);
       qn -= n;
       if (qn > 0) {  // move the remainder to the front
         const uint32_t t = lane < qn ? ws.pairq[32 + lane] : 0u;
@@ -883,12 +884,14 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
 // instantiations so the fragment path's code (and register allocation) does not carry them
 // kPC: perspective_correct fixed at compile time (0 / 1) for the fragment instantiations, read from A (2) for the
 // fused consumers (their own instantiations already multiply the kernel count)
-template <typename OutT, int NW, int KMAX, int kMode, int kPC = 2>
+template <typename OutT, int NW, int KMAX, int kMode, int kPC = 2, int kCL = 2>
 __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
   const bool persp = kPC == 2 ? A.persp : kPC == 1;
+  // clip_barycentric_coords; the depth-ordered bins and K-th-depth culling are on exactly when it is (make_plan)
+  const bool clip = kCL == 2 ? A.clip : kCL == 1;
   WarpSmem ws;
   {
     const int KL = KMAX > 0 ? KMAX : K;  // list layout (compile-time on the register path)
@@ -984,10 +987,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
           ib = entry_ibbox(e);
         } else {
           fid = (int32_t)(f0 + ci);
-          key = A.zsort ? A.zkey[fid] : 0.f;
+          key = clip ? A.zkey[fid] : 0.f;
           ib = A.ibbox[fid];
         }
-        if (!A.zsort || !((double)key > T)) r = cover_rect(ib, mi0, mj0, vh, vw);
+        if (!clip || !((double)key > T)) r = cover_rect(ib, mi0, mj0, vh, vw);
       }
       unsigned todo = __ballot_sync(0xffffffffu, r != 0u);
       const bool last = c0 + 32 >= nsrc;
@@ -1005,7 +1008,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
         bool ran = false;
         while (pending >= 32 || (last && todo == 0u && pending > 0)) {
           const int G = min(pending, 32);
-          process_group<KMAX>(A, ws, head, G, lane, persp);
+          process_group<KMAX>(A, ws, head, G, lane, persp, clip);
           head = (head + G) % kRing;
           pending -= G;
           ran = true;
@@ -1014,7 +1017,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
           __syncwarp();
           merge_buffers<KMAX>(ws, K, lane);
           __syncwarp();
-          if (A.zsort) {  // max of the K-th depths (the list tails alone are a valid, looser threshold)
+          if (clip) {  // max of the K-th depths (the list tails alone are a valid, looser threshold)
             double t = valid_px ? ws.tz[ws.li<(KMAX == 0)>(K - 1, lane)] : -pos_inf();
 #pragma unroll
             for (int d = 16; d >= 1; d >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, d));
@@ -1070,7 +1073,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
 #pragma unroll
         for (int t = 0; t < 9; ++t) v[t] = vn[t];
         fetch(fn, vn, sn, zn, xn, yn);
-        if (slot >= 0) emit_slot<OutT>(A, slot, f != INT_MAX, z, f, v, qx, qy, persp);
+        if (slot >= 0) emit_slot<OutT>(A, slot, f != INT_MAX, z, f, v, qx, qy, persp, clip);
       }
       __syncwarp();
       continue;
@@ -1126,7 +1129,8 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
             acc[2] += c[2] * w;
           }
         } else {
-          emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[ws.li<(KMAX == 0)>(s, lane)], f, v, px, py, persp);
+          emit_slot<OutT>(A, slot0 + s, f != INT_MAX, ws.tz[ws.li<(KMAX == 0)>(s, lane)], f, v, px, py, persp,
+                          clip);
         }
       }
       if constexpr (kMode == 1) A.alpha[((int64_t)b * A.H + pi) * A.W + pj] = (OutT)(1.0 - keep);  // shading.cpp:86
@@ -1244,16 +1248,18 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
         return cudaErrorInvalidValue;
       }
     }
-    if (A.persp) {
-      if (A.K == 1) return go(k_fine<OutT, NW, 1, 0, 1>);
-      if (A.K <= 4) return go(k_fine<OutT, NW, 4, 0, 1>);
-      if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0, 1>);
-      return go(k_fine<OutT, NW, 0, 0, 1>);
-    }
-    if (A.K == 1) return go(k_fine<OutT, NW, 1, 0, 0>);
-    if (A.K <= 4) return go(k_fine<OutT, NW, 4, 0, 0>);
-    if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0, 0>);
-    return go(k_fine<OutT, NW, 0, 0, 0>);
+    // fragment payload: one instantiation per (perspective_correct, clip_barycentric_coords)
+    auto by_flags = [&](auto pc, auto cl) -> cudaError_t {
+      constexpr int PC = decltype(pc)::value, CL = decltype(cl)::value;
+      if (A.K == 1) return go(k_fine<OutT, NW, 1, 0, PC, CL>);
+      if (A.K <= 4) return go(k_fine<OutT, NW, 4, 0, PC, CL>);
+      if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0, PC, CL>);
+      return go(k_fine<OutT, NW, 0, 0, PC, CL>);
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    if (A.persp) return A.clip ? by_flags(I1{}, I1{}) : by_flags(I1{}, I0{});
+    return A.clip ? by_flags(I0{}, I1{}) : by_flags(I0{}, I0{});
   };
   if (nw == 8) return by_k(std::integral_constant<int, 8>{});
   return by_k(std::integral_constant<int, 2>{});
