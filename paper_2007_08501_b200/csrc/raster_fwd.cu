@@ -884,11 +884,12 @@ __device__ __forceinline__ void process_group(const FineArgs<OutT>& A, const War
 // instantiations so the fragment path's code (and register allocation) does not carry them
 // kPC: perspective_correct fixed at compile time (0 / 1) for the fragment instantiations, read from A (2) for the
 // fused consumers (their own instantiations already multiply the kernel count)
-template <typename OutT, int NW, int KMAX, int kMode, int kPC = 2, int kCL = 2>
+// kExactK: K == KMAX (the register path's common case), so every loop over the list has a compile-time trip count
+template <typename OutT, int NW, int KMAX, int kMode, int kPC = 2, int kCL = 2, bool kExactK = false>
 __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int K = A.K;
+  const int K = kExactK ? KMAX : A.K;
   const bool persp = kPC == 2 ? A.persp : kPC == 1;
   // clip_barycentric_coords; the depth-ordered bins and K-th-depth culling are on exactly when it is (make_plan)
   const bool clip = kCL == 2 ? A.clip : kCL == 1;
@@ -1251,6 +1252,11 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
     // fragment payload: one instantiation per (perspective_correct, clip_barycentric_coords)
     auto by_flags = [&](auto pc, auto cl) -> cudaError_t {
       constexpr int PC = decltype(pc)::value, CL = decltype(cl)::value;
+      if constexpr (NW == 8) {  // (the register path always runs 8-warp CTAs)
+        if (A.K == 1) return go(k_fine<OutT, NW, 1, 0, PC, CL, true>);
+        if (A.K == 4) return go(k_fine<OutT, NW, 4, 0, PC, CL, true>);
+        if (A.K == 8) return go(k_fine<OutT, NW, 8, 0, PC, CL, true>);
+      }
       if (A.K == 1) return go(k_fine<OutT, NW, 1, 0, PC, CL>);
       if (A.K <= 4) return go(k_fine<OutT, NW, 4, 0, PC, CL>);
       if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0, PC, CL>);
