@@ -274,10 +274,16 @@ def roofline_of(kt, cfg, steps, N, F, S_):
     peaks, peak_kind = measured_peaks()
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
     step_ms_sum = sum(v[0] for v in shares.values()) / steps
+    issue = ncu_issue(cfg, dom)
     return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(cfg, dom), "kernel": dom,
             "kernel_ms": dom_ms, "kernel_share_of_step": shares[dom][0] / steps / max(step_ms_sum, 1e-9),
-            "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind, "issue": ncu_issue(cfg, dom),
+            "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind, "issue": issue,
+            # the resource that binds: K2 / K3 are fp64 issue/latency bound (exact fp64 selection arithmetic), not
+            # HBM bound — their issue-slot utilisation is the fraction that says how close they run to their limit
+            "binding": ({"resource": "SM issue slots (fp64 dependency latency)", "frac": issue["issue_active_frac"],
+                         "fp64_pipe_frac": issue["fp64_pipe_active_frac"], "source": issue["source"]}
+                        if issue else None),
             "per_kernel_ms_per_step": {k: v[0] / steps for k, v in shares.items()}}
 
 
