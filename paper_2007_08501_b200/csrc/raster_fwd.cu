@@ -620,7 +620,8 @@ __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot,
     PixelFaceResult r;
     // fp64 payload: the identical operation sequence => the bits the candidate test produced; fp32 payload: the
     // same formulas with fast (<= 1 ulp) divisions, rounded once to fp32 (selection is already decided)
-    eval_pixel_face<true, std::is_same<OutT, double>::value>(V2{px, py}, g, A.blur, A.znear, persp, clip, r);
+    // fp64 payload: IEEE divisions (bit-identical to the candidate test); fp32 payload: fdiv_payload (~2^-46)
+    eval_pixel_face<true, std::is_same<OutT, double>::value ? 1 : 2>(V2{px, py}, g, A.blur, A.znear, persp, clip, r);
     A.p2f[slot] = fid;
     A.zbuf[slot] = (OutT)z;
     A.bary[3 * slot + 0] = (OutT)r.bary[0];
