@@ -619,8 +619,7 @@ __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot,
     const FaceGeom g = make_face_geom(v);
     PixelFaceResult r;
     // fp64 payload: the identical operation sequence => the bits the candidate test produced; fp32 payload: the
-    // same formulas with fast (<= 1 ulp) divisions, rounded once to fp32 (selection is already decided)
-    // fp64 payload: IEEE divisions (bit-identical to the candidate test); fp32 payload: fdiv_payload (~2^-46)
+    // same formulas with fdiv_payload divisions (~2^-46 relative), rounded once to fp32 (selection is decided)
     eval_pixel_face<true, std::is_same<OutT, double>::value ? 1 : 2>(V2{px, py}, g, A.blur, A.znear, persp, clip, r);
     A.p2f[slot] = fid;
     A.zbuf[slot] = (OutT)z;
