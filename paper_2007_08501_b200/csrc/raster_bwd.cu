@@ -145,19 +145,19 @@ __device__ __forceinline__ void slot_backward(const BwdArgs<InT>& A, V2 p, int32
 
   // MR:46-69 point_triangle_dist2_backward: nearest edge (first strict min), t and sign frozen
   const double d_out = (double)in.dd;
-  double t0, t1, t2;
-  const double e0 = seg_dist2<false>(p, a, pa, fg.ab, fg.len_ab, t0);
-  const double e1 = seg_dist2<false>(p, b, pb, fg.bc, fg.len_bc, t1);
-  const double e2 = seg_dist2<false>(p, c, pc, fg.ca, fg.len_ca, t2);
+  // the nearest point of each edge (the same expressions seg_dist2 evaluates), carried through the argmin instead
+  // of re-selecting the edge's endpoints afterwards
+  const double t0 = seg_t<false>(dot(pa, fg.ab), fg.len_ab), t1 = seg_t<false>(dot(pb, fg.bc), fg.len_bc),
+               t2 = seg_t<false>(dot(pc, fg.ca), fg.len_ca);
+  const V2 q0 = a + fg.ab * t0, q1 = b + fg.bc * t1, q2 = c + fg.ca * t2;
+  const double e0 = norm2(p - q0), e1 = norm2(p - q1), e2 = norm2(p - q2);
   int be = 0;
   double best = e0, bt = t0;
-  if (e1 < best) { best = e1; bt = t1; be = 1; }
-  if (e2 < best) { best = e2; bt = t2; be = 2; }
+  V2 qq = q0;
+  if (e1 < best) { best = e1; bt = t1; be = 1; qq = q1; }
+  if (e2 < best) { best = e2; bt = t2; be = 2; qq = q2; }
   const bool inside = point_triangle_dist2<false>(p, fg, pa, pb, pc).inside;
   const double sign = inside ? -1.0 : 1.0;
-  const V2 ea = be == 0 ? a : (be == 1 ? b : c);
-  const V2 eb = be == 0 ? b : (be == 1 ? c : a);
-  const V2 qq = ea + (eb - ea) * bt;
   const V2 gg = (qq - p) * (2.0 * sign * d_out);
   const V2 g_first = gg * (1.0 - bt), g_second = gg * bt;
   // grads[be] += g*(1-t); grads[(be+1)%3] += g*t
@@ -364,21 +364,20 @@ __device__ __forceinline__ void silhouette_envelope(const double* v, V2 p, doubl
                                                     double& sign) {
   const FaceGeom fg = make_face_geom(v);
   const V2 pa = p - fg.a, pb = p - fg.b, pc = p - fg.c;
-  double t0, t1, t2;
-  const double e0 = seg_dist2<false>(p, fg.a, pa, fg.ab, fg.len_ab, t0);
-  const double e1 = seg_dist2<false>(p, fg.b, pb, fg.bc, fg.len_bc, t1);
-  const double e2 = seg_dist2<false>(p, fg.c, pc, fg.ca, fg.len_ca, t2);
+  // as slot_backward: each edge's nearest point carried through the argmin
+  const double t0 = seg_t<false>(dot(pa, fg.ab), fg.len_ab), t1 = seg_t<false>(dot(pb, fg.bc), fg.len_bc),
+               t2 = seg_t<false>(dot(pc, fg.ca), fg.len_ca);
+  const V2 q0 = fg.a + fg.ab * t0, q1 = fg.b + fg.bc * t1, q2 = fg.c + fg.ca * t2;
+  const double e0 = norm2(p - q0), e1 = norm2(p - q1), e2 = norm2(p - q2);
   be = 0;
   double best = e0;
   bt = t0;
-  if (e1 < best) { best = e1; bt = t1; be = 1; }
-  if (e2 < best) { best = e2; bt = t2; be = 2; }
+  qq = q0;
+  if (e1 < best) { best = e1; bt = t1; be = 1; qq = q1; }
+  if (e2 < best) { best = e2; bt = t2; be = 2; qq = q2; }
   const bool inside = point_triangle_dist2<false>(p, fg, pa, pb, pc).inside;
   sign = inside ? -1.0 : 1.0;
   dist = inside ? -best : best;
-  const V2 ea = be == 0 ? fg.a : (be == 1 ? fg.b : fg.c);
-  const V2 eb = be == 0 ? fg.b : (be == 1 ? fg.c : fg.a);
-  qq = ea + (eb - ea) * bt;
 }
 
 constexpr int kSilThreads = 128;
