@@ -48,6 +48,7 @@ def main():
     data = [dict(zip(hdr, r)) for r in rows[hi + 1:] if len(r) == len(hdr)]
     base = int(data[0]["Address"], 16)
     samp, inst = collections.Counter(), collections.Counter()
+    fp64 = collections.Counter()  # per (region, opcode): fp64-pipe instructions (D* ops, conversions to/from F64)
     for d in data:
         chain = chains.get(int(d["Address"], 16) - base, [])
         own = [l for f, l in chain if f == srcname]
@@ -58,9 +59,19 @@ def main():
             region = "?"
         samp[region] += float(d["Warp Stall Sampling (All Samples)"] or 0)
         inst[region] += float(d["Instructions Executed"] or 0)
+        op = d["Source"].split()[0] if d["Source"].split() else ""
+        if op.startswith("@"):
+            op = d["Source"].split()[1]
+        if re.match(r"D(ADD|MUL|FMA|SETP|MNMX|MMA)", op) or ("F64" in op and op.split(".")[0] in ("F2F", "I2F", "F2I")):
+            fp64[(region, op.split(".")[0])] += float(d["Instructions Executed"] or 0)
     ts, ti = sum(samp.values()), sum(inst.values())
     for k, v in samp.most_common():
         print(f"{v / ts * 100:5.1f}% samples {inst[k] / ti * 100:5.1f}% inst  {k}")
+    tf = sum(fp64.values())
+    if tf:
+        print(f"fp64-pipe instructions: {tf:.3e} ({tf / ti * 100:.1f}% of all)")
+        for (region, op), v in fp64.most_common(25):
+            print(f"  {v / tf * 100:5.1f}%  {region:24s} {op}")
 
 
 if __name__ == "__main__":
