@@ -15,7 +15,8 @@ sys.path.insert(0, ROOT)
 from bench import config_settings  # noqa: E402
 
 NAMES = ["list entries scanned", "faces staged", "pairs enumerated", "pairs evaluated (not z-culled)",
-         "pairs passing", "micro-tiles", "early exits", "pair steps"]
+         "pairs passing", "micro-tiles", "(unused)", "pair steps", "candidates merged (register path)",
+         "merge calls (warps)", "merged below the list tail", "overflow merges (warps)"]
 
 
 def main():
@@ -30,7 +31,7 @@ def main():
         first = torch.as_tensor(m.mesh_to_face_first_idx(), device=dev)
         num = torch.as_tensor(m.num_faces_per_mesh(), device=dev)
         rs = config_settings(cfg)
-        out = (C.c_ulonglong * 8)()
+        out = (C.c_ulonglong * 12)()
         fn(out, 1)
         p2f = rasterize_meshes(fv, first, num, rs)[0]
         torch.cuda.synchronize()
