@@ -26,7 +26,7 @@
 #endif
 #if DR_STATS
 // debug build only (tools/fine_stats.py): work counters of K2
-__device__ unsigned long long g_stats[8];
+__device__ unsigned long long g_stats[12];
 #define STAT_ADD(i, v) do { const unsigned long long sv_ = (unsigned long long)(v); if ((threadIdx.x & 31) == 0) atomicAdd(&g_stats[i], sv_); } while (0)
 #else
 #define STAT_ADD(i, v) do { } while (0)
@@ -707,6 +707,11 @@ __device__ __forceinline__ void list_insert(const WarpSmem& ws, int K, int p, do
 template <int KMAX>
 __device__ __forceinline__ void merge_buffers(const WarpSmem& ws, int K, int lane) {
   const int n = ws.bcnt[lane];
+#if DR_STATS
+  STAT_ADD(8, __reduce_add_sync(0xffffffffu, (unsigned)n));
+  STAT_ADD(9, 1);
+  unsigned below = 0;
+#endif
   if (n > 0) {
     if constexpr (KMAX == 0) {
       for (int c = 0; c < n; ++c) list_insert<true>(ws, K, lane, ws.bz[ws.bi(c, lane)], ws.bid[ws.bi(c, lane)]);
@@ -722,6 +727,9 @@ __device__ __forceinline__ void merge_buffers(const WarpSmem& ws, int K, int lan
         const double zc = ws.bz[ws.bi(c, lane)];
         const int32_t ic = ws.bid[ws.bi(c, lane)];
         if (!cand_less(zc, ic, z[KMAX - 1], id[KMAX - 1])) continue;  // not below the list tail
+#if DR_STATS
+        ++below;
+#endif
 #pragma unroll
         for (int s = KMAX - 1; s >= 0; --s) {
           const int sp = s > 0 ? s - 1 : 0;
@@ -746,6 +754,9 @@ __device__ __forceinline__ void merge_buffers(const WarpSmem& ws, int K, int lan
     }
     ws.bcnt[lane] = 0;
   }
+#if DR_STATS
+  STAT_ADD(10, __reduce_add_sync(0xffffffffu, below));
+#endif
 }
 
 // Append a passing candidate to its pixel's buffer (merging every buffer first if one would overflow).
@@ -769,6 +780,7 @@ __device__ __forceinline__ void insert_candidate(const FineArgs<OutT>& A, const 
     todo = todo && !ok;
     if (__any_sync(0xffffffffu, todo)) {  // a buffer is full: merge them all, then retry the rest
       __syncwarp();
+      STAT_ADD(11, 1);
       if (todo && pos == kBufT<KMAX>) ws.bcnt[p] = kBufT<KMAX>;  // undo the failed increments (one writer)
       __syncwarp();
       merge_buffers<KMAX>(ws, K, lane);
@@ -1281,9 +1293,9 @@ cudaError_t launch_fine(const FineArgs<double>& A, int nwarps, cudaStream_t st) 
 #if DR_STATS
 extern "C" int dr_debug_stats(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_stats, sizeof(unsigned long long) * 8);
+  cudaMemcpyFromSymbol(out, g_stats, sizeof(unsigned long long) * 12);
   if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[12] = {};
     cudaMemcpyToSymbol(g_stats, z, sizeof(z));
   }
   return 0;
