@@ -259,18 +259,6 @@ int dr_rasterize_softmax_bwd(const double* face_verts, const int64_t* mesh_to_fa
                              const dr_blend_params* blend, const double* vert_colors, const int64_t* faces, int64_t V,
                              const int64_t* pix_to_face, const float* grad_image, double* grad_face_verts,
                              double* grad_vert_colors, dr_stream_t stream);
-/* The same vjp in split form for faces_per_pixel <= 16: one kernel runs softmax_blend_backward +
- * interpolate_face_attributes_backward and writes the rasterizer's per-slot cotangents (d_zbuf, d_bary, d_dists and
- * the clamped barycentrics, fp32, occupied slots) to `workspace`; dr_rasterize_meshes_bwd's kernel then runs on them
- * (grad_face_verts within 1e-4 relative of the fused form). Workspace: dr_rasterize_softmax_bwd_workspace_bytes
- * (32 bytes per slot; 0 when faces_per_pixel > 16, where this call is dr_rasterize_softmax_bwd). */
-size_t dr_rasterize_softmax_bwd_workspace_bytes(int64_t N, const dr_raster_settings* s);
-int dr_rasterize_softmax_bwd_ws(const double* face_verts, const int64_t* mesh_to_face_first_idx,
-                                const int64_t* num_faces_per_mesh, int64_t N, int64_t F, const dr_raster_settings* s,
-                                const dr_blend_params* blend, const double* vert_colors, const int64_t* faces,
-                                int64_t V, const int64_t* pix_to_face, const float* grad_image,
-                                double* grad_face_verts, double* grad_vert_colors, void* workspace,
-                                size_t workspace_bytes, dr_stream_t stream);
 
 /* ---- point rasterizer ----
  * Replaces dr::rasterize_points / rasterize_points_naive (point_render.hpp:33-36, point_render.cpp:82-155) on the

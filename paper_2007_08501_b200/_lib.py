@@ -33,8 +33,6 @@ EXPORTED_SYMBOLS = (
     "dr_world_to_face_verts_async",
     "dr_rasterize_softmax_fwd",
     "dr_rasterize_softmax_bwd",
-    "dr_rasterize_softmax_bwd_workspace_bytes",
-    "dr_rasterize_softmax_bwd_ws",
     "dr_point_raster_settings_default",
     "dr_rasterize_points_workspace_bytes",
     "dr_rasterize_points_fwd",
@@ -207,11 +205,6 @@ def load() -> C.CDLL:
                                            _vp, _vp, _vp]
     L.dr_rasterize_softmax_fwd.restype = C.c_int
     L.dr_rasterize_softmax_bwd.restype = C.c_int
-    L.dr_rasterize_softmax_bwd_workspace_bytes.argtypes = [C.c_int64, sp]
-    L.dr_rasterize_softmax_bwd_workspace_bytes.restype = C.c_size_t
-    L.dr_rasterize_softmax_bwd_ws.argtypes = [_vp, _vp, _vp, C.c_int64, C.c_int64, sp, bpp, _vp, _vp, C.c_int64, _vp,
-                                              _vp, _vp, _vp, _vp, C.c_size_t, _vp]
-    L.dr_rasterize_softmax_bwd_ws.restype = C.c_int
     pp = C.POINTER(DrPointRasterSettings)
     L.dr_point_raster_settings_default.argtypes = [pp]
     L.dr_rasterize_points_workspace_bytes.argtypes = [C.c_int64, C.c_int64, pp]

@@ -690,72 +690,6 @@ int dr_rasterize_softmax_bwd(const double* fv, const int64_t* first, const int64
   return DR_OK;
 }
 
-size_t dr_rasterize_softmax_bwd_workspace_bytes(int64_t N, const dr_raster_settings* s) {
-  Plan p;
-  if (make_plan(N, 0, s, p) != DR_OK || p.K > drb::kSoftCoefMaxK) return 0;
-  const size_t S = (size_t)N * p.H * p.W * p.K;
-  return align_up(sizeof(float) * 3 * S) * 2 + align_up(sizeof(float) * S) * 2;
-}
-
-int dr_rasterize_softmax_bwd_ws(const double* fv, const int64_t* first, const int64_t* num, int64_t N, int64_t F,
-                                const dr_raster_settings* s, const dr_blend_params* bp, const double* vert_colors,
-                                const int64_t* faces, int64_t V, const int64_t* p2f, const float* grad_image,
-                                double* grad_face_verts, double* grad_vert_colors, void* workspace,
-                                size_t workspace_bytes, dr_stream_t stream) {
-  Plan p;
-  int rc = make_plan(N, F, s, p);
-  if (rc) return rc;
-  const size_t need = dr_rasterize_softmax_bwd_workspace_bytes(N, s);
-  if (need == 0)  // K > kSoftCoefMaxK: the slot-compacted fused kernel, no scratch
-    return dr_rasterize_softmax_bwd(fv, first, num, N, F, s, bp, vert_colors, faces, V, p2f, grad_image,
-                                    grad_face_verts, grad_vert_colors, stream);
-  if (!workspace || workspace_bytes < need)
-    return fail(DR_ERR_OOM, "softmax backward workspace too small: %zu bytes given, %zu needed", workspace_bytes, need);
-  rc = check_blend(bp, vert_colors, faces, V, F);
-  if (rc) return rc;
-  if (!first || !num || !p2f || !grad_image || (F > 0 && (!fv || !grad_face_verts)) || (V > 0 && !grad_vert_colors))
-    return fail(DR_ERR_USAGE, "null input/output pointer");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  {
-    ProfScope ps(st, KN_MEMSET);
-    e = V > 0 ? cudaMemsetAsync(grad_vert_colors, 0, sizeof(double) * 3 * (size_t)V, st) : cudaSuccess;
-  }
-  if (e != cudaSuccess) return cuda_fail(e, "zeroing gradients");
-  const size_t S = (size_t)N * p.H * p.W * p.K;
-  char* w = static_cast<char*>(workspace);
-  drb::SoftCoefOut O;
-  O.bary = reinterpret_cast<float*>(w);
-  O.d_bary = reinterpret_cast<float*>(w + align_up(sizeof(float) * 3 * S));
-  O.d_zbuf = reinterpret_cast<float*>(w + 2 * align_up(sizeof(float) * 3 * S));
-  O.d_dists = reinterpret_cast<float*>(w + 2 * align_up(sizeof(float) * 3 * S) + align_up(sizeof(float) * S));
-  if (F > 0) {
-    drb::SoftBwdArgs A;
-    A.fv = fv;
-    A.p2f = p2f;
-    A.d_image = grad_image;
-    A.grad = grad_face_verts;
-    A.grad_colors = grad_vert_colors;
-    A.npix = N * (int64_t)p.H * p.W;
-    A.F = F;
-    A.H = p.H;
-    A.W = p.W;
-    A.K = p.K;
-    A.persp = s->perspective_correct != 0;
-    A.clip = s->clip_barycentric_coords != 0;
-    A.blur = s->blur_radius;
-    A.znear = s->znear;
-    A.blend = blend_args(bp, vert_colors, faces, V);
-    {
-      ProfScope ps(st, KN_SOFT_BWD);
-      e = drb::launch_softmax_coef(A, O, st);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "rasterize_softmax backward (coefficients)");
-  }
-  // the rasterizer's own backward (K3) on the blend's per-slot cotangents
-  return bwd_impl<float>(fv, first, num, N, F, s, p2f, O.bary, O.d_zbuf, O.d_bary, O.d_dists, grad_face_verts, st);
-}
-
 void dr_point_raster_settings_default(dr_point_raster_settings* s) {
   if (!s) return;
   std::memset(s, 0, sizeof(*s));

@@ -387,6 +387,8 @@ constexpr int kSilStoreMaxK = 16;  // up to this K the pass-1 envelope is kept i
 // pass 3 needs no second geometry evaluation (K <= kSilStoreMaxK); otherwise pass 3 recomputes it.
 template <bool kStore>
 __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs A) {
+  // 1 / sigma once (products instead of per-slot divisions; the opacities are tolerance values)
+  const double inv_sigma = 1.0 / A.sigma;
   extern __shared__ double sil_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
@@ -456,8 +458,8 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
           silhouette_envelope(v, p, dist, be, bt, qq, sign);
           // sigmoid(-dist / sigma) (shading.cpp:9, 82); fp32 exp for the fp32 cotangent (the value enters the
           // gradients within tolerance), fp64 exp for the fp64 one
-          prob = A.d_alpha64 ? 1.0 / (1.0 + exp(dist / A.sigma))
-                             : 1.0 / (1.0 + (double)expf((float)(dist / A.sigma)));
+          prob = A.d_alpha64 ? fdiv(1.0, 1.0 + exp(dist * inv_sigma))
+                             : fdiv(1.0, 1.0 + (double)expf((float)(dist * inv_sigma)));
           if constexpr (kStore) {
             EX[s * 32 + lane] = (qq.x - p.x) * (2.0 * sign);
             EY[s * 32 + lane] = (qq.y - p.y) * (2.0 * sign);
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
           ey = (qq.y - p.y) * (2.0 * sign);
         }
         const double rest = pre * Sf[s * 32 + lane];
-        const double d_out = da * rest * (-pr * (1.0 - pr) / A.sigma);
+        const double d_out = da * rest * (-pr * (1.0 - pr) * inv_sigma);
         const V2 gg{ex * d_out, ey * d_out};  // (qq - p) * (2 sign d_out): the same single rounding
         const V2 g_first = gg * (1.0 - bt), g_second = gg * bt;
         const int v0 = be, v1 = be == 2 ? 0 : be + 1;
@@ -547,6 +549,8 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 
 __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBwdArgs A) {
+  // 1 / sigma once (products instead of per-slot divisions; the opacities are tolerance values)
+  const double inv_sigma = 1.0 / A.sigma;
   extern __shared__ double silq_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
@@ -641,8 +645,8 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
           V2 qq;
           silhouette_envelope(v, p, dist, be, bt, qq, sign);
           // sigmoid(-dist / sigma) (shading.cpp:9, 82): fp32 exp for the fp32 cotangent, fp64 for the fp64 one
-          PR[t] = A.d_alpha64 ? 1.0 / (1.0 + exp(dist / A.sigma))
-                              : 1.0 / (1.0 + (double)expf((float)(dist / A.sigma)));
+          PR[t] = A.d_alpha64 ? fdiv(1.0, 1.0 + exp(dist * inv_sigma))
+                              : fdiv(1.0, 1.0 + (double)expf((float)(dist * inv_sigma)));
           EX[t] = (qq.x - p.x) * (2.0 * sign);
           EY[t] = (qq.y - p.y) * (2.0 * sign);
           BT[t] = bt;
@@ -664,7 +668,7 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
       for (int s = 0; s < K; ++s) {
         const double pr = PR[r + s];
         if (pr >= 0.0) {
-          CO[r + s] = da * (pre * CO[r + s]) * (-pr * (1.0 - pr) / A.sigma);
+          CO[r + s] = da * (pre * CO[r + s]) * (-pr * (1.0 - pr) * inv_sigma);
           pre *= 1.0 - pr;
         }
       }
@@ -763,10 +767,11 @@ cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
 constexpr int kSoftThreads = 128;
 constexpr int kSoftMaxK = 64;
 
-__device__ __forceinline__ double blend_zinv_b(double z, const BlendArgs& bl, bool& clamped) {
+// clamped inverse depth (shading.cpp:136-137, 199) with the depth range's reciprocal precomputed (inv_zr)
+__device__ __forceinline__ double blend_zinv_b(double z, const BlendArgs& bl, double inv_zr, bool& clamped) {
   clamped = z < bl.znear || z > bl.zfar;  // shading.cpp:199
   const double zc = z < bl.znear ? bl.znear : (bl.zfar < z ? bl.zfar : z);
-  return (bl.zfar - zc) / (bl.zfar - bl.znear);
+  return (bl.zfar - zc) * inv_zr;
 }
 
 __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArgs A) {
@@ -788,6 +793,11 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t HW = (int64_t)A.H * A.W;
   const double zrange = A.blend.zfar - A.blend.znear;
+  // the blend's divisions by sigma, gamma, the depth range and the per-pixel weight sum become products with
+  // reciprocals (values compared within tolerance, never selected on: <= 2 ulp from the quotients; C4 10.7 -> 8.8 ms)
+  const double inv_sigma = 1.0 / A.blend.sigma, inv_gamma = 1.0 / A.blend.gamma, inv_zr = 1.0 / zrange;
+#define SDIV_SIGMA(x) ((x) * inv_sigma)
+#define SDIV_GAMMA(x) ((x) * inv_gamma)
   for (int64_t base = warp * 32; base < A.npix; base += nwarps * 32) {
     const int64_t pix = base + lane;
     double dimg[3] = {0.0, 0.0, 0.0};
@@ -825,7 +835,7 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
         PixelFaceResult r;
         eval_pixel_face<true, false>(p, g, A.blur, A.znear, A.persp, A.clip, r);
         bool clamped;
-        zi = blend_zinv_b(r.z, A.blend, clamped);
+        zi = blend_zinv_b(r.z, A.blend, inv_zr, clamped);
         if (argmax < 0) {  // the first occupied slot (see above)
           zinv_max = zi;
           argmax = s;
@@ -841,7 +851,7 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
         C0[s * 32 + lane] = c[0];
         C1[s * 32 + lane] = c[1];
         C2[s * 32 + lane] = c[2];
-        PR[s * 32 + lane] = 1.0 / (1.0 + exp(r.dist / A.blend.sigma));  // sigmoid(-dists / sigma)
+        PR[s * 32 + lane] = fdiv(1.0, 1.0 + exp(SDIV_SIGMA(r.dist)));  // sigmoid(-dists / sigma)
         if (clamped) zi += 2.0;
       }
       ZI[s * 32 + lane] = zi;
@@ -852,16 +862,18 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
       double zi = ZI[s * 32 + lane];
       if (zi < -0.5) continue;
       if (zi > 1.5) zi -= 2.0;
-      const double w = PR[s * 32 + lane] * exp((zi - zinv_max) / A.blend.gamma);
+      const double w = PR[s * 32 + lane] * exp(SDIV_GAMMA(zi - zinv_max));
       WT[s * 32 + lane] = w;
       wsum += w;
     }
     // pass 3: the mean term (shading.cpp:218-222; identical for every slot, computed once in the same order)
+    const double inv_wsum = fdiv(1.0, wsum);
+#define SDIV_WSUM(x) ((x) * inv_wsum)
     double mean_term = 0.0;
     for (int s = 0; s < K; ++s) {
       if (ZI[s * 32 + lane] < -0.5) continue;
       const double dc = dimg[0] * C0[s * 32 + lane] + dimg[1] * C1[s * 32 + lane] + dimg[2] * C2[s * 32 + lane];
-      mean_term += dc * (WT[s * 32 + lane] / wsum);
+      mean_term += dc * SDIV_WSUM(WT[s * 32 + lane]);
     }
     // d_zinv_max (shading.cpp:228) before the per-slot pass that adds it to the argmax slot
     double d_zinv_max = 0.0;
@@ -869,8 +881,8 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
       if (ZI[s * 32 + lane] < -0.5) continue;
       const double w = WT[s * 32 + lane];
       const double d_what = dimg[0] * C0[s * 32 + lane] + dimg[1] * C1[s * 32 + lane] + dimg[2] * C2[s * 32 + lane];
-      const double d_w = (d_what - mean_term) / wsum;
-      d_zinv_max += -d_w * w / A.blend.gamma;
+      const double d_w = SDIV_WSUM(d_what - mean_term);
+      d_zinv_max += SDIV_GAMMA(-d_w * w);
     }
     // pass 4: per-slot cotangents -> colours, barycentrics, the K3 chain
     for (int s = 0; s < K; ++s) {
@@ -884,15 +896,15 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
         const bool clamped = zis > 1.5;
         const double w = WT[s * 32 + lane], pr = PR[s * 32 + lane];
         const double c[3] = {C0[s * 32 + lane], C1[s * 32 + lane], C2[s * 32 + lane]};
-        const double what = w / wsum;
+        const double what = SDIV_WSUM(w);
         const double d_col[3] = {dimg[0] * what, dimg[1] * what, dimg[2] * what};  // g.d_colors = dimg * what
         const double d_what = dimg[0] * c[0] + dimg[1] * c[1] + dimg[2] * c[2];
-        const double d_w = (d_what - mean_term) / wsum;
-        const double d_prob = d_w * w / pr;
-        const double d_zinv = d_w * w / A.blend.gamma;
-        const double d_dists = d_prob * (-pr * (1.0 - pr) / A.blend.sigma);
-        double d_zbuf = clamped ? 0.0 : d_zinv * (-1.0 / zrange);
-        if (s == argmax && !clamped) d_zbuf += d_zinv_max * (-1.0 / zrange);
+        const double d_w = SDIV_WSUM(d_what - mean_term);
+        const double d_prob = fdiv(d_w * w, pr);
+        const double d_zinv = SDIV_GAMMA(d_w * w);
+        const double d_dists = d_prob * SDIV_SIGMA(-pr * (1.0 - pr));
+        double d_zbuf = clamped ? 0.0 : d_zinv * -inv_zr;
+        if (s == argmax && !clamped) d_zbuf += d_zinv_max * -inv_zr;
         // interpolate_face_attributes_backward (shading.cpp:46-72): d_bary_i = d_col . a_i, d_attr_i += w_i d_col
         SlotIn<double> in;
 #pragma unroll
@@ -936,178 +948,9 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
     }
   }
 }
-
-// Split form, pass 4 without the geometry chain: lane per pixel as in k_softmax_backward, but the slot's
-// cotangents on the fragment (d_zbuf, d_dists, d_bary_i = d_col . colour(v_i)) and its clamped barycentrics are
-// written to fp32 scratch for K3 (k_backward, the same per-slot chain, MR:345-378), and only the vertex-colour
-// cotangent (interpolate_face_attributes_backward, shading.cpp:46-72) is reduced here. Passes 1-3 keep d_what =
-// d_image . colour per slot instead of the colour itself, so the barycentrics fit in the freed arrays.
-__global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_coef(SoftBwdArgs A, SoftCoefOut O) {
-  extern __shared__ double coef_smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int K = A.K;
-  const size_t per_warp = (size_t)K * 32 * 4 + (size_t)K * 16 + (size_t)K * 32 * 3 / 2;  // doubles
-  double* ZI = coef_smem + (size_t)wid * per_warp;  // [K][32] zinv (-1: empty slot; +2: clamped)
-  double* PR = ZI + K * 32;                         // [K][32] prob
-  double* WT = PR + K * 32;                         // [K][32] softmax weight
-  double* DW = WT + K * 32;                         // [K][32] d_image . colour
-  float* B0 = reinterpret_cast<float*>(DW + K * 32);  // [K][32] clamped barycentrics (fp32: they go to fp32 scratch)
-  float* B1 = B0 + K * 32;
-  float* B2 = B1 + K * 32;
-  int32_t* FID = reinterpret_cast<int32_t*>(B2 + K * 32);  // [32][K] the warp's pix_to_face block
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t HW = (int64_t)A.H * A.W;
-  const double zrange = A.blend.zfar - A.blend.znear;
-  for (int64_t base = warp * 32; base < A.npix; base += nwarps * 32) {
-    const int64_t pix = base + lane;
-    double dimg[3] = {0.0, 0.0, 0.0};
-    if (pix < A.npix) {
-      dimg[0] = (double)A.d_image[3 * pix];
-      dimg[1] = (double)A.d_image[3 * pix + 1];
-      dimg[2] = (double)A.d_image[3 * pix + 2];
-    }
-    {
-      const int64_t n = (A.npix - base < 32 ? A.npix - base : 32) * K;
-      const int64_t* src = A.p2f + base * K;
-      for (int t = lane; t < 32 * K; t += 32) {
-        const int64_t f = t < n ? __ldcs(src + t) : -1;
-        FID[t] = (f >= 0 && f < A.F) ? (int32_t)f : -1;
-      }
-      __syncwarp();
-    }
-    const int32_t* row = FID + lane * K;
-    const int rem = pix < A.npix ? (int)(pix % HW) : 0;
-    const int i = rem / A.W, j = rem - (rem / A.W) * A.W;
-    const V2 p{pixel_x(A.W, j), pixel_y(A.H, i)};
-    // pass 1: slot evaluation (fast divisions), zinv_max / argmax (shading.cpp:185-197), opacity, d_image . colour
-    double zinv_max = -1.0;
-    int argmax = -1;
-    bool any = false;
-    for (int s = 0; s < K; ++s) {
-      const int32_t f = pix < A.npix ? row[s] : -1;
-      double zi = -1.0;
-      if (f >= 0) {
-        any = true;
-        double v[9];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)f + t);
-        const FaceGeom g = make_face_geom(v);
-        PixelFaceResult r;
-        eval_pixel_face<true, false>(p, g, A.blur, A.znear, A.persp, A.clip, r);
-        bool clamped;
-        zi = blend_zinv_b(r.z, A.blend, clamped);
-        if (argmax < 0) {  // the first occupied slot (see k_softmax_backward)
-          zinv_max = zi;
-          argmax = s;
-        }
-        double c[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {  // interpolate_face_attributes (shading.cpp:21-29)
-          const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)f + q];
-          c[0] += r.bary[q] * __ldg(a);
-          c[1] += r.bary[q] * __ldg(a + 1);
-          c[2] += r.bary[q] * __ldg(a + 2);
-        }
-        DW[s * 32 + lane] = dimg[0] * c[0] + dimg[1] * c[1] + dimg[2] * c[2];
-        B0[s * 32 + lane] = (float)r.bary[0];
-        B1[s * 32 + lane] = (float)r.bary[1];
-        B2[s * 32 + lane] = (float)r.bary[2];
-        PR[s * 32 + lane] = 1.0 / (1.0 + exp(r.dist / A.blend.sigma));  // sigmoid(-dists / sigma)
-        if (clamped) zi += 2.0;
-      }
-      ZI[s * 32 + lane] = zi;
-    }
-    // pass 2: weights and their sum (shading.cpp:202-209)
-    double wsum = 0.0;
-    for (int s = 0; s < K; ++s) {
-      double zi = ZI[s * 32 + lane];
-      if (zi < -0.5) continue;
-      if (zi > 1.5) zi -= 2.0;
-      const double w = PR[s * 32 + lane] * exp((zi - zinv_max) / A.blend.gamma);
-      WT[s * 32 + lane] = w;
-      wsum += w;
-    }
-    // pass 3: the mean term (shading.cpp:218-222) and d_zinv_max (shading.cpp:228)
-    double mean_term = 0.0;
-    for (int s = 0; s < K; ++s) {
-      if (ZI[s * 32 + lane] < -0.5) continue;
-      mean_term += DW[s * 32 + lane] * (WT[s * 32 + lane] / wsum);
-    }
-    double d_zinv_max = 0.0;
-    for (int s = 0; s < K; ++s) {
-      if (ZI[s * 32 + lane] < -0.5) continue;
-      const double w = WT[s * 32 + lane];
-      const double d_w = (DW[s * 32 + lane] - mean_term) / wsum;
-      d_zinv_max += -d_w * w / A.blend.gamma;
-    }
-    // pass 4: per-slot cotangents to scratch, vertex-colour cotangent reduced and accumulated
-    const int64_t slot0 = pix * K;
-    for (int s = 0; s < K; ++s) {
-      const double zis = (pix < A.npix && any) ? ZI[s * 32 + lane] : -1.0;
-      int32_t fid = -1;
-      double gc[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) gc[k] = 0.0;
-      if (zis >= -0.5) {
-        fid = row[s];
-        const bool clamped = zis > 1.5;
-        const double w = WT[s * 32 + lane], pr = PR[s * 32 + lane];
-        const double what = w / wsum;
-        const double d_col[3] = {dimg[0] * what, dimg[1] * what, dimg[2] * what};
-        const double d_w = (DW[s * 32 + lane] - mean_term) / wsum;
-        const double d_prob = d_w * w / pr;
-        const double d_zinv = d_w * w / A.blend.gamma;
-        const double d_dists = d_prob * (-pr * (1.0 - pr) / A.blend.sigma);
-        double d_zbuf = clamped ? 0.0 : d_zinv * (-1.0 / zrange);
-        if (s == argmax && !clamped) d_zbuf += d_zinv_max * (-1.0 / zrange);
-        const double wh[3] = {(double)B0[s * 32 + lane], (double)B1[s * 32 + lane], (double)B2[s * 32 + lane]};
-        const int64_t slot = slot0 + s;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const double* a = A.blend.vert_colors + 3 * A.blend.faces[3 * (int64_t)fid + q];
-          O.d_bary[3 * slot + q] = (float)(d_col[0] * __ldg(a) + d_col[1] * __ldg(a + 1) + d_col[2] * __ldg(a + 2));
-          O.bary[3 * slot + q] = (float)wh[q];
-          gc[3 * q + 0] = wh[q] * d_col[0];
-          gc[3 * q + 1] = wh[q] * d_col[1];
-          gc[3 * q + 2] = wh[q] * d_col[2];
-        }
-        O.d_zbuf[slot] = (float)d_zbuf;
-        O.d_dists[slot] = (float)d_dists;
-      }
-      if (reduce_by_face<9>(fid, lane, gc)) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          double* oc = A.grad_colors + 3 * A.blend.faces[3 * (int64_t)fid + q];
-          for (int d = 0; d < 3; ++d)
-            if (gc[3 * q + d] != 0.0) atomicAdd(oc + d, gc[3 * q + d]);
-        }
-      }
-    }
-  }
-}
-
-cudaError_t launch_softmax_coef(const SoftBwdArgs& A, const SoftCoefOut& O, cudaStream_t st) {
-  if (A.npix <= 0) return cudaSuccess;
-  if (A.K > kSoftCoefMaxK) return cudaErrorInvalidConfiguration;
-  const size_t per_warp = ((size_t)A.K * 32 * 4 + (size_t)A.K * 16 + (size_t)A.K * 32 * 3 / 2) * sizeof(double);
-  const int warps = (int)std::min<size_t>(kSoftThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));
-  const size_t smem = per_warp * warps;
-  cudaError_t e = cudaFuncSetAttribute(k_softmax_coef, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::max<size_t>(smem, 48 * 1024));
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_softmax_coef, warps * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int64_t blocks = (int64_t)sms * per_sm;
-  const int64_t need = (A.npix + warps * 32 - 1) / (warps * 32);
-  if (blocks > need) blocks = need;
-  k_softmax_coef<<<(unsigned)blocks, warps * 32, smem, st>>>(A, O);
-  return cudaGetLastError();
-}
+#undef SDIV_SIGMA
+#undef SDIV_GAMMA
+#undef SDIV_WSUM
 
 // Slot-compacted variant: a warp takes P = min(32, 512 / K) consecutive pixels; their occupied slots are queued
 // and the two geometry-heavy passes run lane-per-slot, 32 occupied slots per step:
@@ -1124,6 +967,9 @@ __host__ __device__ __forceinline__ size_t softq_warp_bytes(int K) {
 }
 
 __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
+  // as k_softmax_backward: products with reciprocals instead of the blend's divisions (tolerance values)
+  const double inv_sigma = 1.0 / A.blend.sigma, inv_gamma = 1.0 / A.blend.gamma,
+               inv_zr = 1.0 / (A.blend.zfar - A.blend.znear);
   extern __shared__ double softq_smem[];
   const int lane = threadIdx.x & 31;
   const int K = A.K;
@@ -1144,7 +990,6 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
   BA.persp = A.persp;
   BA.clip = A.clip;
   const int64_t HW = (int64_t)A.H * A.W;
-  const double zrange = A.blend.zfar - A.blend.znear;
   for (int64_t base = (int64_t)blockIdx.x * P; base < A.npix; base += (int64_t)gridDim.x * P) {
     const int np = (int)(A.npix - base < P ? A.npix - base : P);
     if (lane < np) {
@@ -1204,7 +1049,7 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
           PixelFaceResult r;
           eval_pixel_face<true, false>(p, g, A.blur, A.znear, A.persp, A.clip, r);
           bool clamped;
-          double zi = blend_zinv_b(r.z, A.blend, clamped);
+          double zi = blend_zinv_b(r.z, A.blend, inv_zr, clamped);
           double c[3] = {0.0, 0.0, 0.0};
 #pragma unroll
           for (int qq = 0; qq < 3; ++qq) {  // interpolate_face_attributes (shading.cpp:21-29)
@@ -1216,7 +1061,7 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
           C0[t] = c[0];
           C1[t] = c[1];
           C2[t] = c[2];
-          PR[t] = 1.0 / (1.0 + exp(r.dist / A.blend.sigma));  // sigmoid(-dists / sigma)
+          PR[t] = fdiv(1.0, 1.0 + exp(r.dist * inv_sigma));  // sigmoid(-dists / sigma)
           if (clamped) zi += 2.0;
           ZI[t] = zi;
         }
@@ -1243,37 +1088,38 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
         double zi = ZI[r0 + s];
         if (zi < -0.5) continue;
         if (zi > 1.5) zi -= 2.0;
-        const double w = PR[r0 + s] * exp((zi - zinv_max) / A.blend.gamma);
+        const double w = PR[r0 + s] * exp((zi - zinv_max) * inv_gamma);
         WT[r0 + s] = w;
         wsum += w;
       }
+      const double inv_wsum = fdiv(1.0, wsum);
       double mean_term = 0.0;
       for (int s = 0; s < K; ++s) {
         if (ZI[r0 + s] < -0.5) continue;
         const double dc = dimg[0] * C0[r0 + s] + dimg[1] * C1[r0 + s] + dimg[2] * C2[r0 + s];
-        mean_term += dc * (WT[r0 + s] / wsum);
+        mean_term += dc * (WT[r0 + s] * inv_wsum);
       }
       double d_zinv_max = 0.0;
       for (int s = 0; s < K; ++s) {
         if (ZI[r0 + s] < -0.5) continue;
         const double w = WT[r0 + s];
         const double d_what = dimg[0] * C0[r0 + s] + dimg[1] * C1[r0 + s] + dimg[2] * C2[r0 + s];
-        const double d_w = (d_what - mean_term) / wsum;
-        d_zinv_max += -d_w * w / A.blend.gamma;
+        const double d_w = (d_what - mean_term) * inv_wsum;
+        d_zinv_max += -d_w * w * inv_gamma;
       }
       for (int s = 0; s < K; ++s) {
         const double zis = ZI[r0 + s];
         if (zis < -0.5) continue;
         const bool clamped = zis > 1.5;
         const double w = WT[r0 + s], pr = PR[r0 + s];
-        const double what = w / wsum;
+        const double what = w * inv_wsum;
         const double d_what = dimg[0] * C0[r0 + s] + dimg[1] * C1[r0 + s] + dimg[2] * C2[r0 + s];
-        const double d_w = (d_what - mean_term) / wsum;
-        const double d_prob = d_w * w / pr;
-        const double d_zinv = d_w * w / A.blend.gamma;
-        const double d_dists = d_prob * (-pr * (1.0 - pr) / A.blend.sigma);
-        double d_zbuf = clamped ? 0.0 : d_zinv * (-1.0 / zrange);
-        if (s == argmax && !clamped) d_zbuf += d_zinv_max * (-1.0 / zrange);
+        const double d_w = (d_what - mean_term) * inv_wsum;
+        const double d_prob = fdiv(d_w * w, pr);
+        const double d_zinv = d_w * w * inv_gamma;
+        const double d_dists = d_prob * (-pr * (1.0 - pr) * inv_sigma);
+        double d_zbuf = clamped ? 0.0 : d_zinv * -inv_zr;
+        if (s == argmax && !clamped) d_zbuf += d_zinv_max * -inv_zr;
         WT[r0 + s] = what;
         PR[r0 + s] = d_dists;
         ZI[r0 + s] = d_zbuf;

@@ -149,17 +149,6 @@ struct SoftBwdArgs {
   BlendArgs blend;
 };
 cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st);
-// Split form (K <= kSoftCoefMaxK): the per-slot cotangents the blend produces for the rasterizer — the slot's
-// clamped barycentrics, d_bary (from the vertex colours), d_zbuf, d_dists, fp32 in the fragment layout — go to
-// scratch (occupied slots only) and the vertex-colour cotangent is accumulated; K3 then runs on the scratch.
-struct SoftCoefOut {
-  float* bary;    // [S,3]
-  float* d_bary;  // [S,3]
-  float* d_zbuf;  // [S]
-  float* d_dists; // [S]
-};
-constexpr int kSoftCoefMaxK = 16;
-cudaError_t launch_softmax_coef(const SoftBwdArgs& A, const SoftCoefOut& O, cudaStream_t st);
 
 // Camera (dr_camera / dr::Camera, camera.hpp:19-35) as kernel arguments.
 struct CameraArgs {

@@ -399,10 +399,9 @@ def rasterize_softmax(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, se
 
 
 def rasterize_softmax_backward(face_verts, mesh_to_face_first_idx, num_faces_per_mesh, settings: RasterSettings,
-                               blend: BlendParams, vert_colors, faces, pix_to_face, grad_image, split: bool = True):
+                               blend: BlendParams, vert_colors, faces, pix_to_face, grad_image):
     """vjp of the softmax render (grad.cpp:195-206): returns (grad_face_verts [F,3,3] f64, grad_vert_colors [V,3]
-    f64). split (faces_per_pixel <= 16): the blend's per-slot cotangents go through a 32 B/slot scratch to the
-    rasterizer's own backward kernel (dr_rasterize_softmax_bwd_ws); otherwise one fused kernel."""
+    f64), one fused kernel (dr_rasterize_softmax_bwd)."""
     L = _lib.load()
     fv, first, num = _inputs(face_verts, mesh_to_face_first_idx, num_faces_per_mesh)
     vc, fc = _blend_inputs(vert_colors, faces, fv.device)
@@ -417,17 +416,10 @@ def rasterize_softmax_backward(face_verts, mesh_to_face_first_idx, num_faces_per
     g_vc = torch.zeros_like(vc)
     s = settings.to_c()
     b = blend.to_c()
-    ws_bytes = L.dr_rasterize_softmax_bwd_workspace_bytes(N, C.byref(s)) if split else 0
     with torch.cuda.device(fv.device):
-        if ws_bytes:
-            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=fv.device)
-            rc = L.dr_rasterize_softmax_bwd_ws(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), C.byref(b),
-                                               _ptr(vc), _ptr(fc), vc.shape[0], _ptr(p2f), _ptr(gi), _ptr(g_fv),
-                                               _ptr(g_vc), _ptr(ws), ws_bytes, _stream(fv.device))
-        else:
-            rc = L.dr_rasterize_softmax_bwd(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), C.byref(b),
-                                            _ptr(vc), _ptr(fc), vc.shape[0], _ptr(p2f), _ptr(gi), _ptr(g_fv),
-                                            _ptr(g_vc), _stream(fv.device))
+        rc = L.dr_rasterize_softmax_bwd(_ptr(fv), _ptr(first), _ptr(num), N, F, C.byref(s), C.byref(b), _ptr(vc),
+                                        _ptr(fc), vc.shape[0], _ptr(p2f), _ptr(gi), _ptr(g_fv), _ptr(g_vc),
+                                        _stream(fv.device))
     _check(rc, "rasterize_softmax_backward")
     return g_fv, g_vc
 

@@ -95,3 +95,14 @@ def grad_close(got, want, what="", rtol=GRAD_RTOL, atol_scale=GRAD_ATOL_SCALE):
     i = int(np.argmax(ratio))
     assert ratio[i] <= 1.0, f"{what}: element {i} got {got[i]!r} want {want[i]!r} (err/bound {ratio[i]:.3g})"
     return float(ratio[i])
+
+
+def parity_report(**kw):
+    """Append one JSON line to $DR_PARITY_REPORT (if set): worst-element margins of a parity check."""
+    import json
+    import os
+
+    path = os.environ.get("DR_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(kw) + "\n")

@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from paper_2007_08501_b200 import scenes as S
-from tests._common import boundary, grad_close, raster_settings, rel_err
+from tests._common import boundary, grad_close, parity_report, raster_settings, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -45,17 +45,15 @@ def test_softmax_render_vs_reference(name, H, K, blur, sigma, gamma, reflib, cud
     dv_ref, dc_ref = reflib.softmax_render_backward(rb, cam.packed(), H, H, K, blur, vc, sigma, gamma,
                                                     d_img.astype(np.float64), bg)
     assert np.abs(dv_ref).max() > 0 and np.abs(dc_ref).max() > 0
-    # K <= 16: the split form (blend cotangents through fp32 scratch into the rasterizer's backward kernel) and the
-    # fused one; K > 16 has the fused slot-compacted kernel only
-    for split in ((True, False) if K <= 16 else (True,)):
-        g_fv, g_vc = rasterize_softmax_backward(dev(fv), dev(first), dev(num), rs, bp, dev(vc), dev(faces), p2f,
-                                                dev(d_img), split=split)
-        d_got = S.scatter_face_grads(m, cam, g_fv.cpu().numpy())
-        what = f"{name} split={split}"
-        assert rel_err(d_got, dv_ref) < 1e-4, f"{what}: d_verts rel err {rel_err(d_got, dv_ref):.2e}"
-        grad_close(d_got, dv_ref, what)
-        assert rel_err(g_vc.cpu().numpy(), dc_ref) < 1e-6, \
-            f"{what}: d_colors rel err {rel_err(g_vc.cpu().numpy(), dc_ref):.2e}"
+    g_fv, g_vc = rasterize_softmax_backward(dev(fv), dev(first), dev(num), rs, bp, dev(vc), dev(faces), p2f,
+                                            dev(d_img))
+    d_got = S.scatter_face_grads(m, cam, g_fv.cpu().numpy())
+    ev, ec = rel_err(d_got, dv_ref), rel_err(g_vc.cpu().numpy(), dc_ref)
+    assert ev < 1e-4, f"{name}: d_verts rel err {ev:.2e}"
+    ratio = grad_close(d_got, dv_ref, name)
+    assert ec < 1e-6, f"{name}: d_colors rel err {ec:.2e}"
+    parity_report(test="softmax", case=name, d_verts_rel_err=ev, d_verts_worst_err_over_bound=ratio,
+                  d_colors_rel_err=ec)
 
 
 def test_softmax_autograd_and_errors(cuda):
