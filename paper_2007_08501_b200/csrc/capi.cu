@@ -611,6 +611,9 @@ drb::BlendArgs blend_args(const dr_blend_params* bp, const double* vert_colors, 
   for (int c = 0; c < 3; ++c) b.background[c] = bp->background[c];
   b.znear = bp->znear;
   b.zfar = bp->zfar;
+  b.inv_sigma = 1.0 / b.sigma;
+  b.inv_gamma = 1.0 / b.gamma;
+  b.inv_zr = 1.0 / (b.zfar - b.znear);
   return b;
 }
 

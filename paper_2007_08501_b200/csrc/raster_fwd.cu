@@ -639,18 +639,18 @@ __device__ __forceinline__ void emit_slot(const FineArgs<OutT>& A, int64_t slot,
 
 // silhouette_blend's per-slot opacity (shading.cpp:82-83): sigmoid(-dist / sigma) of the slot's signed squared
 // distance, recomputed from the face (fast divisions: the value is consumed within tolerance, not selected on)
-__device__ __forceinline__ double silhouette_prob(const double* v, double px, double py, double sigma) {
+// (inv_sigma = 1 / sigma: a product and a fast quotient instead of two IEEE divisions per slot)
+__device__ __forceinline__ double silhouette_prob(const double* v, double px, double py, double inv_sigma) {
   const FaceGeom g = make_face_geom(v);
   const V2 p{px, py};
   const DistResult dr = point_triangle_dist2<false>(p, g, p - g.a, p - g.b, p - g.c);
-  const double x = -dr.dist / sigma;
-  return 1.0 / (1.0 + exp(-x));
+  return fdiv(1.0, 1.0 + exp(dr.dist * inv_sigma));  // sigmoid(-dist / sigma)
 }
 
 // softmax_blend's clamped inverse depth (shading.cpp:136-137): (zfar - clamp(z, znear, zfar)) / (zfar - znear)
 __device__ __forceinline__ double blend_zinv(double z, const BlendArgs& bl) {
   const double zc = z < bl.znear ? bl.znear : (bl.zfar < z ? bl.zfar : z);  // std::clamp
-  return (bl.zfar - zc) / (bl.zfar - bl.znear);
+  return (bl.zfar - zc) * bl.inv_zr;
 }
 
 // one occupied slot of the softmax render: interpolate_face_attributes of the vertex colours with the slot's
@@ -671,8 +671,7 @@ __device__ __forceinline__ void softmax_slot(const FineArgs<OutT>& A, const doub
     c[1] += r.bary[i] * __ldg(a + 1);
     c[2] += r.bary[i] * __ldg(a + 2);
   }
-  const double x = -r.dist / A.blend.sigma;
-  prob = 1.0 / (1.0 + exp(-x));
+  prob = fdiv(1.0, 1.0 + exp(r.dist * A.blend.inv_sigma));  // sigmoid(-dists / sigma)
 }
 
 // Insert (zc, f) into pixel p's sorted list (column p of [K][32]) in shared memory: shifting loop.
@@ -1105,6 +1104,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
         for (int t = 0; t < 9; ++t) vnext[t] = __ldg(A.fv + 9 * (int64_t)fnext + t);
       }
       double keep = 1.0;  // silhouette mode: prod over occupied slots of (1 - prob)
+      const double inv_sigma = kMode == 1 ? 1.0 / A.sigma : 0.0;
       // softmax mode (shading.cpp:123-160): zinv_max over the occupied slots from the exact depths in the list
       double zinv_max = -1.0, wsum = 0.0, acc[3] = {0.0, 0.0, 0.0};
       bool any = false;
@@ -1128,14 +1128,14 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_fine(FineArgs<OutT> A) {
         }
         if constexpr (kMode == 1) {
           if (A.p2f) A.p2f[slot0 + s] = f != INT_MAX ? (int64_t)f : -1;
-          if (f != INT_MAX) keep *= 1.0 - silhouette_prob(v, px, py, A.sigma);
+          if (f != INT_MAX) keep *= 1.0 - silhouette_prob(v, px, py, inv_sigma);
         } else if constexpr (kMode == 2) {
           if (A.p2f) A.p2f[slot0 + s] = f != INT_MAX ? (int64_t)f : -1;
           if (f != INT_MAX) {
             double c[3], prob;
             softmax_slot(A, v, f, px, py, c, prob);
             const double zi = blend_zinv(ws.tz[ws.li<(KMAX == 0)>(s, lane)], A.blend);
-            const double w = prob * exp((zi - zinv_max) / A.blend.gamma);
+            const double w = prob * exp((zi - zinv_max) * A.blend.inv_gamma);
             wsum += w;
             acc[0] += c[0] * w;  // Vec3 += Vec3 * double
             acc[1] += c[1] * w;

@@ -18,6 +18,9 @@ struct BlendArgs {
   double sigma = 1e-4, gamma = 1e-4;    // BlendParams (shading.hpp:13-17)
   double background[3] = {0.0, 0.0, 0.0};
   double znear = 0.1, zfar = 100.0;     // Camera.znear / zfar
+  // 1 / sigma, 1 / gamma, 1 / (zfar - znear), computed once on the host: the render's per-slot blend values are
+  // products with these instead of IEEE divisions (tolerance values, never selected on)
+  double inv_sigma = 1e4, inv_gamma = 1e4, inv_zr = 1.0 / 99.9;
 };
 
 // Unsigned 32-bit division by a run-time invariant divisor with one multiply-high (Granlund & Montgomery,
