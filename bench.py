@@ -463,13 +463,22 @@ def main():
     from paper_2007_08501_b200 import (KernelTimer, launch_count, rasterize_meshes, rasterize_meshes_backward,
                                        workspace_bytes)
 
+    # DR_BENCH_SHARED_GPU=1 (tests only): ranks share the visible GPUs (local rank mod device count) over gloo and
+    # skip the NCCL gather (NCCL refuses two ranks on one device), so the N > 1 code path (plan, global ranges,
+    # max-over-ranks timing, the JSON line) runs on a one-GPU box; its timings are not scaling numbers
+    shared_gpu = os.environ.get("DR_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     # mesh sharding (include/dr_shard.h): every rank holds the whole packed face_verts and rasterizes ITS meshes
     # (LPT by face count) through their GLOBAL face ranges: global face ids, its own rows of grad_face_verts, no
@@ -508,7 +517,7 @@ def main():
     n_groups = max(1, min(args.gather_groups, int(plan.local_index.max()) + 1 if N_all else 1))
     gsize = -(-(int(plan.local_index.max()) + 1) // n_groups) if N_all else 1
     glob = None
-    if world > 1:
+    if world > 1 and not shared_gpu:
         from paper_2007_08501_b200.shard import NcclGather
 
         gather = NcclGather(rank, world)
@@ -669,7 +678,7 @@ def main():
                           "blur_radius": c["blur"], "bin_size": c["bin_size"], "parallelism": f"mesh-shard{world}",
                           "l2": "inputs+outputs (GBs) exceed the 126 MB L2; no flush"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "like_for_like": like,
-               "gather_to_root": bool(args.gather) and world > 1, "gather_mode": other, "other_configs": others,
+               "gather_to_root": headline_gather, "gather_mode": other, "other_configs": others,
                "gpu_launches": int(launches),
                "clocks": clk.summary()}
         print(json.dumps(out))
