@@ -774,7 +774,11 @@ __device__ __forceinline__ double blend_zinv_b(double z, const BlendArgs& bl, do
   return (bl.zfar - zc) * inv_zr;
 }
 
+// one instantiation per (perspective_correct, clip_barycentric_coords), as K3: both the slot re-evaluation and the K3
+// chain carry only their own branch (the kernel is instruction-cache bound)
+template <int kPC, int kCL>
 __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArgs A) {
+  constexpr bool persp = kPC == 1, clip = kCL == 1;
   extern __shared__ double soft_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
@@ -833,7 +837,7 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
         for (int t = 0; t < 9; ++t) v[t] = __ldg(A.fv + 9 * (int64_t)f + t);
         const FaceGeom g = make_face_geom(v);
         PixelFaceResult r;
-        eval_pixel_face<true, false>(p, g, A.blur, A.znear, A.persp, A.clip, r);
+        eval_pixel_face<true, false>(p, g, A.blur, A.znear, persp, clip, r);
         bool clamped;
         zi = blend_zinv_b(r.z, A.blend, inv_zr, clamped);
         if (argmax < 0) {  // the first occupied slot (see above)
@@ -918,7 +922,7 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
 #pragma unroll
         for (int t = 0; t < 9; ++t) in.v[t] = __ldg(A.fv + 9 * (int64_t)fid + t);
         double wh[3];
-        slot_backward<double, true>(BA, p, fid, in, g, wh);  // the slot's clamped barycentrics come back in wh
+        slot_backward<double, true, kPC, kCL>(BA, p, fid, in, g, wh);  // the slot's clamped barycentrics come back in wh
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           gc[3 * q + 0] = wh[q] * d_col[0];
@@ -966,7 +970,9 @@ __host__ __device__ __forceinline__ size_t softq_warp_bytes(int K) {
   return n * (6 * sizeof(double) + sizeof(int32_t) + sizeof(uint16_t)) + 32 * 5 * sizeof(double) + 16;
 }
 
+template <int kPC, int kCL>
 __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
+  constexpr bool persp = kPC == 1, clip = kCL == 1;
   // as k_softmax_backward: products with reciprocals instead of the blend's divisions (tolerance values)
   const double inv_sigma = 1.0 / A.blend.sigma, inv_gamma = 1.0 / A.blend.gamma,
                inv_zr = 1.0 / (A.blend.zfar - A.blend.znear);
@@ -1047,7 +1053,7 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
           const V2 p{PXY[2 * pl], PXY[2 * pl + 1]};
           const FaceGeom g = make_face_geom(v);
           PixelFaceResult r;
-          eval_pixel_face<true, false>(p, g, A.blur, A.znear, A.persp, A.clip, r);
+          eval_pixel_face<true, false>(p, g, A.blur, A.znear, persp, clip, r);
           bool clamped;
           double zi = blend_zinv_b(r.z, A.blend, inv_zr, clamped);
           double c[3] = {0.0, 0.0, 0.0};
@@ -1151,7 +1157,7 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
 #pragma unroll
         for (int u = 0; u < 9; ++u) in.v[u] = __ldg(A.fv + 9 * (int64_t)fid + u);
         double g[9], wh[3];
-        slot_backward<double, true>(BA, p, fid, in, g, wh);
+        slot_backward<double, true, kPC, kCL>(BA, p, fid, in, g, wh);
 #pragma unroll
         for (int k = 0; k < 9; ++k) gg[k] = g[k];
 #pragma unroll
@@ -1178,48 +1184,52 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
   }
 }
 
-cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
-  if (A.npix <= 0) return cudaSuccess;
-  if (A.K > kSoftMaxK) return cudaErrorInvalidConfiguration;
+template <int kPC, int kCL>
+static cudaError_t launch_softmax_backward_t(const SoftBwdArgs& A, cudaStream_t st) {
   // measured (C4 K=8 / C5 K=50): per-pixel kernel 10.9 / 39.1 ms, slot-compacted 15.1 / 16.1 ms — the
   // compaction pays once a pixel's K slots are unevenly filled (large K)
-  auto go_q = [&](auto kern, const SoftBwdArgs& args) -> cudaError_t {
-    const size_t smem = softq_warp_bytes(args.K);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // (a two-kernel form for K <= 16, coefficients through an [S][3] scratch, measured 11.6 vs 10.9 ms per-pixel)
+  if (A.K > 16) {
+    auto kern = k_softmax_backward_q<kPC, kCL>;
+    const size_t smem = softq_warp_bytes(A.K);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = (int64_t)sms * per_sm;
-    const int P = softq_pixels(args.K);
-    const int64_t need = (args.npix + P - 1) / P;
+    const int P = softq_pixels(A.K);
+    const int64_t need = (A.npix + P - 1) / P;
     if (blocks > need) blocks = need;
-    kern<<<(unsigned)blocks, 32, smem, st>>>(args);
+    kern<<<(unsigned)blocks, 32, smem, st>>>(A);
     return cudaGetLastError();
-  };
-  // (a two-kernel form for K <= 16, coefficients through an [S][3] scratch, measured 11.6 vs 10.9 ms per-pixel)
-  if (A.K > 16) return go_q(k_softmax_backward_q, A);
+  }
+  auto kern = k_softmax_backward<kPC, kCL>;
   const size_t per_warp = ((size_t)A.K * 32 * 6 + (size_t)A.K * 16) * sizeof(double);
   const int warps = (int)std::min<size_t>(kSoftThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));
   const size_t smem = per_warp * warps;
-  cudaError_t e = cudaFuncSetAttribute(k_softmax_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(smem, 48 * 1024));
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_softmax_backward, warps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t blocks = (int64_t)sms * per_sm;
   const int64_t need = (A.npix + warps * 32 - 1) / (warps * 32);
   if (blocks > need) blocks = need;
-  k_softmax_backward<<<(unsigned)blocks, warps * 32, smem, st>>>(A);
+  kern<<<(unsigned)blocks, warps * 32, smem, st>>>(A);
   return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
+  if (A.npix <= 0) return cudaSuccess;
+  if (A.K > kSoftMaxK) return cudaErrorInvalidConfiguration;
+  if (A.persp) return A.clip ? launch_softmax_backward_t<1, 1>(A, st) : launch_softmax_backward_t<1, 0>(A, st);
+  return A.clip ? launch_softmax_backward_t<0, 1>(A, st) : launch_softmax_backward_t<0, 0>(A, st);
 }
 
 template <typename InT>
