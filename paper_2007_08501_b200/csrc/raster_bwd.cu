@@ -938,13 +938,17 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
         gg[9 + k] = gc[k];
       }
       if (reduce_by_face<18>(fid, lane, gg)) {
+        // the face's vertex ids (L1) before the face_verts atomics, so those cover the load's latency
+        int64_t vi[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) vi[q] = __ldg(A.blend.faces + 3 * (int64_t)fid + q);
         double* out = A.grad + 9 * (int64_t)fid;
 #pragma unroll
         for (int k = 0; k < 9; ++k)
           if (gg[k] != 0.0) atomicAdd(out + k, gg[k]);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          double* oc = A.grad_colors + 3 * A.blend.faces[3 * (int64_t)fid + q];
+          double* oc = A.grad_colors + 3 * vi[q];
           for (int d = 0; d < 3; ++d)
             if (gg[9 + 3 * q + d] != 0.0) atomicAdd(oc + d, gg[9 + 3 * q + d]);
         }
@@ -1168,13 +1172,17 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
         }
       }
       if (reduce_by_face<18>(fid, lane, gg)) {
+        // the face's vertex ids (L1) before the face_verts atomics, so those cover the load's latency
+        int64_t vi[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) vi[q] = __ldg(A.blend.faces + 3 * (int64_t)fid + q);
         double* out = A.grad + 9 * (int64_t)fid;
 #pragma unroll
         for (int k = 0; k < 9; ++k)
           if (gg[k] != 0.0) atomicAdd(out + k, gg[k]);
 #pragma unroll
         for (int qq = 0; qq < 3; ++qq) {
-          double* oc = A.grad_colors + 3 * A.blend.faces[3 * (int64_t)fid + qq];
+          double* oc = A.grad_colors + 3 * vi[qq];
           for (int d = 0; d < 3; ++d)
             if (gg[9 + 3 * qq + d] != 0.0) atomicAdd(oc + d, gg[9 + 3 * qq + d]);
         }
