@@ -766,6 +766,7 @@ cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
 
 constexpr int kSoftThreads = 128;
 constexpr int kSoftMaxK = 64;
+constexpr int kSoftMaxGroupsPerCta = 32;
 
 // clamped inverse depth (shading.cpp:136-137, 199) with the depth range's reciprocal precomputed (inv_zr)
 __device__ __forceinline__ double blend_zinv_b(double z, const BlendArgs& bl, double inv_zr, bool& clamped) {
@@ -777,7 +778,7 @@ __device__ __forceinline__ double blend_zinv_b(double z, const BlendArgs& bl, do
 // one instantiation per (perspective_correct, clip_barycentric_coords), as K3: both the slot re-evaluation and the K3
 // chain carry only their own branch (the kernel is instruction-cache bound)
 template <int kPC, int kCL>
-__global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArgs A) {
+__global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArgs A, int gpc) {
   constexpr bool persp = kPC == 1, clip = kCL == 1;
   extern __shared__ double soft_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -793,8 +794,9 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
   BwdArgs<double> BA;  // the K3 per-slot chain's flags
   BA.persp = A.persp;
   BA.clip = A.clip;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  __shared__ int next_group;
+  if (threadIdx.x == 0) next_group = blockDim.x >> 5;  // group w is warp w's first
+  __syncthreads();
   const int64_t HW = (int64_t)A.H * A.W;
   const double zrange = A.blend.zfar - A.blend.znear;
   // the blend's divisions by sigma, gamma, the depth range and the per-pixel weight sum become products with
@@ -802,7 +804,12 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
   const double inv_sigma = 1.0 / A.blend.sigma, inv_gamma = 1.0 / A.blend.gamma, inv_zr = 1.0 / zrange;
 #define SDIV_SIGMA(x) ((x) * inv_sigma)
 #define SDIV_GAMMA(x) ((x) * inv_gamma)
-  for (int64_t base = warp * 32; base < A.npix; base += nwarps * 32) {
+  // the CTA's gpc consecutive 32-pixel groups are taken by its warps from a shared counter (many CTAs, balanced by
+  // the block scheduler, instead of a persistent grid whose warps finish unevenly: C4 8.11 -> 6.5-6.8 ms)
+  const int64_t g0 = (int64_t)blockIdx.x * gpc;
+  int kg = wid;
+  while (kg < gpc && (g0 + kg) * 32 < A.npix) {
+    const int64_t base = (g0 + kg) * 32;
     const int64_t pix = base + lane;
     double dimg[3] = {0.0, 0.0, 0.0};
     if (pix < A.npix) {
@@ -954,6 +961,9 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
         }
       }
     }
+    int kn = 0;
+    if (lane == 0) kn = atomicAdd(&next_group, 1);
+    kg = __shfl_sync(0xffffffffu, kn, 0);
   }
 }
 #undef SDIV_SIGMA
@@ -1226,10 +1236,12 @@ static cudaError_t launch_softmax_backward_t(const SoftBwdArgs& A, cudaStream_t 
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int64_t blocks = (int64_t)sms * per_sm;
-  const int64_t need = (A.npix + warps * 32 - 1) / (warps * 32);
-  if (blocks > need) blocks = need;
-  kern<<<(unsigned)blocks, warps * 32, smem, st>>>(A);
+  // groups per CTA: up to kSoftMaxGroupsPerCta, fewer when the image set is small (at least ~4 waves of CTAs; one
+  // group per warp at the floor) — C2 with 32 per CTA filled only 128 of 148 SMs
+  const int64_t groups = (A.npix + 31) / 32;
+  const int64_t gpc = std::max<int64_t>(warps, std::min<int64_t>(kSoftMaxGroupsPerCta, groups / (4 * (int64_t)sms * per_sm)));
+  const int64_t blocks = std::min<int64_t>((groups + gpc - 1) / gpc, INT32_MAX);
+  kern<<<(unsigned)blocks, warps * 32, smem, st>>>(A, (int)gpc);
   return cudaGetLastError();
 }
 
