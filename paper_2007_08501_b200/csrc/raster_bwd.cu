@@ -229,7 +229,7 @@ __device__ __forceinline__ void backward_batch(const BwdArgs<InT>& A, V2 p, int3
 // bary / cotangents loaded before the current step computes.
 constexpr int kPixTab = 2048;  // pixel-centre tables in shared memory when H + W fits
 
-constexpr int kBwdChunksPerCta = 32;
+constexpr int kBwdMaxChunksPerCta = 32;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -275,7 +275,7 @@ __device__ __forceinline__ void backward_chunk(const BwdArgs<InT>& A, int64_t c0
   }
 }
 
-// CTA = kBwdChunksPerCta consecutive chunks; its warps take chunks from a shared counter (so they finish
+// CTA = A.cpc consecutive chunks; its warps take chunks from a shared counter (so they finish
 // together and the CTA's registers are released without idle warps holding them). While a warp computes chunk
 // c, the pix_to_face words of its next chunk stream into shared memory with cp.async (no registers held);
 // the chunk is then compacted (occupied slots -> queue of 16-bit offsets + face ids) straight from shared memory.
@@ -294,12 +294,12 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_backward(BwdArgs
       pix_tab[t] = t < A.W ? pixel_x(A.W, t) : pixel_y(A.H, t - A.W);
   __syncthreads();
   constexpr int kSteps = kBwdChunk / 32;
-  // chunk k of this CTA starts at slot chunk0(k); valid while k < kBwdChunksPerCta and it starts before S
+  // chunk k of this CTA starts at slot chunk0(k); valid while k < A.cpc and it starts before S
   // (only k is carried across the chunk's compute: everything else is recomputed, to stay spill-free)
   auto chunk0 = [&](int k) {
-    return ((int64_t)blockIdx.x * kBwdChunksPerCta + k) * kBwdChunk;
+    return ((int64_t)blockIdx.x * A.cpc + k) * kBwdChunk;
   };
-  auto valid = [&](int k) { return k < kBwdChunksPerCta && chunk0(k) < A.S; };
+  auto valid = [&](int k) { return k < A.cpc && chunk0(k) < A.S; };
   auto issue = [&](int k) {  // start the copy of chunk k's pix_to_face words (slots past S are not copied)
     const int lane = threadIdx.x & 31;
     const int64_t c0 = chunk0(k);
@@ -1255,14 +1255,22 @@ cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st) {
 template <typename InT>
 static cudaError_t launch_backward_t(const BwdArgs<InT>& A, cudaStream_t st) {
   if (A.S <= 0) return cudaSuccess;
-  // many CTAs of kBwdChunksPerCta chunks instead of one persistent wave: the block scheduler then balances the
+  // many CTAs of up to kBwdMaxChunksPerCta chunks instead of one persistent wave: the block scheduler then balances the
   // uneven per-chunk work (occupied-slot density varies across the image); a single wave measured 10.8 of 16
   // achievable warps per SM on C4
-  const int64_t per_cta = (int64_t)kBwdChunk * kBwdChunksPerCta;
-  const int64_t blocks = std::min<int64_t>((A.S + per_cta - 1) / per_cta, INT32_MAX);
+  // chunks per CTA: 32 for the large configs (C4: 16 per CTA 2.28 ms, 8 2.58 vs 2.25), fewer once that leaves less
+  // than ~2 waves of CTAs (C2, 2,048 chunks: 32 per CTA filled 64 of 148 SMs, 0.155 ms; 8 per CTA 0.050)
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nchunks = (A.S + kBwdChunk - 1) / kBwdChunk;
+  BwdArgs<InT> B = A;
+  B.cpc = (int)std::max<int64_t>(kBwdThreads / 32,  // at least one chunk per warp
+                                 std::min<int64_t>(kBwdMaxChunksPerCta, nchunks / (2 * (int64_t)sms * kBwdMinBlocks)));
+  const int64_t blocks = std::min<int64_t>((nchunks + B.cpc - 1) / B.cpc, INT32_MAX);
   // one instantiation per (perspective_correct, clip_barycentric_coords)
   auto go = [&](auto kern) {
-    kern<<<(unsigned)blocks, kBwdThreads, 0, st>>>(A);
+    kern<<<(unsigned)blocks, kBwdThreads, 0, st>>>(B);
     return cudaGetLastError();
   };
   if (A.persp) return A.clip ? go(k_backward<InT, 1, 1>) : go(k_backward<InT, 1, 0>);

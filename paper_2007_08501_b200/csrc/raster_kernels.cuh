@@ -89,6 +89,7 @@ struct BwdArgs {
   int H, W, K;
   bool persp, clip;
   FastDivU32 divK, divW;  // slot -> pixel -> (i, j) without integer division instructions
+  int cpc = 32;           // K3: 512-slot chunks per CTA (set by the launcher from the slot count)
 };
 
 // fused silhouette_blend_backward + rasterize_backward (shading.cpp:93-121, MR:329-403 with d_zbuf = d_bary = 0)
