@@ -150,7 +150,7 @@ def _ncu_summaries():
 
     def key(path):
         nums = [int(x) for x in re.findall(r"\d+", os.path.relpath(path, ROOT))]
-        return nums
+        return nums, os.path.basename(path)  # same round: the later capture tag (r2j < r2l)
 
     return sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_*_summary.json")), key=key, reverse=True)
 
@@ -517,10 +517,22 @@ def main():
     n_groups = max(1, min(args.gather_groups, int(plan.local_index.max()) + 1 if N_all else 1))
     gsize = -(-(int(plan.local_index.max()) + 1) // n_groups) if N_all else 1
     glob = None
+    gather_error = None
     if world > 1 and not shared_gpu:
         from paper_2007_08501_b200.shard import NcclGather
 
-        gather = NcclGather(rank, world)
+        # the gather is an extra leg: if its communicator cannot be built on some rank, every rank drops it (agreed
+        # with an all_reduce) and the compute-only line is still printed, with the reason
+        try:
+            gather = NcclGather(rank, world)
+        except Exception as ex:  # noqa: BLE001 - reported in the JSON line
+            gather, gather_error = None, f"{type(ex).__name__}: {ex}"[:300]
+        ok = torch.tensor([1 if gather is not None else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and gather is not None:
+            gather.close()
+            gather, gather_error = None, "the gather communicator failed on another rank"
+    if gather is not None:
         comm_st = torch.cuda.Stream(device=dev)
         if rank == 0:
             glob = {"pix_to_face": torch.empty((N_all, H, W, K), dtype=torch.int64, device=dev),
@@ -679,6 +691,7 @@ def main():
                           "l2": "inputs+outputs (GBs) exceed the 126 MB L2; no flush"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "like_for_like": like,
                "gather_to_root": headline_gather, "gather_mode": other, "other_configs": others,
+               **({"gather_error": gather_error} if gather_error else {}),
                "gpu_launches": int(launches),
                "clocks": clk.summary()}
         print(json.dumps(out))
