@@ -43,7 +43,7 @@ struct dr_host_pipeline {
   double* grad = nullptr;
   void* ws = nullptr;
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
-  std::vector<cudaEvent_t> ev;  // per group: in, fwd, out, d2h
+  std::vector<cudaEvent_t> ev;  // per group: in, fwd, out, d2h, fv_in
   cudaEvent_t ev_start = nullptr, ev_end[3] = {nullptr, nullptr, nullptr};
 };
 
@@ -171,7 +171,7 @@ int dr_host_pipeline_create(const int64_t* host_first, const int64_t* host_num, 
   if (e == cudaSuccess) e = cudaMemcpy(p->d_num, host_num, sizeof(int64_t) * N, cudaMemcpyHostToDevice);
   for (cudaStream_t* st : {&p->h2d, &p->comp, &p->d2h})
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
-  p->ev.assign(4 * p->groups.size(), nullptr);
+  p->ev.assign(5 * p->groups.size(), nullptr);
   for (cudaEvent_t& ev : p->ev)
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming);
@@ -212,22 +212,24 @@ int dr_host_pipeline_run(dr_host_pipeline_t p, const double* face_verts, int64_t
     const int64_t g0 = p->groups[gi].first, g1 = p->groups[gi].second, n = g1 - g0;
     const int64_t lo = p->first[(size_t)g0], hi = p->first[(size_t)(g1 - 1)] + p->num[(size_t)(g1 - 1)];
     const int64_t s0 = g0 * HWK, ns = n * HWK;
-    cudaEvent_t ev_in = p->ev[4 * gi], ev_fwd = p->ev[4 * gi + 1], ev_out = p->ev[4 * gi + 2],
-                ev_d2h = p->ev[4 * gi + 3];
+    cudaEvent_t ev_in = p->ev[5 * gi], ev_fwd = p->ev[5 * gi + 1], ev_out = p->ev[5 * gi + 2],
+                ev_d2h = p->ev[5 * gi + 3], ev_fv = p->ev[5 * gi + 4];
     if (p->lookahead > 0 && gi >= (size_t)p->lookahead) {
-      e = cudaStreamWaitEvent(p->h2d, p->ev[4 * (gi - p->lookahead) + 3], 0);
+      e = cudaStreamWaitEvent(p->h2d, p->ev[5 * (gi - p->lookahead) + 3], 0);
       if (e != cudaSuccess) return cuda_err(e, "lookahead");
     }
     // h2d
     if (hi > lo) e = cudaMemcpyAsync(p->fv + 9 * lo, face_verts + 9 * lo, sizeof(double) * 9 * (hi - lo),
                                      cudaMemcpyHostToDevice, p->h2d);
+    // the forward needs only the face_verts rows: it starts (and its fragments leave) while the cotangents arrive
+    if (e == cudaSuccess) e = cudaEventRecord(ev_fv, p->h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->comp, ev_fv, 0);
     if (p->backward) {
       if (e == cudaSuccess) e = cudaMemcpyAsync(p->dz + s0, grad_zbuf + s0, sizeof(float) * ns, cudaMemcpyHostToDevice, p->h2d);
       if (e == cudaSuccess) e = cudaMemcpyAsync(p->db + 3 * s0, grad_bary + 3 * s0, sizeof(float) * 3 * ns, cudaMemcpyHostToDevice, p->h2d);
       if (e == cudaSuccess) e = cudaMemcpyAsync(p->dd + s0, grad_dists + s0, sizeof(float) * ns, cudaMemcpyHostToDevice, p->h2d);
     }
     if (e == cudaSuccess) e = cudaEventRecord(ev_in, p->h2d);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->comp, ev_in, 0);
     if (e != cudaSuccess) return cuda_err(e, "h2d");
     // comp
     int rc = dr_rasterize_meshes_fwd_hr(p->fv, p->d_first + g0, p->d_num + g0, n, p->F, &p->s, p->p2f + s0,
@@ -238,6 +240,8 @@ int dr_host_pipeline_run(dr_host_pipeline_t p, const double* face_verts, int64_t
     e = cudaEventRecord(ev_fwd, p->comp);
     if (e != cudaSuccess) return cuda_err(e, "forward event");
     if (p->backward) {
+      e = cudaStreamWaitEvent(p->comp, ev_in, 0);  // the group's cotangents
+      if (e != cudaSuccess) return cuda_err(e, "cotangent wait");
       rc = dr_rasterize_meshes_bwd_hr(p->fv, p->d_first + g0, p->d_num + g0, n, p->F, &p->s, p->p2f + s0,
                                       p->bary + 3 * s0, p->dz + s0, p->db + 3 * s0, p->dd + s0, p->grad,
                                       reinterpret_cast<dr_stream_t>(p->comp), p->first.data() + g0,
