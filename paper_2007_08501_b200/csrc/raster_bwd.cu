@@ -535,8 +535,12 @@ __global__ void __launch_bounds__(kSilThreads) k_silhouette_backward(SilBwdArgs 
 constexpr int kSilQMaxK = 64;
 constexpr int kSilQWarps = 1;  // one-warp CTAs: 14 resident per SM by shared memory (C4: 4 warps 3.65 ms, 2 3.11, 1 2.87)
 
-// pixels per chunk: 32, or fewer for large K so a chunk stays <= 512 slots
-__host__ __device__ __forceinline__ int silq_pixels(int K) { return K >= 512 ? 1 : min(32, 512 / K); }
+// chunk size: at most 256 slots and 28 pixels (shared memory per warp sets the resident warps: measured C4 (K=8)
+// 28 px 2.54 ms vs 32 px 2.73, 24 px 2.60, 16 px 2.78; C5 (K=50) 5 px 2.80 vs 10 px 3.55, 3 px 2.98)
+constexpr int kSilQSlots = 256, kSilQMaxP = 28;
+__host__ __device__ __forceinline__ int silq_pixels(int K) {
+  return K >= kSilQSlots ? 1 : min(kSilQMaxP, kSilQSlots / K);
+}
 __host__ __device__ __forceinline__ size_t silq_warp_bytes(int K) {
   const size_t n = (size_t)silq_pixels(K) * K;
   return n * (5 * sizeof(double) + sizeof(int64_t) + sizeof(int32_t) + sizeof(int32_t) + sizeof(uint16_t)) +
@@ -708,7 +712,7 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
 
 cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
-  if (A.K <= kSilQMaxK) {  // (any K: chunks shrink to 512 / K pixels)
+  if (A.K <= kSilQMaxK) {  // (any K: chunks shrink to kSilQSlots / K pixels)
     const size_t smem = (size_t)kSilQWarps * silq_warp_bytes(A.K);
     cudaError_t e = cudaFuncSetAttribute(k_silhouette_backward_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
@@ -970,13 +974,14 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
 #undef SDIV_GAMMA
 #undef SDIV_WSUM
 
-// Slot-compacted variant: a warp takes P = min(32, 512 / K) consecutive pixels; their occupied slots are queued
+// Slot-compacted variant: a warp takes P = min(32, kSoftQSlots / K) consecutive pixels; their occupied slots are queued
 // and the two geometry-heavy passes run lane-per-slot, 32 occupied slots per step:
 //   B  per slot: exact-sequence re-evaluation (fast divisions), inverse depth, opacity, interpolated colour
 //   C  per pixel (lane < P): zinv_max (the first occupied slot, see above), weights, the mean term, d_zinv_max,
 //      then per slot what = w / wsum, d_dists and d_zbuf (same operation order as the per-pixel kernel)
 //   D  per slot: d_bary from the vertex colours, the K3 chain, the colour cotangent, one 18-value reduce-by-face
-constexpr int kSoftQSlots = 512;
+// at most 320 slots per chunk (C5, K=50: 6 pixels 8.96 ms vs 10 pixels 9.46, 5 pixels 9.29, 7 pixels 9.11)
+constexpr int kSoftQSlots = 320;
 
 __host__ __device__ __forceinline__ int softq_pixels(int K) { return K >= kSoftQSlots ? 1 : min(32, kSoftQSlots / K); }
 __host__ __device__ __forceinline__ size_t softq_warp_bytes(int K) {
