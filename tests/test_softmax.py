@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 
 CASES = [("ico2", 48, 4, 2e-4, 1e-4, 1e-4), ("C2", 96, 8, 1e-4, 1e-4, 1e-4), ("C2g", 64, 8, 1e-4, 3e-4, 1e-2),
          ("ico2k1", 40, 1, 0.0, 1e-4, 1e-4), ("C2k20", 48, 20, 5e-4, 2e-4, 1e-3),
-         ("C2k64", 40, 64, 9.2e-4, 1e-4, 1e-4)]  # K > 16: the slot-compacted backward (8-pixel chunks at K=64)
+         ("C2k64", 40, 64, 9.2e-4, 1e-4, 1e-4),  # K > 16: the slot-compacted backward (5-pixel chunks at K=64)
+         ("C2big", 256, 8, 1e-4, 1e-4, 1e-4)]  # enough 32-pixel groups for > 1 group per warp of a backward CTA
 
 
 def _scene(name):
