@@ -788,13 +788,16 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = A.K;
   const size_t per_warp = (size_t)K * 32 * 6 + (size_t)K * 16;  // doubles
+  // one base pointer and K * 32 live across the loops; the arrays' bases are formed at each use (separate pointer
+  // registers had pushed ptxas into spilling one of them on the hot path)
   double* ZI = soft_smem + (size_t)wid * per_warp;  // [K][32] zinv (-1: empty slot; +2: clamped)
-  double* PR = ZI + K * 32;                         // [K][32] prob
-  double* WT = PR + K * 32;                         // [K][32] softmax weight
-  double* C0 = WT + K * 32;                         // [K][32] interpolated colour
-  double* C1 = C0 + K * 32;
-  double* C2 = C1 + K * 32;
-  int32_t* FID = reinterpret_cast<int32_t*>(C2 + K * 32);  // [32][K] the warp's pix_to_face block
+  const int K32 = K * 32;
+#define PR (ZI + K32)                                    // [K][32] prob
+#define WT (ZI + 2 * K32)                                // [K][32] softmax weight
+#define C0 (ZI + 3 * K32)                                // [K][32] interpolated colour
+#define C1 (ZI + 4 * K32)
+#define C2 (ZI + 5 * K32)
+#define FID (reinterpret_cast<int32_t*>(ZI + 6 * K32))  // [32][K] the warp's pix_to_face block
   BwdArgs<double> BA;  // the K3 per-slot chain's flags
   BA.persp = A.persp;
   BA.clip = A.clip;
@@ -802,18 +805,20 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
   if (threadIdx.x == 0) next_group = blockDim.x >> 5;  // group w is warp w's first
   __syncthreads();
   const int64_t HW = (int64_t)A.H * A.W;
-  const double zrange = A.blend.zfar - A.blend.znear;
   // the blend's divisions by sigma, gamma, the depth range and the per-pixel weight sum become products with
   // reciprocals (values compared within tolerance, never selected on: <= 2 ulp from the quotients; C4 10.7 -> 8.8 ms)
-  const double inv_sigma = 1.0 / A.blend.sigma, inv_gamma = 1.0 / A.blend.gamma, inv_zr = 1.0 / zrange;
+  // (the host's reciprocals, BlendArgs::inv_*: kernel-parameter operands, no registers held across the loop)
+#define inv_sigma (A.blend.inv_sigma)
+#define inv_gamma (A.blend.inv_gamma)
+#define inv_zr (A.blend.inv_zr)
 #define SDIV_SIGMA(x) ((x) * inv_sigma)
 #define SDIV_GAMMA(x) ((x) * inv_gamma)
   // the CTA's gpc consecutive 32-pixel groups are taken by its warps from a shared counter (many CTAs, balanced by
   // the block scheduler, instead of a persistent grid whose warps finish unevenly: C4 8.11 -> 6.5-6.8 ms)
-  const int64_t g0 = (int64_t)blockIdx.x * gpc;
+  const int g0 = (int)blockIdx.x * gpc;  // group indices fit 32 bits (the launcher caps the grid at INT32_MAX)
   int kg = wid;
-  while (kg < gpc && (g0 + kg) * 32 < A.npix) {
-    const int64_t base = (g0 + kg) * 32;
+  while (kg < gpc && (int64_t)(g0 + kg) * 32 < A.npix) {
+    const int64_t base = (int64_t)(g0 + kg) * 32;
     const int64_t pix = base + lane;
     double dimg[3] = {0.0, 0.0, 0.0};
     if (pix < A.npix) {
@@ -970,6 +975,15 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
     kg = __shfl_sync(0xffffffffu, kn, 0);
   }
 }
+#undef PR
+#undef WT
+#undef C0
+#undef C1
+#undef C2
+#undef FID
+#undef inv_sigma
+#undef inv_gamma
+#undef inv_zr
 #undef SDIV_SIGMA
 #undef SDIV_GAMMA
 #undef SDIV_WSUM
