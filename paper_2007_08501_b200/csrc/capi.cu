@@ -526,10 +526,10 @@ int points_fwd_impl(const double* pts, const int64_t* first, const int64_t* num,
       if (e != cudaSuccess) return cuda_fail(e, "zeroing point bin counts");
     }
     ProfScope ps(st, KN_BIN);
-    drb::launch_bin_faces(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, st);
+    drb::launch_bin_faces(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, st, /*smem_hist=*/true);
     drb::launch_scan_bins(counts, p.nbins_total, bin_off, st);
     drb::launch_fill_bins(ibbox, first, num, N, max_pts, p.bs, p.nbx, p.nby, counts, bin_off, cursor, p.pool, zkey,
-                          entries, st);
+                          entries, st, /*smem_hist=*/true);
   }
   const bool sorted = p.binned;
   if (sorted) {

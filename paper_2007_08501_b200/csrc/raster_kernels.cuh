@@ -195,11 +195,13 @@ __host__ __device__ __forceinline__ bool bin_fits(int64_t off, int cnt, int64_t 
   return off + cnt <= pool && (cap <= 0 || cnt <= cap);
 }
 void launch_bin_faces(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
-                      int bs, int nbx, int nby, int* counts, cudaStream_t st);  // count pass
+                      int bs, int nbx, int nby, int* counts, cudaStream_t st,
+                      bool smem_hist = false);  // count pass
 void launch_scan_bins(const int* counts, int64_t nbins_total, int64_t* off, cudaStream_t st);
 void launch_fill_bins(const int4* ibbox, const int64_t* first, const int64_t* num, int64_t N, int64_t max_faces,
                       int bs, int nbx, int nby, const int* counts, const int64_t* off, int* cursor, int64_t pool,
-                      const float* zkey, int4* entries, cudaStream_t st);
+                      const float* zkey, int4* entries, cudaStream_t st, bool smem_hist = false);
+// smem_hist: the CTA-level shared-memory histogram form (k_bin_faces_smem), for items in no spatial order (points)
 // The bins k_sort_bins depth-orders: every non-empty bin of at most kSortMaxBig entries that is read as a list.
 // The fine stages treat exactly these bins as sorted (the point stage reads their bucket map for its exit bound),
 // so the sort and both fine stages share this one predicate.
