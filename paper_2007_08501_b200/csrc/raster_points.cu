@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
   __shared__ double sx[kPtThreads], sy[kPtThreads], sz[kPtThreads];
   __shared__ int32_t sid[kPtThreads];
   __shared__ double s_kth[kPtThreads / 32];
+  __shared__ uint16_t s_wl[kPtThreads / 32][kPtThreads];  // per warp: staged points that can reach its two rows
   // per-pixel sorted (z, id) list: KMAX > 0 => registers (fully unrolled, +inf padded), else local memory
   constexpr int KL = KMAX > 0 ? KMAX : kPtMaxK;
   double lz[KL];
@@ -138,6 +139,9 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
     const int i = bi0 + (int)(threadIdx.x >> 4), j = bj0 + (int)(threadIdx.x & 15);
     const bool valid = i < bi1 && j < bj1;
     const double px = pixel_x(A.W, j), py = pixel_y(A.H, i);  // pixel_center_ndc (camera.cpp:100-102)
+    // the warp's two pixel rows (threads 16r .. 16r+15 hold row r of the block)
+    const int wi0 = bi0 + 2 * (int)(threadIdx.x >> 5);
+    const double wpy0 = pixel_y(A.H, wi0), wpy1 = pixel_y(A.H, wi0 + 1);
     // candidate points: the bin list, or the whole cloud (naive / spilled bin)
     const int64_t p0 = A.first[b], np = A.num[b];
     const int4* list = nullptr;
@@ -211,8 +215,30 @@ __global__ void __launch_bounds__(kPtThreads) k_points_fine(PointFineArgs<OutT> 
       }
       __syncthreads();
       const int m = (int)(nsrc - c0 < kPtThreads ? nsrc - c0 : kPtThreads);
+      // warp filter: a staged point can pass PR:145 at one of the warp's pixels only if its own y term alone does:
+      // the test's d2 = fl(fl(vx * vx) + fl(vy * vy)) >= fl(vy * vy) (rounding is monotone, vx * vx >= 0), and vy is
+      // computed here exactly as the test computes it. The warp then walks only those points (~1/4 of the batch
+      // for a radius of a pixel or two in a 16-row block) instead of all of them.
+      int wn = 0;
+      uint16_t* wl = s_wl[threadIdx.x >> 5];
+      {
+        const int lane = threadIdx.x & 31;
+        for (int q0 = 0; q0 < m; q0 += 32) {
+          const int q = q0 + lane;
+          bool keep = false;
+          if (q < m && sid[q] >= 0) {
+            const double vy0 = wpy0 - sy[q], vy1 = wpy1 - sy[q];
+            keep = vy0 * vy0 <= A.r2 || vy1 * vy1 <= A.r2;
+          }
+          const unsigned kb = __ballot_sync(0xffffffffu, keep);
+          if (keep) wl[wn + __popc(kb & ((1u << lane) - 1u))] = (uint16_t)q;
+          wn += __popc(kb);
+        }
+        __syncwarp();
+      }
       if (valid) {
-        for (int q = 0; q < m; ++q) {
+        for (int k = 0; k < wn; ++k) {
+          const int q = wl[k];
           const int32_t pid = sid[q];
           const double vx = px - sx[q], vy = py - sy[q];  // pix - pr.xy
           const double d2 = vx * vx + vy * vy;            // Vec2::norm2 (core.hpp:66)
