@@ -1384,10 +1384,24 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
     kern<<<(unsigned)(sms * per_sm), nw * 32, smem, st>>>(A);  // persistent: warps pull micro-tiles
     return cudaGetLastError();
   };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  // the fused consumers at K == 8 on the register path (the headline K): flags and K fixed at compile time too
+  auto consumer_k8 = [&](auto mode_c) -> cudaError_t {
+    constexpr int M = decltype(mode_c)::value;
+    auto f = [&](auto pc, auto cl) -> cudaError_t {
+      return go(k_fine<OutT, 8, 8, M, decltype(pc)::value, decltype(cl)::value, true>);
+    };
+    if (A.persp) return A.clip ? f(I1{}, I1{}) : f(I1{}, I0{});
+    return A.clip ? f(I0{}, I1{}) : f(I0{}, I0{});
+  };
   auto by_k = [&](auto nw_c) -> cudaError_t {
     constexpr int NW = decltype(nw_c)::value;
     // register-resident merge for small K, shared-memory shifting loop otherwise
     if (A.alpha) {  // fused silhouette: fp32 alpha, or fp64 for the fit loop (fit.py)
+      if constexpr (NW == 8) {
+        if (A.K == 8) return consumer_k8(std::integral_constant<int, 1>{});
+      }
       if (A.K == 1) return go(k_fine<OutT, NW, 1, 1>);
       if (A.K <= 4) return go(k_fine<OutT, NW, 4, 1>);
       if (A.K <= 8) return go(k_fine<OutT, NW, 8, 1>);
@@ -1395,6 +1409,9 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
     }
     if (A.image) {
       if constexpr (std::is_same<OutT, float>::value) {  // the fused softmax render writes an fp32 image only
+        if constexpr (NW == 8) {
+          if (A.K == 8) return consumer_k8(std::integral_constant<int, 2>{});
+        }
         if (A.K == 1) return go(k_fine<OutT, NW, 1, 2>);
         if (A.K <= 4) return go(k_fine<OutT, NW, 4, 2>);
         if (A.K <= 8) return go(k_fine<OutT, NW, 8, 2>);
@@ -1416,8 +1433,6 @@ static cudaError_t launch_fine_t(const FineArgs<OutT>& A, int nw, cudaStream_t s
       if (A.K <= 8) return go(k_fine<OutT, NW, 8, 0, PC, CL>);
       return go(k_fine<OutT, NW, 0, 0, PC, CL>);
     };
-    using I0 = std::integral_constant<int, 0>;
-    using I1 = std::integral_constant<int, 1>;
     if (A.persp) return A.clip ? by_flags(I1{}, I1{}) : by_flags(I1{}, I0{});
     return A.clip ? by_flags(I0{}, I1{}) : by_flags(I0{}, I0{});
   };
