@@ -781,12 +781,13 @@ __device__ __forceinline__ double blend_zinv_b(double z, const BlendArgs& bl, do
 
 // one instantiation per (perspective_correct, clip_barycentric_coords), as K3: both the slot re-evaluation and the K3
 // chain carry only their own branch (the kernel is instruction-cache bound)
-template <int kPC, int kCL>
+// kK: K fixed at compile time (8, the headline K: constant shared-memory offsets), or 0 = read from A
+template <int kPC, int kCL, int kK = 0>
 __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArgs A, int gpc) {
   constexpr bool persp = kPC == 1, clip = kCL == 1;
   extern __shared__ double soft_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int K = A.K;
+  const int K = kK ? kK : A.K;
   const size_t per_warp = (size_t)K * 32 * 6 + (size_t)K * 16;  // doubles
   // one base pointer and K * 32 live across the loops; the arrays' bases are formed at each use (separate pointer
   // registers had pushed ptxas into spilling one of them on the hot path)
@@ -843,6 +844,7 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
     double zinv_max = -1.0;
     int argmax = -1;
     bool any = false;
+#pragma unroll 1
     for (int s = 0; s < K; ++s) {
       const int32_t f = pix < A.npix ? row[s] : -1;
       double zi = -1.0;
@@ -905,6 +907,7 @@ __global__ void __launch_bounds__(kSoftThreads, 4) k_softmax_backward(SoftBwdArg
       d_zinv_max += SDIV_GAMMA(-d_w * w);
     }
     // pass 4: per-slot cotangents -> colours, barycentrics, the K3 chain
+#pragma unroll 1
     for (int s = 0; s < K; ++s) {
       const double zis = (pix < A.npix && any) ? ZI[s * 32 + lane] : -1.0;
       int32_t fid = -1;
@@ -1245,7 +1248,7 @@ static cudaError_t launch_softmax_backward_t(const SoftBwdArgs& A, cudaStream_t 
     kern<<<(unsigned)blocks, 32, smem, st>>>(A);
     return cudaGetLastError();
   }
-  auto kern = k_softmax_backward<kPC, kCL>;
+  auto kern = A.K == 8 ? k_softmax_backward<kPC, kCL, 8> : k_softmax_backward<kPC, kCL>;
   const size_t per_warp = ((size_t)A.K * 32 * 6 + (size_t)A.K * 16) * sizeof(double);
   const int warps = (int)std::min<size_t>(kSoftThreads / 32, std::max<size_t>(1, (size_t)(96 * 1024) / per_warp));
   const size_t smem = per_warp * warps;
