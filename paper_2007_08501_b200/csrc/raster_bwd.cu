@@ -552,12 +552,14 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 
+// kK: K fixed at compile time (8, the headline K: constant chunk layout and slot -> pixel divisions), 0 = from A
+template <int kK = 0>
 __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBwdArgs A) {
   // 1 / sigma once (products instead of per-slot divisions; the opacities are tolerance values)
   const double inv_sigma = 1.0 / A.sigma;
   extern __shared__ double silq_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int K = A.K;
+  const int K = kK ? kK : A.K;
   const int KS = K;  // per-pixel row stride (K + 1, conflict-free for the lane-per-pixel pass, measured slower)
   const int P = silq_pixels(K);
   const int n = P * KS;
@@ -714,19 +716,20 @@ cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
   if (A.npix <= 0) return cudaSuccess;
   if (A.K <= kSilQMaxK) {  // (any K: chunks shrink to kSilQSlots / K pixels)
     const size_t smem = (size_t)kSilQWarps * silq_warp_bytes(A.K);
-    cudaError_t e = cudaFuncSetAttribute(k_silhouette_backward_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = A.K == 8 ? k_silhouette_backward_q<8> : k_silhouette_backward_q<0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_silhouette_backward_q, kSilQWarps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSilQWarps * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = (int64_t)sms * per_sm;
     const int64_t need = (A.npix + (int64_t)kSilQWarps * silq_pixels(A.K) - 1) / ((int64_t)kSilQWarps * silq_pixels(A.K));
     if (blocks > need) blocks = need;
-    k_silhouette_backward_q<<<(unsigned)blocks, kSilQWarps * 32, smem, st>>>(A);
+    kern<<<(unsigned)blocks, kSilQWarps * 32, smem, st>>>(A);
     return cudaGetLastError();
   }
   const bool store = A.K <= kSilStoreMaxK;
