@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
         const int t = t0 + lane;
         const int tp = t;
         const int64_t f = t < nslots ? STG[t] : -1;
-        const bool occ = t < P * K && f >= 0 && f < A.F && ((act_mask >> (t / K)) & 1u);
+        const bool occ = t < P * K && f >= 0 && f < A.F && ((act_mask >> (kK ? t / kK : (int)A.divK.div((uint32_t)t))) & 1u);
         if (t < P * K) {
           FID[tp] = occ ? (int32_t)f : -1;
           PR[tp] = -1.0;
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(kSilQWarps * 32) k_silhouette_backward_q(SilBw
           for (int u = 0; u < 9; ++u) vn[u] = __ldg(A.fv + 9 * (int64_t)fn + u);
         }
         if (t >= 0) {
-          const int pl = t / KS;
+          const int pl = (kK ? t / kK : (int)A.divK.div((uint32_t)t));
           const V2 p{PXY[2 * pl], PXY[2 * pl + 1]};
           double dist, bt, sign;
           int be;
@@ -717,6 +717,8 @@ cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
   if (A.K <= kSilQMaxK) {  // (any K: chunks shrink to kSilQSlots / K pixels)
     const size_t smem = (size_t)kSilQWarps * silq_warp_bytes(A.K);
     auto kern = A.K == 8 ? k_silhouette_backward_q<8> : k_silhouette_backward_q<0>;
+    SilBwdArgs B = A;
+    B.divK = FastDivU32((uint32_t)A.K);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
@@ -729,7 +731,7 @@ cudaError_t launch_silhouette_backward(const SilBwdArgs& A, cudaStream_t st) {
     int64_t blocks = (int64_t)sms * per_sm;
     const int64_t need = (A.npix + (int64_t)kSilQWarps * silq_pixels(A.K) - 1) / ((int64_t)kSilQWarps * silq_pixels(A.K));
     if (blocks > need) blocks = need;
-    kern<<<(unsigned)blocks, kSilQWarps * 32, smem, st>>>(A);
+    kern<<<(unsigned)blocks, kSilQWarps * 32, smem, st>>>(B);
     return cudaGetLastError();
   }
   const bool store = A.K <= kSilStoreMaxK;
@@ -1088,7 +1090,7 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
           for (int u = 0; u < 9; ++u) vn[u] = __ldg(A.fv + 9 * (int64_t)fn + u);
         }
         if (t >= 0) {
-          const int pl = t / KS;
+          const int pl = (int)A.divK.div((uint32_t)t);
           const V2 p{PXY[2 * pl], PXY[2 * pl + 1]};
           const FaceGeom g = make_face_geom(v);
           PixelFaceResult r;
@@ -1180,7 +1182,7 @@ __global__ void __launch_bounds__(32) k_softmax_backward_q(SoftBwdArgs A) {
       for (int k = 0; k < 18; ++k) gg[k] = 0.0;
       if (t >= 0) {
         fid = FID[t];
-        const int pl = t / KS;
+        const int pl = (int)A.divK.div((uint32_t)t);
         const V2 p{PXY[2 * pl], PXY[2 * pl + 1]};
         const double what = WT[t];
         const double d_col[3] = {DIM[3 * pl] * what, DIM[3 * pl + 1] * what, DIM[3 * pl + 2] * what};
@@ -1248,7 +1250,9 @@ static cudaError_t launch_softmax_backward_t(const SoftBwdArgs& A, cudaStream_t 
     const int P = softq_pixels(A.K);
     const int64_t need = (A.npix + P - 1) / P;
     if (blocks > need) blocks = need;
-    kern<<<(unsigned)blocks, 32, smem, st>>>(A);
+    SoftBwdArgs B = A;
+    B.divK = FastDivU32((uint32_t)A.K);
+    kern<<<(unsigned)blocks, 32, smem, st>>>(B);
     return cudaGetLastError();
   }
   auto kern = A.K == 8 ? k_softmax_backward<kPC, kCL, 8> : k_softmax_backward<kPC, kCL>;

@@ -103,6 +103,7 @@ struct SilBwdArgs {
   int64_t F;
   int H, W, K;
   double sigma;
+  FastDivU32 divK;  // slot -> pixel in the slot-compacted kernel (set by the launcher)
 };
 
 // point rasterizer (raster_points.cu)
@@ -151,6 +152,7 @@ struct SoftBwdArgs {
   bool persp, clip;
   double blur, znear;      // raster settings (exact re-evaluation of each slot)
   BlendArgs blend;
+  FastDivU32 divK;         // slot -> pixel in the slot-compacted kernel (set by the launcher)
 };
 cudaError_t launch_softmax_backward(const SoftBwdArgs& A, cudaStream_t st);
 
