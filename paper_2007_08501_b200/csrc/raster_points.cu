@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(256) k_point_setup(const double* __restrict__ 
 // P2: fine stage
 
 constexpr int kPtThreads = 256;  // one thread per pixel of a <= 16x16 block
+constexpr int kPtTab = 2048;     // backward pixel-centre table (W + H entries)
 
 __device__ __forceinline__ bool pt_less(double za, int32_t ia, double zb, int32_t ib) {  // PR:37
   return za != zb ? za < zb : ia < ib;
@@ -306,7 +307,16 @@ template <typename InT>
 __global__ void __launch_bounds__(256) k_points_backward(const double* __restrict__ pts, const int64_t* __restrict__ idx,
                                                          const InT* __restrict__ g_zbuf,
                                                          const InT* __restrict__ g_dists2, int64_t S, int64_t P, int H,
-                                                         int W, int K, double* __restrict__ grad) {
+                                                         int W, int K, double* __restrict__ grad, FastDivU32 divK,
+                                                         FastDivU32 divHW, FastDivU32 divW) {
+  // pixel centres from a shared table (pixel_x(W, j) for j < W, then pixel_y(H, i)) and slot -> (pixel, i, j) by
+  // precomputed reciprocals when the indices fit 32 bits: no 64-bit divisions and no fp64 division per slot
+  __shared__ double tab[kPtTab];
+  const bool use_tab = W + H <= kPtTab;
+  if (use_tab)
+    for (int t = threadIdx.x; t < W + H; t += blockDim.x) tab[t] = t < W ? pixel_x(W, t) : pixel_y(H, t - W);
+  __syncthreads();
+  const bool s32 = S <= 0xffffffffll;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < S; base += stride) {
@@ -317,12 +327,22 @@ __global__ void __launch_bounds__(256) k_points_backward(const double* __restric
       const int64_t p = idx[slot];
       if (p >= 0 && p < P) {
         pid = (int32_t)p;
-        const int64_t pix = slot / K;
-        const int rem = (int)(pix % ((int64_t)H * W));
-        const int i = rem / W, j = rem - (rem / W) * W;
+        int i, j;
+        if (s32) {
+          const uint32_t pix = divK.div((uint32_t)slot);
+          const uint32_t rem = pix - divHW.div(pix) * divHW.d;
+          i = (int)divW.div(rem);
+          j = (int)rem - i * W;
+        } else {
+          const int64_t pix = slot / K;
+          const int rem = (int)(pix % ((int64_t)H * W));
+          i = rem / W;
+          j = rem - i * W;
+        }
         const double gd = (double)g_dists2[slot];
-        g[0] = -2.0 * (pixel_x(W, j) - pts[3 * p]) * gd;      // d|pix - xy|^2 / dx
-        g[1] = -2.0 * (pixel_y(H, i) - pts[3 * p + 1]) * gd;
+        const double cx = use_tab ? tab[j] : pixel_x(W, j), cy = use_tab ? tab[W + i] : pixel_y(H, i);
+        g[0] = -2.0 * (cx - pts[3 * p]) * gd;      // d|pix - xy|^2 / dx
+        g[1] = -2.0 * (cy - pts[3 * p + 1]) * gd;
         g[2] = (double)g_zbuf[slot];                          // zbuf = z_view
       }
     }
@@ -390,7 +410,8 @@ static cudaError_t launch_points_backward_t(const double* pts, const int64_t* id
                                             cudaStream_t st) {
   if (S <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>((S + 255) / 256, 148 * 16);
-  k_points_backward<InT><<<grid, 256, 0, st>>>(pts, idx, gz, gd, S, P, H, W, K, grad);
+  k_points_backward<InT><<<grid, 256, 0, st>>>(pts, idx, gz, gd, S, P, H, W, K, grad, FastDivU32((uint32_t)K),
+                                                FastDivU32((uint32_t)((int64_t)H * W)), FastDivU32((uint32_t)W));
   return cudaGetLastError();
 }
 cudaError_t launch_points_backward(const double* pts, const int64_t* idx, const float* gz, const float* gd, int64_t S,
