@@ -410,8 +410,11 @@ static cudaError_t launch_points_backward_t(const double* pts, const int64_t* id
                                             cudaStream_t st) {
   if (S <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>((S + 255) / 256, 148 * 16);
-  k_points_backward<InT><<<grid, 256, 0, st>>>(pts, idx, gz, gd, S, P, H, W, K, grad, FastDivU32((uint32_t)K),
-                                                FastDivU32((uint32_t)((int64_t)H * W)), FastDivU32((uint32_t)W));
+  const bool s32 = S <= 0xffffffffll;  // the kernel's 32-bit path (then H * W < 2^32 as well)
+  k_points_backward<InT><<<grid, 256, 0, st>>>(pts, idx, gz, gd, S, P, H, W, K, grad,
+                                                s32 ? FastDivU32((uint32_t)K) : FastDivU32(),
+                                                s32 ? FastDivU32((uint32_t)((int64_t)H * W)) : FastDivU32(),
+                                                s32 ? FastDivU32((uint32_t)W) : FastDivU32());
   return cudaGetLastError();
 }
 cudaError_t launch_points_backward(const double* pts, const int64_t* idx, const float* gz, const float* gd, int64_t S,
